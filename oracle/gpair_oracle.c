@@ -1,0 +1,221 @@
+/*
+ * gpair_oracle.c -- fp64 CPU ORACLE for the GPAIR closed-form forward operator
+ * and its adjoint.  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+ * `--impl reference`) may load this library.  The product path
+ * (paper_2602_03893_b200/) never imports, links or executes anything under
+ * oracle/, and this file shares no code, header, table or constant generator
+ * with the CUDA path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, cited P:<line>):
+ *
+ *   Eq. 7, outgoing spherical wave of one Gaussian kernel:
+ *       p(r, t) = A/(2r) * d * exp(-d^2 / (2 sigma^2)),   d = r - v t
+ *   3-sigma truncation: "-3 sigma < d < 3 sigma"; k is a parameter,
+ *       strict inequality (reading R1).
+ *   Direct enumeration: "iterate over all source-detector pairs and
+ *       evaluate the contribution at each temporal sampling point where d
+ *       falls within the +-3 sigma range".
+ *   Superposition (Eq. 2): y_j[n] = sum_i A_i a_ijn.
+ *   Adjoint = exact transpose: g_i = sum_j sum_n a_ijn delta_j[n].
+ *
+ *   a_ijn = d * exp(-d^2/(2 sigma^2)) / (2 r_ij)   if |d| < k sigma, else 0,
+ *   r_ij  = || c_i - s_j ||,  t_n = t0 + n / f_s  (reading R3), d = r_ij - v t_n.
+ *
+ * Plain definition, no blocking or reordering: fp64 throughout, libm exp/sqrt,
+ * built with -O2 -fno-fast-math -ffp-contract=off.  Inputs are the fp32 values
+ * the GPU receives, promoted exactly to fp64.  Forward accumulates each y_j[n]
+ * in ascending kernel order i; adjoint accumulates each g_i in ascending j then
+ * ascending n.  OpenMP only parallelises over independent outputs (sensors for
+ * the forward, kernels for the adjoint), so results are bit-reproducible for
+ * any thread count.
+ *
+ * Candidate samples: n from floor(((r - k s)/v - t0) f_s) - 2 to
+ * ceil(((r + k s)/v - t0) f_s) + 2, clipped to [0, N_t); the membership test
+ * |d| < k sigma is applied literally to each candidate (record-edge clipping:
+ * reading R8).  Pairs with r_ij <= k sigma are rejected (reading R2: Eq. 7 is
+ * a far-field model) with return code ORACLE_ERR_GEOMETRY.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORACLE_OK 0
+#define ORACLE_ERR_INVALID 1
+#define ORACLE_ERR_GEOMETRY 2
+
+static int g_threads = 0; /* 0 = OpenMP default */
+
+void oracle_set_threads(int n) { g_threads = n; }
+
+int oracle_get_threads(void) {
+#ifdef _OPENMP
+    return g_threads > 0 ? g_threads : omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* Eq. 6: full pressure including the incoming term. */
+double oracle_pressure_full(double A, double r, double t, double v, double sigma) {
+    double a = r - v * t, b = r + v * t, s2 = 2.0 * sigma * sigma;
+    return A / (2.0 * r) * (a * exp(-(a * a) / s2) + b * exp(-(b * b) / s2));
+}
+
+/* Eq. 7 with the P:291 truncation |d| < k sigma. */
+double oracle_pressure_outgoing(double A, double r, double t, double v, double sigma, double k) {
+    double d = r - v * t;
+    if (!(fabs(d) < k * sigma)) return 0.0;
+    return A / (2.0 * r) * d * exp(-(d * d) / (2.0 * sigma * sigma));
+}
+
+/* Distance r_ij from the fp32 inputs promoted to fp64 (differences exact). */
+static double pair_distance(const float* centers, int64_t M, int64_t i,
+                            const float* sensors, int32_t Nd, int32_t j) {
+    double dx = (double)centers[i] - (double)sensors[j];
+    double dy = (double)centers[M + i] - (double)sensors[Nd + j];
+    double dz = (double)centers[2 * M + i] - (double)sensors[2 * Nd + j];
+    return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+/* Candidate sample range for one pair (generous; membership tested per n). */
+static void candidate_range(double r, double ks, double v, double fs, double t0,
+                            int32_t Nt, int64_t* n0, int64_t* n1) {
+    double lo = floor(((r - ks) / v - t0) * fs) - 2.0;
+    double hi = ceil(((r + ks) / v - t0) * fs) + 2.0;
+    if (lo < 0.0) lo = 0.0;
+    if (hi > (double)(Nt - 1)) hi = (double)(Nt - 1);
+    *n0 = (int64_t)lo;
+    *n1 = (int64_t)hi;
+}
+
+static int check_args(int64_t M, int32_t Nd, int32_t Nt, double sigma, double v,
+                      double fs, double k) {
+    if (M < 0 || Nd < 1 || Nt < 1) return ORACLE_ERR_INVALID;
+    if (!(sigma > 0.0) || !(v > 0.0) || !(fs > 0.0) || !(k > 0.0)) return ORACLE_ERR_INVALID;
+    return ORACLE_OK;
+}
+
+/*
+ * Forward: y[j_out][n] = sum_i amp[i] * a_ijn for the sensors listed in
+ * `rows` (n_rows entries; rows == NULL means all N_d sensors in order).
+ * centers: [3][M] SoA fp32 metres; sensors: [3][N_d] SoA fp32 metres;
+ * sigmas: optional per-kernel sigma (NULL -> sigma); y: [n_rows][N_t] fp64.
+ */
+int oracle_forward(int64_t M, const float* centers, const double* amp,
+                   double sigma, const double* sigmas,
+                   int32_t Nd, const float* sensors,
+                   double v, double fs, double t0, int32_t Nt, double k,
+                   const int32_t* rows, int32_t n_rows, double* y) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc) return rc;
+    if (rows == NULL) n_rows = Nd;
+    int err = ORACLE_OK;
+    int nth = oracle_get_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nth)
+    for (int32_t jo = 0; jo < n_rows; ++jo) {
+        int32_t j = rows ? rows[jo] : jo;
+        double* yj = y + (int64_t)jo * Nt;
+        for (int32_t n = 0; n < Nt; ++n) yj[n] = 0.0;
+        for (int64_t i = 0; i < M; ++i) {
+            double s = sigmas ? sigmas[i] : sigma;
+            double ks = k * s;
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            if (!(r > ks)) {
+#pragma omp atomic write
+                err = ORACLE_ERR_GEOMETRY;
+                continue;
+            }
+            int64_t n0, n1;
+            candidate_range(r, ks, v, fs, t0, Nt, &n0, &n1);
+            for (int64_t n = n0; n <= n1; ++n) {
+                double t = t0 + (double)n / fs;
+                double d = r - v * t;
+                if (fabs(d) < ks) {
+                    double a = d * exp(-(d * d) / (2.0 * s * s)) / (2.0 * r);
+                    yj[n] += amp[i] * a;
+                }
+            }
+        }
+    }
+    return err;
+}
+
+/*
+ * Adjoint: g[i_out] = sum_j sum_n a_ijn * delta[j][n] for the kernels listed
+ * in `cols` (n_cols entries; cols == NULL means all M kernels in order).
+ * delta: [N_d][N_t] fp64 row-major; g: [n_cols] fp64.
+ */
+int oracle_adjoint(int64_t M, const float* centers,
+                   double sigma, const double* sigmas,
+                   int32_t Nd, const float* sensors,
+                   double v, double fs, double t0, int32_t Nt, double k,
+                   const double* delta, const int64_t* cols, int64_t n_cols,
+                   double* g) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc) return rc;
+    if (cols == NULL) n_cols = M;
+    int err = ORACLE_OK;
+    int nth = oracle_get_threads();
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nth)
+    for (int64_t io = 0; io < n_cols; ++io) {
+        int64_t i = cols ? cols[io] : io;
+        double s = sigmas ? sigmas[i] : sigma;
+        double ks = k * s;
+        double acc = 0.0;
+        for (int32_t j = 0; j < Nd; ++j) {
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            if (!(r > ks)) {
+#pragma omp atomic write
+                err = ORACLE_ERR_GEOMETRY;
+                continue;
+            }
+            const double* dj = delta + (int64_t)j * Nt;
+            int64_t n0, n1;
+            candidate_range(r, ks, v, fs, t0, Nt, &n0, &n1);
+            for (int64_t n = n0; n <= n1; ++n) {
+                double t = t0 + (double)n / fs;
+                double d = r - v * t;
+                if (fabs(d) < ks) {
+                    double a = d * exp(-(d * d) / (2.0 * s * s)) / (2.0 * r);
+                    acc += a * dj[n];
+                }
+            }
+        }
+        g[io] = acc;
+    }
+    return err;
+}
+
+/*
+ * Exact count of in-window samples (useful pair-samples) over all pairs,
+ * used by bench.py / tests for the algorithmic work count of one operator.
+ */
+int64_t oracle_count_pair_samples(int64_t M, const float* centers, double sigma,
+                                  int32_t Nd, const float* sensors,
+                                  double v, double fs, double t0, int32_t Nt, double k,
+                                  const int64_t* cols, int64_t n_cols) {
+    if (cols == NULL) n_cols = M;
+    int64_t total = 0;
+    double ks = k * sigma;
+    int nth = oracle_get_threads();
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : total) num_threads(nth)
+    for (int64_t io = 0; io < n_cols; ++io) {
+        int64_t i = cols ? cols[io] : io;
+        for (int32_t j = 0; j < Nd; ++j) {
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            int64_t n0, n1;
+            candidate_range(r, ks, v, fs, t0, Nt, &n0, &n1);
+            for (int64_t n = n0; n <= n1; ++n) {
+                double t = t0 + (double)n / fs;
+                double d = r - v * t;
+                if (fabs(d) < ks) total += 1;
+            }
+        }
+    }
+    return total;
+}
