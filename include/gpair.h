@@ -1,0 +1,206 @@
+/*
+ * gpair.h -- C ABI of the B200-native GPAIR hot path (libgpair.so).
+ *
+ * Implements the closed-form Gaussian-kernel forward operator, its exact
+ * adjoint and the fused update of the iterative reconstruction of
+ * "GPAIR: Gaussian-Kernel-Based Ultrafast 3D Photoacoustic Iterative
+ * Reconstruction" (arXiv 2602.03893).  Citations P:<line> refer to that
+ * paper's text; readings R<n> are listed in DESIGN.md.
+ *
+ * Operator (Eq. 7, with the 3-sigma truncation of P:291 and the
+ * direct pair enumeration of P:295):
+ *
+ *   a_ijn = d exp(-d^2 / (2 sigma^2)) / (2 r_ij)  if |d| < k sigma, else 0
+ *   r_ij  = |c_i - s_j|,  d = r_ij - v t_n,  t_n = t0 + n / f_s   (R3)
+ *   forward:  y_j[n] = sum_i A_i a_ijn          (superposition)
+ *   adjoint:  g_i    = sum_j sum_n a_ijn delta_j[n]   (transpose)
+ *
+ * Conventions (apply to every call unless stated):
+ *   - Every array pointer is a DEVICE pointer (cudaMalloc / torch CUDA
+ *     tensor) on the device current when gpair_create was called, fp32,
+ *     contiguous, unless the comment says "host".
+ *   - Layouts: kernel centres and sensor positions are SoA [3][n] (x row, y
+ *     row, z row), metres.  Signals y, b, residuals are row-major
+ *     [N_d][N_t] (detector-major).  Per-kernel vectors are [M_local]
+ *     in the caller's kernel order; the spatial permutation is internal.
+ *   - Ownership: the caller owns every buffer passed in.  gpair_create copies
+ *     what it needs (centres, sensors) and keeps no caller pointer except the
+ *     borrowed nccl_comm, which must outlive the context.
+ *   - Outputs are overwritten, never accumulated into.
+ *   - Asynchrony: calls other than gpair_create/gpair_destroy enqueue work
+ *     on `stream` (a cudaStream_t; NULL = legacy default stream) and return
+ *     without synchronising.  Argument and geometry validation errors are
+ *     returned synchronously before anything is enqueued; asynchronous CUDA
+ *     or NCCL faults are sticky and reported by the next call.
+ *   - Errors: a non-GPAIR_OK status leaves outputs unspecified; the message
+ *     is available from gpair_last_error(ctx).
+ *   - Threading: a context is not thread-safe; use one context per rank
+ *     (device).  The library never calls exit() or prints.
+ */
+#ifndef GPAIR_H
+#define GPAIR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpair_ctx_s gpair_ctx;
+
+typedef enum {
+    GPAIR_OK = 0,
+    GPAIR_ERR_INVALID_ARGUMENT = 1, /* bad size, NULL, non-positive or non-finite scalar */
+    GPAIR_ERR_GEOMETRY = 2,         /* some r_ij <= k sigma (far-field Eq. 7 invalid), or
+                                       kernel cloud too sparse for cell anchoring */
+    GPAIR_ERR_RESOURCE = 3,         /* allocation failure, int32 index overflow, smem too small */
+    GPAIR_ERR_NUMERICAL = 4,        /* non-finite loss when GPAIR_CHECK_FINITE is set */
+    GPAIR_ERR_CUDA = 5,             /* CUDA runtime / launch error (no device, bad pointer, ...) */
+    GPAIR_ERR_NCCL = 6              /* NCCL not loadable or a collective failed */
+} gpair_status;
+
+/* gpair_desc.flags */
+enum {
+    GPAIR_TOF_EXACT = 0,        /* Eq. 7 evaluated at the exact time of flight (this build) */
+    GPAIR_TOF_ASSA = 1,         /* reserved: ASSA-snapped ToF, not implemented */
+    GPAIR_CHECK_FINITE = 1 << 9 /* gpair_iterate syncs and checks the loss is finite */
+};
+
+/* Problem description (P:230-233 kernels, P:319 sensors, P:251 v, P:303-309 f_s, N_t). */
+typedef struct {
+    double sound_speed;    /* v [m/s] > 0                                         */
+    double sampling_rate;  /* f_s [Hz] > 0                                 */
+    int32_t n_samples;     /* N_t >= 1                                            */
+    double t0;             /* time of sample 0 [s] (R3); t_n = t0 + n / f_s              */
+    int64_t n_kernels;     /* M_local >= 1: kernels owned by this rank            */
+    const float* centers;  /* DEVICE [3][M_local] SoA centres c_i [m], caller order      */
+    double sigma;          /* Gaussian std-dev [m] > 0, shared by all kernels    */
+    const float* sigmas;   /* must be NULL: per-kernel sigma is a NEXT row (R5)          */
+    double window_k;       /* k in |d| < k sigma; paper: 3                        */
+    int32_t n_sensors;     /* N_d >= 1                                                    */
+    const float* sensors;  /* DEVICE [3][N_d] SoA point-detector positions [m]   */
+    int32_t rank, world;   /* kernel-shard index / count; world >= 1                      */
+    void* nccl_comm;       /* ncclComm_t over `world` ranks (borrowed) or NULL if world=1 */
+    int32_t flags;         /* GPAIR_TOF_EXACT | GPAIR_CHECK_FINITE                        */
+} gpair_desc;
+
+/* One IR iteration's hyper-parameters (Algorithm 2). */
+typedef struct {
+    float lr;          /* eta_t for this iteration (caller computes, e.g. gpair_cawr_lr) */
+    float beta1;       /* Adam beta1, 0.9 (R11)                                          */
+    float beta2;       /* Adam beta2, 0.999 (R11)                                        */
+    float adam_eps;    /* Adam epsilon, 1e-8 (R11)                                       */
+    float eps_npc;     /* NPC epsilon, 1e-8                                      */
+    float grad_scale;  /* dL/dy = grad_scale (y - b); <= 0 -> 2/(N_d N_t) (R10)          */
+    int32_t step;      /* 1-based Adam step count t >= 1 (bias correction)               */
+    int32_t mode;      /* 0 = NPC x=(z+eps)^2 + Adam (paper);
+                          1 = clamp: state z holds x, x <- max(x - lr g, 0) (R15)       */
+} gpair_step;
+
+/* Accumulated device time of the library's own kernels (gpair_profile_*). */
+enum {
+    GPAIR_PROF_GATHER = 0,   /* amplitude gather (+NPC) into the spatial order      */
+    GPAIR_PROF_FORWARD = 1,  /* forward pair evaluation (dominant)                  */
+    GPAIR_PROF_REDUCE = 2,   /* region partials -> y (+ residual, loss partials)    */
+    GPAIR_PROF_ALLREDUCE = 3,/* ncclAllReduce of y (world > 1)                      */
+    GPAIR_PROF_RESIDUAL = 4, /* residual + loss (world > 1 only)                    */
+    GPAIR_PROF_ADJOINT = 5,  /* adjoint gather (+ fused update) (dominant)          */
+    GPAIR_PROF_LOSS = 6,     /* loss finalisation                                   */
+    GPAIR_PROF_N = 7
+};
+typedef struct {
+    double ms[GPAIR_PROF_N];       /* summed CUDA-event durations [ms]                */
+    int64_t launches[GPAIR_PROF_N];/* number of timed launches                        */
+} gpair_profile;
+
+/* Static description of what gpair_create built (for benchmarks and tests). */
+typedef struct {
+    int64_t n_kernels;          /* M_local                                              */
+    int64_t n_kernels_padded;   /* rounded up to whole 32-kernel cells                  */
+    int32_t n_cells;            /* 32-kernel spatial cells                              */
+    int32_t fwd_region_cells;   /* cells per forward region                              */
+    int32_t fwd_regions;        /* forward regions                                      */
+    int32_t fwd_window;         /* per-(region, sensor) window length (padded)          */
+    int32_t fwd_warps;          /* sensor warps per forward CTA                         */
+    int32_t adj_region_cells;   /* cells (= warps) per adjoint CTA                       */
+    int32_t adj_regions;        /* adjoint CTAs                                         */
+    int32_t adj_window;         /* per-(region, sensor) residual window length          */
+    int32_t wmax;               /* max in-window samples per pair (unrolled length)      */
+    int32_t grid_detected;      /* 1 if centres were recognised as a regular grid        */
+    double max_eps;             /* max |q|/R^2 of the anchor expansion       */
+    int64_t workspace_bytes;    /* device bytes owned by the context                    */
+} gpair_info;
+
+/* Create a context: validates `d`, sorts the kernels into 32-kernel spatial
+ * cells, builds per-(region, sensor) sample windows and allocates
+ * workspaces.  Runs on `stream` and synchronises it before returning.
+ * Errors: INVALID_ARGUMENT, GEOMETRY (r_ij <= k sigma for some pair, checked
+ * conservatively per cell), RESOURCE, CUDA.  *out is NULL on error. */
+gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream);
+
+/* Forward operator (Eq. 7 summed over kernels).
+ * amplitudes: DEVICE [M_local] A_i (caller order).
+ * signals:    DEVICE [N_d][N_t] output y; with world > 1 the sum over all
+ *             ranks (ncclAllReduce in place), identical on every rank. */
+gpair_status gpair_forward(gpair_ctx* ctx, const float* amplitudes, float* signals, void* stream);
+
+/* Adjoint operator (exact transpose of gpair_forward).
+ * residual: DEVICE [N_d][N_t] delta (replicated on every rank).
+ * grad:     DEVICE [M_local] output g_i = sum_j sum_n a_ijn delta_j[n]. */
+gpair_status gpair_adjoint(gpair_ctx* ctx, const float* residual, float* grad, void* stream);
+
+/* One iteration of Algorithm 2, lambda = 0:
+ *   x = (z + eps)^2 (mode 0) or x = z (mode 1);  y = A x  [+ allreduce];
+ *   L = (1/N) |y - b|^2;  g = A^T (grad_scale (y - b));
+ *   mode 0: dz = g 2 (z + eps); Adam step on (z, m, v) with s->lr, s->step;
+ *   mode 1: z = max(z - lr g, 0).
+ * z, m, v:     DEVICE [M_local] in/out state (m, v unused in mode 1, may be NULL).
+ * b:           DEVICE [N_d][N_t] measured signals.
+ * signals_out: DEVICE [N_d][N_t] y of this iteration, or NULL.
+ * x_out:       DEVICE [M_local] x of the UPDATED state, or NULL.
+ * loss_out:    DEVICE float scalar L (of the pre-update state), or NULL. */
+gpair_status gpair_iterate(gpair_ctx* ctx, float* z, float* m, float* v, const float* b,
+                           const gpair_step* s, float* signals_out, float* x_out,
+                           float* loss_out, void* stream);
+
+/* Exact number of in-window pair-samples (|d| < k sigma, n in [0, N_t)) of
+ * this rank's operator; synchronous.  Host output. */
+gpair_status gpair_count_pair_samples(gpair_ctx* ctx, int64_t* out_host, void* stream);
+
+/* Fill *out (host struct) with the context's build parameters. */
+gpair_status gpair_get_info(const gpair_ctx* ctx, gpair_info* out);
+
+/* Release all device memory and events of the context (synchronises). NULL ok. */
+gpair_status gpair_destroy(gpair_ctx* ctx);
+
+/* Per-kernel device timing with CUDA events recorded on the launch stream.
+ * enable != 0 starts accumulating (and resets the counters); read
+ * synchronises the pending events and copies the totals to *out (host). */
+gpair_status gpair_profile_enable(gpair_ctx* ctx, int enable);
+gpair_status gpair_profile_read(gpair_ctx* ctx, gpair_profile* out);
+
+/* CAWR learning rate, Eq. 24, host function.
+ * printed_formula != 0: T_cur = t mod T0, T_i = T0 Tmult^floor(t/T0) as
+ * printed (R13); 0: SGDR restarts (identical when Tmult = 1).
+ * Returns NaN for T0 < 1 or Tmult < 1 or t < 0. */
+double gpair_cawr_lr(int64_t t, double eta_min, double eta_max, int64_t T0, int64_t Tmult,
+                     int printed_formula);
+
+/* NCCL bootstrap helpers (host).  NCCL is loaded with dlopen("libnccl.so.2")
+ * at first use.  unique_id: host buffer of 128 bytes (ncclUniqueId).
+ * comm_out receives an ncclComm_t to pass as gpair_desc.nccl_comm. */
+gpair_status gpair_nccl_unique_id(void* unique_id_host128);
+gpair_status gpair_nccl_comm_init(void** comm_out, int32_t world, const void* unique_id_host128,
+                                  int32_t rank);
+gpair_status gpair_nccl_comm_destroy(void* comm);
+
+/* Static strings; never NULL. */
+const char* gpair_strerror(gpair_status s);
+const char* gpair_last_error(const gpair_ctx* ctx); /* host string valid until the next call */
+const char* gpair_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GPAIR_H */

@@ -1,0 +1,462 @@
+// gpair_api.cu -- the C ABI of include/gpair.h.
+//
+// Host logic only: argument validation, operator constants, kernel sequencing
+// on the caller's stream, the NCCL all-reduce call site (kernel sharding,
+// SURVEY 8e) and optional CUDA-event profiling.  All arithmetic of the
+// method runs in the kernels of gpair_kernels.cu / gpair_setup.cu.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "gpair_ctx.h"
+
+using gpair::EpiParams;
+
+namespace {
+
+thread_local std::string g_static_err;
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+typedef int nccl_res_t;
+struct nccl_uid_t {
+    char internal[128];
+};
+struct NcclApi {
+    bool tried = false, ok = false;
+    nccl_res_t (*GetUniqueId)(nccl_uid_t*) = nullptr;
+    nccl_res_t (*CommInitRank)(void**, int, nccl_uid_t, int) = nullptr;
+    nccl_res_t (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    nccl_res_t (*CommDestroy)(void*) = nullptr;
+    const char* (*GetErrorString)(nccl_res_t) = nullptr;
+};
+NcclApi g_nccl;
+constexpr int NCCL_FLOAT32 = 7, NCCL_SUM = 0;
+
+bool nccl_load() {
+    if (g_nccl.tried) return g_nccl.ok;
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+    g_nccl.GetUniqueId = (nccl_res_t(*)(nccl_uid_t*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (nccl_res_t(*)(void**, int, nccl_uid_t, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (nccl_res_t(*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (nccl_res_t(*)(void*))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (const char* (*)(nccl_res_t))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+    return g_nccl.ok;
+}
+
+// ---------------------------------------------------------------- helpers
+gpair_status fail(gpair_ctx* c, gpair_status s, const std::string& msg) {
+    if (c)
+        c->err = msg;
+    else
+        g_static_err = msg;
+    return s;
+}
+
+gpair_status cuda_fail(gpair_ctx* c, cudaError_t e, const char* where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return fail(c, GPAIR_ERR_CUDA, m);
+}
+
+#define API_CUDA(c, x, where)                              \
+    do {                                                   \
+        cudaError_t e_ = (x);                              \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+    } while (0)
+
+bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
+
+// Event-timed launch wrapper.
+struct ProfScope {
+    gpair_ctx* c;
+    int id;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(gpair_ctx* c_, int id_, cudaStream_t st_) : c(c_), id(id_), st(st_) {
+        if (!c->prof_on) return;
+        a = take();
+        b = take();
+        if (a) cudaEventRecord(a, st);
+    }
+    cudaEvent_t take() {
+        cudaEvent_t e = nullptr;
+        if (!c->prof_free.empty()) {
+            e = c->prof_free.back();
+            c->prof_free.pop_back();
+        } else if (cudaEventCreate(&e) != cudaSuccess) {
+            e = nullptr;
+        }
+        return e;
+    }
+    ~ProfScope() {
+        if (!c->prof_on || !a || !b) return;
+        cudaEventRecord(b, st);
+        c->prof_pending.push_back({id, a, b});
+    }
+};
+
+void prof_drain(gpair_ctx* c) {
+    for (auto& p : c->prof_pending) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p.stop) == cudaSuccess && cudaEventElapsedTime(&ms, p.start, p.stop) == cudaSuccess) {
+            c->prof_ms[p.id] += ms;
+            c->prof_n[p.id] += 1;
+        }
+        c->prof_free.push_back(p.start);
+        c->prof_free.push_back(p.stop);
+    }
+    c->prof_pending.clear();
+}
+
+void free_ctx(gpair_ctx* c) {
+    if (!c) return;
+    cudaFree(c->d_sens);
+    cudaFree(c->d_kd);
+    cudaFree(c->d_cell);
+    cudaFree(c->d_orig);
+    cudaFree(c->d_perm);
+    cudaFree(c->d_wlo_f);
+    cudaFree(c->d_wlo_fT);
+    cudaFree(c->d_jlo);
+    cudaFree(c->d_jlen);
+    cudaFree(c->d_partial);
+    cudaFree(c->d_wlo_a);
+    cudaFree(c->d_amp);
+    cudaFree(c->d_y);
+    cudaFree(c->d_delta);
+    cudaFree(c->d_loss_part);
+    cudaFree(c->d_count);
+    cudaFree(c->d_flags);
+    prof_drain(c);
+    for (auto e : c->prof_free) cudaEventDestroy(e);
+    delete c;
+}
+
+gpair_status sticky_check(gpair_ctx* c) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "pending asynchronous CUDA error");
+    return GPAIR_OK;
+}
+
+gpair_status allreduce(gpair_ctx* c, float* y, cudaStream_t st) {
+    if (c->world <= 1) return GPAIR_OK;
+    ProfScope ps(c, GPAIR_PROF_ALLREDUCE, st);
+    nccl_res_t r = g_nccl.AllReduce(y, y, (size_t)c->Nd * c->Nt, NCCL_FLOAT32, NCCL_SUM, c->nccl, st);
+    if (r != 0)
+        return fail(c, GPAIR_ERR_NCCL,
+                    std::string("ncclAllReduce failed: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+    return GPAIR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gpair_version(void) { return "gpair-b200 0.1 (sm_100a)"; }
+
+const char* gpair_strerror(gpair_status s) {
+    switch (s) {
+        case GPAIR_OK: return "ok";
+        case GPAIR_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case GPAIR_ERR_GEOMETRY: return "geometry conflict";
+        case GPAIR_ERR_RESOURCE: return "resource limit";
+        case GPAIR_ERR_NUMERICAL: return "numerical failure";
+        case GPAIR_ERR_CUDA: return "CUDA error";
+        case GPAIR_ERR_NCCL: return "NCCL error";
+    }
+    return "unknown status";
+}
+
+const char* gpair_last_error(const gpair_ctx* ctx) { return ctx ? ctx->err.c_str() : g_static_err.c_str(); }
+
+double gpair_cawr_lr(int64_t t, double eta_min, double eta_max, int64_t T0, int64_t Tmult, int printed_formula) {
+    if (T0 < 1 || Tmult < 1 || t < 0) return NAN;
+    double T_cur, T_i;
+    if (printed_formula || Tmult == 1) {
+        // Eq. 24 as printed: T_cur = t mod T0, T_i = T0 Tmult^floor(t/T0)
+        T_cur = (double)(t % T0);
+        T_i = (double)T0 * std::pow((double)Tmult, (double)(t / T0));
+    } else {
+        // SGDR restarts: periods T0, T0 Tmult, T0 Tmult^2, ...
+        int64_t start = 0, period = T0;
+        while (t >= start + period) {
+            start += period;
+            period *= Tmult;
+        }
+        T_cur = (double)(t - start);
+        T_i = (double)period;
+    }
+    return eta_min + 0.5 * (eta_max - eta_min) * (1.0 + std::cos(M_PI * T_cur / T_i));
+}
+
+gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
+    if (!out) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!d) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "desc is NULL");
+    if (!finite_pos(d->sound_speed)) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "sound_speed must be finite > 0");
+    if (!finite_pos(d->sampling_rate)) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "sampling_rate must be finite > 0");
+    if (!finite_pos(d->sigma)) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "sigma must be finite > 0");
+    if (!finite_pos(d->window_k)) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "window_k must be finite > 0");
+    if (!std::isfinite(d->t0)) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "t0 must be finite");
+    if (d->n_samples < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_samples must be >= 1");
+    if (d->n_sensors < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_sensors must be >= 1");
+    if (d->n_kernels < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_kernels must be >= 1");
+    if (!d->centers || !d->sensors) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "centers/sensors NULL");
+    if (d->sigmas) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "per-kernel sigmas are not supported (must be NULL)");
+    if (d->flags & GPAIR_TOF_ASSA) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "GPAIR_TOF_ASSA not implemented");
+    if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
+        return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "rank/world invalid");
+    if (d->world > 1 && !d->nccl_comm) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "world > 1 needs nccl_comm");
+    if ((int64_t)d->n_sensors * d->n_samples >= (1LL << 31))
+        return fail(nullptr, GPAIR_ERR_RESOURCE, "N_d * N_t must be < 2^31");
+    if (d->n_kernels >= (1LL << 31) - 64) return fail(nullptr, GPAIR_ERR_RESOURCE, "n_kernels must be < 2^31 - 64");
+    if (d->world > 1 && !nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+
+    // operator constants (fp64 on the host)
+    const double v = d->sound_speed, fs = d->sampling_rate, s = d->sigma, kk = d->window_k;
+    const double h = v / fs;
+    const double log2e = 1.4426950408889634;
+    gpair::OpConst k{};
+    k.v = v;
+    k.fs = fs;
+    k.t0 = d->t0;
+    k.ks = kk * s;  // same expression as the oracle's k * sigma
+    k.Nt = d->n_samples;
+    k.Nd = d->n_sensors;
+    double Lw = 2.0 * k.ks / h;
+    double Lr = std::nearbyint(Lw);
+    int wmax = (std::fabs(Lw - Lr) < 1e-6 * std::max(1.0, Lw)) ? (int)Lr : (int)std::ceil(Lw);
+    k.wmax = std::max(wmax, 1);
+    k.h = (float)h;
+    k.inv_h = (float)(1.0 / h);
+    k.ksf = (float)k.ks;
+    k.K1 = (float)(-log2e / (2.0 * s * s));
+    k.K2 = (float)(log2e * h / (s * s));
+    k.K3 = (float)(-log2e * h * h / (2.0 * s * s));
+    k.cq = (float)std::exp(-h * h / (s * s));
+
+    gpair_ctx* c = new (std::nothrow) gpair_ctx();
+    if (!c) return fail(nullptr, GPAIR_ERR_RESOURCE, "host allocation failed");
+    cudaError_t e = cudaGetDevice(&c->device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(nullptr, e, "cudaGetDevice");
+    }
+    c->k = k;
+    c->M = d->n_kernels;
+    c->Nd = d->n_sensors;
+    c->Nt = d->n_samples;
+    c->rank = d->rank;
+    c->world = d->world;
+    c->nccl = d->nccl_comm;
+    c->flags = d->flags;
+    cudaStream_t st = (cudaStream_t)stream;
+    std::string why;
+    int geom_err = 0;
+    e = gpair::build_geometry(c, d->centers, d->sensors, st, why, geom_err);
+    if (e != cudaSuccess) {
+        std::string m = std::string("gpair_create: ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+        free_ctx(c);
+        return fail(nullptr, e == cudaErrorMemoryAllocation ? GPAIR_ERR_RESOURCE : GPAIR_ERR_CUDA, m);
+    }
+    if (geom_err) {
+        free_ctx(c);
+        return fail(nullptr, (gpair_status)geom_err, why);
+    }
+    *out = c;
+    return GPAIR_OK;
+}
+
+gpair_status gpair_destroy(gpair_ctx* ctx) {
+    if (!ctx) return GPAIR_OK;
+    cudaDeviceSynchronize();
+    free_ctx(ctx);
+    return GPAIR_OK;
+}
+
+gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
+    if (!c || !o) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "NULL argument");
+    o->n_kernels = c->M;
+    o->n_kernels_padded = c->Mpad;
+    o->n_cells = c->ncells;
+    o->fwd_region_cells = c->f_cpr;
+    o->fwd_regions = c->f_regions;
+    o->fwd_window = c->Lf;
+    o->fwd_warps = c->f_warps;
+    o->adj_region_cells = c->a_cpr;
+    o->adj_regions = c->a_regions;
+    o->adj_window = c->La;
+    o->wmax = c->k.wmax;
+    o->grid_detected = c->grid_detected;
+    o->max_eps = c->max_eps;
+    o->workspace_bytes = c->workspace_bytes;
+    return GPAIR_OK;
+}
+
+static gpair_status do_forward_core(gpair_ctx* c, const float* src, int npc, float eps, float* y,
+                                    const float* b, cudaStream_t st) {
+    {
+        ProfScope ps(c, GPAIR_PROF_GATHER, st);
+        API_CUDA(c, gpair::launch_gather(c, src, npc, eps, st), "gather");
+    }
+    {
+        ProfScope ps(c, GPAIR_PROF_FORWARD, st);
+        API_CUDA(c, gpair::launch_forward(c, st), "forward");
+    }
+    if (c->world == 1) {
+        ProfScope ps(c, GPAIR_PROF_REDUCE, st);
+        API_CUDA(c, gpair::launch_reduce(c, y, b, b ? c->d_delta : nullptr, st), "reduce");
+    } else {
+        {
+            ProfScope ps(c, GPAIR_PROF_REDUCE, st);
+            API_CUDA(c, gpair::launch_reduce(c, y, nullptr, nullptr, st), "reduce");
+        }
+        gpair_status s = allreduce(c, y, st);
+        if (s != GPAIR_OK) return s;
+        if (b) {
+            ProfScope ps(c, GPAIR_PROF_RESIDUAL, st);
+            API_CUDA(c, gpair::launch_residual(c, y, b, c->d_delta, st), "residual");
+        }
+    }
+    return GPAIR_OK;
+}
+
+gpair_status gpair_forward(gpair_ctx* c, const float* amplitudes, float* signals, void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!amplitudes || !signals) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "amplitudes/signals NULL");
+    gpair_status s = sticky_check(c);
+    if (s) return s;
+    return do_forward_core(c, amplitudes, 0, 0.f, signals, nullptr, (cudaStream_t)stream);
+}
+
+gpair_status gpair_adjoint(gpair_ctx* c, const float* residual, float* grad, void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!residual || !grad) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "residual/grad NULL");
+    gpair_status s = sticky_check(c);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    EpiParams ep{};
+    ep.scale = 1.f;
+    ep.g_out = grad;
+    ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+    API_CUDA(c, gpair::launch_adjoint(c, residual, gpair::EPI_GRAD, ep, st), "adjoint");
+    return GPAIR_OK;
+}
+
+gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const float* b, const gpair_step* s,
+                           float* signals_out, float* x_out, float* loss_out, void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!z || !b || !s) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "z/b/step NULL");
+    if (s->mode != 0 && s->mode != 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "mode must be 0 (NPC) or 1 (clamp)");
+    if (s->mode == 0 && (!m || !v)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "Adam state m/v NULL");
+    if (s->mode == 0 && s->step < 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "step must be >= 1");
+    if (!std::isfinite(s->lr)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lr not finite");
+    gpair_status st0 = sticky_check(c);
+    if (st0) return st0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int npc = s->mode == 0;
+    float* y = signals_out ? signals_out : c->d_y;
+    gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (c->world == 1 && !signals_out) ? nullptr : y, b, st);
+    if (r) return r;
+    if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
+        ProfScope ps(c, GPAIR_PROF_LOSS, st);
+        float* lo = loss_out ? loss_out : (float*)(c->d_count);  // scratch word when only checking
+        API_CUDA(c, gpair::launch_loss(c, lo, st), "loss");
+        if (c->flags & GPAIR_CHECK_FINITE) {
+            float h = 0.f;
+            API_CUDA(c, cudaMemcpyAsync(&h, lo, sizeof(float), cudaMemcpyDeviceToHost, st), "loss readback");
+            API_CUDA(c, cudaStreamSynchronize(st), "loss sync");
+            if (!std::isfinite(h)) return fail(c, GPAIR_ERR_NUMERICAL, "loss is not finite");
+        }
+    }
+    EpiParams ep{};
+    const double N = (double)c->Nd * (double)c->Nt;
+    ep.scale = s->grad_scale > 0.f ? s->grad_scale : (float)(2.0 / N);
+    ep.lr = s->lr;
+    ep.beta1 = s->beta1;
+    ep.beta2 = s->beta2;
+    ep.adam_eps = s->adam_eps;
+    ep.eps_npc = s->eps_npc;
+    if (npc) {
+        ep.bc1 = (float)(1.0 / (1.0 - std::pow((double)s->beta1, (double)s->step)));
+        ep.bc2 = (float)(1.0 / (1.0 - std::pow((double)s->beta2, (double)s->step)));
+    }
+    ep.z = z;
+    ep.m = m;
+    ep.v = v;
+    ep.x_out = x_out;
+    ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+    API_CUDA(c, gpair::launch_adjoint(c, c->d_delta, npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP, ep, st),
+             "adjoint+update");
+    return GPAIR_OK;
+}
+
+gpair_status gpair_count_pair_samples(gpair_ctx* c, int64_t* out, void* stream) {
+    if (!c || !out) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    API_CUDA(c, gpair::launch_count(c, st), "count");
+    unsigned long long h = 0;
+    API_CUDA(c, cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, st), "count readback");
+    API_CUDA(c, cudaStreamSynchronize(st), "count sync");
+    *out = (int64_t)h;
+    return GPAIR_OK;
+}
+
+gpair_status gpair_profile_enable(gpair_ctx* c, int enable) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    prof_drain(c);
+    for (int i = 0; i < GPAIR_PROF_N; ++i) {
+        c->prof_ms[i] = 0.0;
+        c->prof_n[i] = 0;
+    }
+    c->prof_on = enable != 0;
+    return GPAIR_OK;
+}
+
+gpair_status gpair_profile_read(gpair_ctx* c, gpair_profile* out) {
+    if (!c || !out) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "NULL argument");
+    prof_drain(c);
+    for (int i = 0; i < GPAIR_PROF_N; ++i) {
+        out->ms[i] = c->prof_ms[i];
+        out->launches[i] = c->prof_n[i];
+    }
+    return GPAIR_OK;
+}
+
+gpair_status gpair_nccl_unique_id(void* uid) {
+    if (!uid) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "NULL buffer");
+    if (!nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    nccl_uid_t id;
+    nccl_res_t r = g_nccl.GetUniqueId(&id);
+    if (r != 0) return fail(nullptr, GPAIR_ERR_NCCL, "ncclGetUniqueId failed");
+    memcpy(uid, id.internal, 128);
+    return GPAIR_OK;
+}
+
+gpair_status gpair_nccl_comm_init(void** comm, int32_t world, const void* uid, int32_t rank) {
+    if (!comm || !uid || world < 1 || rank < 0 || rank >= world)
+        return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "bad argument");
+    if (!nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    nccl_uid_t id;
+    memcpy(id.internal, uid, 128);
+    nccl_res_t r = g_nccl.CommInitRank(comm, world, id, rank);
+    if (r != 0)
+        return fail(nullptr, GPAIR_ERR_NCCL,
+                    std::string("ncclCommInitRank failed: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+    return GPAIR_OK;
+}
+
+gpair_status gpair_nccl_comm_destroy(void* comm) {
+    if (!comm) return GPAIR_OK;
+    if (!nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    g_nccl.CommDestroy(comm);
+    return GPAIR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// gpair_ctx.h -- host-side context of libgpair (not part of the public ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gpair.h"
+#include "gpair_internal.cuh"
+
+struct GpairEventPair {
+    int id;
+    cudaEvent_t start, stop;
+};
+
+struct gpair_ctx_s {
+    int device = 0;
+    gpair::OpConst k{};
+    int64_t M = 0, Mpad = 0;
+    int32_t ncells = 0, Nd = 0, Nt = 0;
+    int32_t rank = 0, world = 1;
+    void* nccl = nullptr;
+    int32_t flags = 0;
+    int grid_detected = 0;
+    double max_eps = 0.0;
+
+    // geometry in the internal (spatially sorted) order
+    float* d_sens = nullptr;   // [3][Nd]
+    float4* d_kd = nullptr;    // [Mpad] (dx, dy, dz, |d|^2) relative to the cell anchor
+    float4* d_cell = nullptr;  // [ncells] (Cx, Cy, Cz, radius) fp32 anchor + conservative radius
+    float* d_orig = nullptr;   // [3][Mpad] original fp32 centres (exact fp64 window fix-up)
+    int32_t* d_perm = nullptr; // [Mpad] sorted -> caller index, -1 = padding
+
+    // forward decomposition
+    int32_t f_cpr = 0, f_regions = 0, f_warps = 0, f_sgroups = 0, Lf = 0;
+    int32_t* d_wlo_f = nullptr;   // [f_regions][Nd] window start (-1 = empty)
+    int32_t* d_wlo_fT = nullptr;  // [Nd][f_regions] transposed copy for the reducer
+    int32_t* d_jlo = nullptr;     // [Nd] live range start per sensor
+    int32_t* d_jlen = nullptr;    // [Nd] live range length per sensor
+    int32_t jlen_max = 0;
+    float* d_partial = nullptr;   // [f_regions][Nd][Lf]
+
+    // adjoint decomposition
+    int32_t a_cpr = 0, a_regions = 0, La = 0;
+    int32_t* d_wlo_a = nullptr;   // [a_regions][Nd]
+
+    // per-call workspaces
+    float* d_amp = nullptr;       // [Mpad] amplitudes in sorted order
+    float* d_y = nullptr;         // [Nd][Nt]
+    float* d_delta = nullptr;     // [Nd][Nt] residual y - b
+    double* d_loss_part = nullptr;// [Nd]
+    unsigned long long* d_count = nullptr;
+    int32_t* d_flags = nullptr;   // scratch flags
+
+    int64_t workspace_bytes = 0;
+    std::string err;
+
+    // profiling
+    bool prof_on = false;
+    std::vector<GpairEventPair> prof_pending;
+    std::vector<cudaEvent_t> prof_free;
+    double prof_ms[GPAIR_PROF_N] = {0};
+    int64_t prof_n[GPAIR_PROF_N] = {0};
+};
+
+namespace gpair {
+
+// setup (gpair_setup.cu)
+cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sensors, cudaStream_t st,
+                           std::string& why, int& geom_err);
+
+// kernels (gpair_kernels.cu)
+cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cudaStream_t st);
+cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st);
+cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st);
+cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st);
+cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st);
+struct EpiParams {
+    float scale;
+    float lr, beta1, beta2, adam_eps, eps_npc, bc1, bc2;
+    float* g_out;
+    float* z;
+    float* m;
+    float* v;
+    float* x_out;
+};
+enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
+cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
+cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
+
+}  // namespace gpair

@@ -1,0 +1,457 @@
+// gpair_kernels.cu -- per-call kernels of the GPAIR hot path.
+//
+//   k_gather    a2: x = (z + eps)^2 (NPC, Eq. 18) or x as given, into the
+//                   spatial order of the cells.
+//   k_forward   a3+a4: lane = sensor, warp = 32 sensors, CTA = region of cells
+//                   x sensor group.  Kernel parameters are staged in shared
+//                   memory and broadcast; each lane accumulates its sensor's
+//                   time trace for the region in a private shared-memory
+//                   column [sample][32] (conflict-free, no atomics), then the
+//                   warp flushes it with 128-byte coalesced stores after an
+//                   in-place XOR-swizzled transpose.
+//   k_reduce    a5+a6: sums the region partial traces of one sensor in a
+//                   fixed order (deterministic), writes y, the residual
+//                   delta = y - b and per-sensor loss partials.
+//   k_adjoint   a7+a8: lane = kernel, warp = one 32-kernel cell, CTA = region
+//                   of cells; residual windows of 32 sensors are staged in
+//                   shared memory and read per lane (gather only, no atomics);
+//                   the epilogue writes g or applies the fused NPC chain rule
+//                   (Eq. 19) + Adam, or the projected clamp step.
+#include <cfloat>
+
+#include "gpair_ctx.h"
+
+namespace gpair {
+
+namespace {
+
+constexpr int STAGE_CELLS = 8;  // cells staged per forward pipeline step
+
+__global__ void k_gather(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t Mpad,
+                         int npc, float eps, float* __restrict__ amp) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= Mpad) return;
+    int32_t p = perm[i];
+    float a = 0.f;
+    if (p >= 0) {
+        float v = src[p];
+        a = npc ? (v + eps) * (v + eps) : v;
+    }
+    amp[i] = a;
+}
+
+// ------------------------------------------------------------------ forward
+template <int WMAX>
+__global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
+                                                 const float4* __restrict__ cell, const float* __restrict__ orig,
+                                                 const float* __restrict__ sens, const int32_t* __restrict__ wlo,
+                                                 float* __restrict__ partial, int32_t cpr, int32_t ncells,
+                                                 int32_t Lf, int64_t Mpad, OpConst k) {
+    extern __shared__ float4 smem4[];
+    float4* s_kd = smem4;                                   // [STAGE_CELLS*32]
+    float4* s_cell = s_kd + STAGE_CELLS * CELL;             // [STAGE_CELLS]
+    float* s_amp = (float*)(s_cell + STAGE_CELLS);          // [STAGE_CELLS*32]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_acc = s_amp + STAGE_CELLS * CELL + (size_t)warp * Lf * 32;
+
+    const int region = blockIdx.x;
+    const int jbase = (blockIdx.y * nw + warp) * 32;
+    const int j = jbase + lane;
+    const bool jok = j < k.Nd;
+    for (int t = lane; t < Lf * 32; t += 32) s_acc[t] = 0.f;
+    const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    if (jok) {
+        sx = sens[j];
+        sy = sens[k.Nd + j];
+        sz = sens[2 * k.Nd + j];
+    }
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
+        const int nc = min(STAGE_CELLS, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            s_kd[t] = kd[(int64_t)cb * CELL + t];
+            s_amp[t] = amp[(int64_t)cb * CELL + t];
+        }
+        if (threadIdx.x < nc) s_cell[threadIdx.x] = cell[cb + threadIdx.x];
+        __syncthreads();
+        if (lo_j < 0) continue;
+        for (int cc = 0; cc < nc; ++cc) {
+            const float4 C = s_cell[cc];
+            const Anchor a = make_anchor(C.x, C.y, C.z, sx, sy, sz, k);
+            for (int t = 0; t < CELL; ++t) {
+                const float4 d4 = s_kd[cc * CELL + t];
+                const float A = s_amp[cc * CELL + t];
+                PairWin p = pair_setup(a, d4, A, k);
+                if (p.amb) {
+                    const int64_t gi = (int64_t)(cb + cc) * CELL + t;
+                    int nlo, cnt;
+                    exact_window(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, p.g_first,
+                                 p.g_last, k, nlo, cnt);
+                    if (cnt > 0) p.e_lo = e_at(a, d4, nlo, k);
+                    p.n_lo = nlo;
+                    p.cnt = cnt;
+                }
+                if (p.cnt <= 0) continue;
+                float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
+                float P = p.w * exp2f(p.e_lo * p.e_lo * k.K1);
+                float q = exp2f(fmaf(p.e_lo, k.K2, k.K3));
+#pragma unroll
+                for (int m = 0; m < WMAX; ++m) {
+                    if (m < p.cnt) {
+                        const float dm = fmaf(-(float)m, k.h, p.e_lo);
+                        ap[m * 32] = fmaf(dm, P, ap[m * 32]);
+                    }
+                    P *= q;
+                    q *= k.cq;
+                }
+                for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
+                    const float dm = fmaf(-(float)m, k.h, p.e_lo);
+                    ap[m * 32] = fmaf(dm, P, ap[m * 32]);
+                    P *= q;
+                    q *= k.cq;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    // flush: per 32-row block, in-place XOR-swizzled transpose then coalesced stores
+    float* dst = partial + ((int64_t)region * k.Nd + jbase) * Lf;
+    for (int m0 = 0; m0 < Lf; m0 += 32) {
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = s_acc[(m0 + t) * 32 + lane];
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 32; ++t) s_acc[(m0 + t) * 32 + (lane ^ t)] = v[t];
+        __syncwarp();
+        for (int jj = 0; jj < 32; ++jj) {
+            if (jbase + jj < k.Nd) dst[(int64_t)jj * Lf + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ reduce
+// One CTA per sensor j.  Warp w sums regions w, w+nw, ... into its private
+// shared-memory copy of the sensor's live range; copies are then summed in
+// warp order (deterministic).  Optionally fuses the residual and loss.
+constexpr int RED_BATCH = 4;
+
+__global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int32_t* __restrict__ wloT,
+                                                const int32_t* __restrict__ jlo_a, const int32_t* __restrict__ jlen_a,
+                                                int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
+                                                const float* __restrict__ b, float* __restrict__ delta,
+                                                double* __restrict__ loss_part) {
+    extern __shared__ float s_copy[];
+    const int j = blockIdx.x;
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jlo = jlo_a[j], jlen = jlen_a[j];
+    float* mine = s_copy + (size_t)warp * jlen;
+    for (int t = lane; t < jlen; t += 32) mine[t] = 0.f;
+    __syncwarp();
+    const int32_t* wl = wloT + (int64_t)j * nregions;
+    for (int r0 = warp; r0 < nregions; r0 += nw * RED_BATCH) {
+        int lo[RED_BATCH];
+#pragma unroll
+        for (int u = 0; u < RED_BATCH; ++u) {
+            int r = r0 + u * nw;
+            lo[u] = r < nregions ? wl[r] : -1;
+        }
+        for (int m0 = 0; m0 < Lf; m0 += 32) {
+            float val[RED_BATCH];
+#pragma unroll
+            for (int u = 0; u < RED_BATCH; ++u) {
+                int r = r0 + u * nw;
+                val[u] = lo[u] >= 0 ? partial[((int64_t)r * k.Nd + j) * Lf + m0 + lane] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < RED_BATCH; ++u) {
+                int n = lo[u] + m0 + lane;
+                if (lo[u] >= 0 && n < k.Nt) mine[n - jlo] += val[u];
+            }
+        }
+    }
+    __syncthreads();
+    double lsum = 0.0;
+    const int64_t row = (int64_t)j * k.Nt;
+    for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
+        float yv = 0.f;
+        int t = n - jlo;
+        if (t >= 0 && t < jlen) {
+            for (int w = 0; w < nw; ++w) yv += s_copy[(size_t)w * jlen + t];
+        }
+        if (y) y[row + n] = yv;
+        if (b) {
+            float dv = yv - b[row + n];
+            delta[row + n] = dv;
+            lsum += (double)dv * (double)dv;
+        }
+    }
+    if (b) {
+        __shared__ double s_red[32];
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+        if (lane == 0) s_red[warp] = lsum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += s_red[w];
+            loss_part[j] = s;
+        }
+    }
+}
+
+// residual + loss partials for world > 1 (y already all-reduced)
+__global__ void k_residual(const float* __restrict__ y, const float* __restrict__ b, int32_t Nt,
+                           float* __restrict__ delta, double* __restrict__ loss_part) {
+    const int j = blockIdx.x;
+    const int64_t row = (int64_t)j * Nt;
+    double lsum = 0.0;
+    for (int n = threadIdx.x; n < Nt; n += blockDim.x) {
+        float dv = y[row + n] - b[row + n];
+        delta[row + n] = dv;
+        lsum += (double)dv * (double)dv;
+    }
+    __shared__ double s_red[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    if (lane == 0) s_red[warp] = lsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += s_red[w];
+        loss_part[j] = s;
+    }
+}
+
+__global__ void k_loss(const double* __restrict__ part, int32_t n, double inv_N, float* out) {
+    __shared__ double s[1024];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = (float)(s[0] * inv_N);
+}
+
+// ------------------------------------------------------------------ adjoint
+template <int WMAX, int MODE>
+__global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, const float4* __restrict__ cell,
+                                                 const float* __restrict__ orig, const int32_t* __restrict__ perm,
+                                                 const float* __restrict__ sens, const int32_t* __restrict__ wlo,
+                                                 const float* __restrict__ resid, int32_t cpr, int32_t ncells,
+                                                 int32_t La, int64_t Mpad, OpConst k, EpiParams ep,
+                                                 unsigned long long* count) {
+    extern __shared__ float4 smem4[];
+    Anchor* s_anc = (Anchor*)smem4;                          // [nw][32]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* s_wlo = (int32_t*)(s_anc + nw * 32);           // [32]
+    float* s_res = (float*)(s_wlo + 32);                     // [32][La]
+
+    const int cid = blockIdx.x * cpr + warp;
+    const bool cok = (warp < cpr) && (cid < ncells);
+    const int64_t gi = (int64_t)cid * CELL + lane;
+    float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 C = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cok) {
+        d4 = kd[gi];
+        C = cell[cid];
+    }
+    float acc = 0.f;
+    unsigned long long npairs = 0;
+    for (int jb = 0; jb < k.Nd; jb += 32) {
+        const int nj = min(32, k.Nd - jb);
+        __syncthreads();
+        if (threadIdx.x < 32) s_wlo[threadIdx.x] = threadIdx.x < nj ? wlo[(int64_t)blockIdx.x * k.Nd + jb + threadIdx.x] : -1;
+        if (cok && lane < nj) {
+            const int j = jb + lane;
+            s_anc[warp * 32 + lane] = make_anchor(C.x, C.y, C.z, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+        }
+        __syncthreads();
+        if (MODE != 3) {
+            for (int t = threadIdx.x; t < 32 * La; t += blockDim.x) {
+                const int jj = t / La, m = t - jj * La;
+                const int lo = s_wlo[jj];
+                const int n = lo + m;
+                s_res[t] = (lo >= 0 && n < k.Nt) ? resid[(int64_t)(jb + jj) * k.Nt + n] : 0.f;
+            }
+            __syncthreads();
+        }
+        if (!cok) continue;
+        float accb = 0.f;
+        for (int jj = 0; jj < nj; ++jj) {
+            const int lo = s_wlo[jj];
+            if (lo < 0) continue;
+            const Anchor a = s_anc[warp * 32 + jj];
+            PairWin p = pair_setup(a, d4, 1.f, k);
+            if (p.amb) {
+                const int j = jb + jj;
+                int nlo, cnt;
+                exact_window(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sens[j], sens[k.Nd + j],
+                             sens[2 * k.Nd + j], p.g_first, p.g_last, k, nlo, cnt);
+                if (cnt > 0) p.e_lo = e_at(a, d4, nlo, k);
+                p.n_lo = nlo;
+                p.cnt = cnt;
+            }
+            if (p.cnt <= 0) continue;
+            if (MODE == 3) {
+                npairs += (perm[gi] >= 0) ? (unsigned long long)p.cnt : 0ull;
+                continue;
+            }
+            const float* rp = s_res + jj * La + (p.n_lo - lo);
+            float P = exp2f(p.e_lo * p.e_lo * k.K1);
+            float q = exp2f(fmaf(p.e_lo, k.K2, k.K3));
+            float part = 0.f;
+#pragma unroll
+            for (int m = 0; m < WMAX; ++m) {
+                if (m < p.cnt) {
+                    const float dm = fmaf(-(float)m, k.h, p.e_lo);
+                    part = fmaf(dm * P, rp[m], part);
+                }
+                P *= q;
+                q *= k.cq;
+            }
+            for (int m = WMAX; m < p.cnt; ++m) {
+                const float dm = fmaf(-(float)m, k.h, p.e_lo);
+                part = fmaf(dm * P, rp[m], part);
+                P *= q;
+                q *= k.cq;
+            }
+            accb = fmaf(p.w, part, accb);
+        }
+        acc += accb;
+    }
+    if (!cok) return;
+    if (MODE == 3) {
+        for (int o = 16; o > 0; o >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, o);
+        if (lane == 0) atomicAdd(count, npairs);
+        return;
+    }
+    const int32_t ic = perm[gi];
+    if (ic < 0) return;
+    const float g = acc * ep.scale;
+    if (MODE == EPI_GRAD) {
+        ep.g_out[ic] = g;
+    } else if (MODE == EPI_NPC_ADAM) {
+        float z = ep.z[ic];
+        const float gz = g * (2.f * (z + ep.eps_npc));              // Eq. 19
+        const float mm = ep.beta1 * ep.m[ic] + (1.f - ep.beta1) * gz;
+        const float vv = ep.beta2 * ep.v[ic] + (1.f - ep.beta2) * gz * gz;
+        const float mh = mm * ep.bc1, vh = vv * ep.bc2;
+        z = z - ep.lr * mh / (sqrtf(vh) + ep.adam_eps);
+        ep.z[ic] = z;
+        ep.m[ic] = mm;
+        ep.v[ic] = vv;
+        if (ep.x_out) ep.x_out[ic] = (z + ep.eps_npc) * (z + ep.eps_npc);
+    } else {  // clamp
+        float x = fmaxf(ep.z[ic] - ep.lr * g, 0.f);
+        ep.z[ic] = x;
+        if (ep.x_out) ep.x_out[ic] = x;
+    }
+}
+
+int pick_wmax(int w) {
+    static const int opts[] = {5, 8, 12, 16, 20, 24, 32, 48, 64};
+    for (int o : opts)
+        if (w <= o) return o;
+    return 64;
+}
+
+template <int W>
+cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
+    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * 16 + (size_t)c->f_warps * c->Lf * 32 * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_forward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(c->f_regions, c->f_sgroups);
+    k_forward<W><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_cell, c->d_orig, c->d_sens,
+                                                      c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
+                                                      c->Mpad, c->k);
+    return cudaGetLastError();
+}
+
+template <int W, int MODE>
+cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    size_t smem = (size_t)c->a_cpr * 32 * sizeof(Anchor) + 32 * 4 + (MODE == 3 ? 0 : (size_t)32 * c->La * 4);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int threads = 32 * std::max(c->a_cpr, 1);
+    k_adjoint<W, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_cell, c->d_orig, c->d_perm, c->d_sens,
+                                                           c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
+                                                           c->k, ep, c->d_count);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    switch (pick_wmax(c->k.wmax)) {
+        case 5: return adj_launch<5, MODE>(c, resid, ep, st);
+        case 8: return adj_launch<8, MODE>(c, resid, ep, st);
+        case 12: return adj_launch<12, MODE>(c, resid, ep, st);
+        case 16: return adj_launch<16, MODE>(c, resid, ep, st);
+        case 20: return adj_launch<20, MODE>(c, resid, ep, st);
+        case 24: return adj_launch<24, MODE>(c, resid, ep, st);
+        case 32: return adj_launch<32, MODE>(c, resid, ep, st);
+        case 48: return adj_launch<48, MODE>(c, resid, ep, st);
+        default: return adj_launch<64, MODE>(c, resid, ep, st);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cudaStream_t st) {
+    k_gather<<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(src, c->d_perm, c->Mpad, npc, eps, c->d_amp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
+    switch (pick_wmax(c->k.wmax)) {
+        case 5: return fwd_launch<5>(c, st);
+        case 8: return fwd_launch<8>(c, st);
+        case 12: return fwd_launch<12>(c, st);
+        case 16: return fwd_launch<16>(c, st);
+        case 20: return fwd_launch<20>(c, st);
+        case 24: return fwd_launch<24>(c, st);
+        case 32: return fwd_launch<32>(c, st);
+        case 48: return fwd_launch<48>(c, st);
+        default: return fwd_launch<64>(c, st);
+    }
+}
+
+cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {
+    int nw = 8;
+    while (nw > 1 && (size_t)nw * c->jlen_max * 4 > 200 * 1024) nw /= 2;
+    size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_wlo_fT, c->d_jlo, c->d_jlen, c->f_regions, c->Lf,
+                                           c->k, y, b, delta, c->d_loss_part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st) {
+    k_residual<<<c->Nd, 256, 0, st>>>(y, b, c->Nt, delta, c->d_loss_part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st) {
+    k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->Nd, 1.0 / ((double)c->Nd * (double)c->Nt), loss_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
+    if (mode == EPI_GRAD) return adj_dispatch<EPI_GRAD>(c, resid, ep, st);
+    if (mode == EPI_NPC_ADAM) return adj_dispatch<EPI_NPC_ADAM>(c, resid, ep, st);
+    return adj_dispatch<EPI_CLAMP>(c, resid, ep, st);
+}
+
+cudaError_t launch_count(gpair_ctx* c, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    EpiParams ep{};
+    return adj_dispatch<3>(c, nullptr, ep, st);
+}
+
+}  // namespace gpair

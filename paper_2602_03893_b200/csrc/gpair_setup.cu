@@ -1,0 +1,417 @@
+// gpair_setup.cu -- create-time geometry processing.
+//
+// 1. Spatial sort: kernels are ordered by the Morton code of their grid
+//    coordinates (exact integer coordinates when the centres form a regular
+//    grid, the paper's voxel lattice P:230; a 1024^3 quantisation otherwise).
+//    Consecutive runs of 32 sorted kernels form a "cell" (4x4x2 voxels on a
+//    grid).  Each cell gets an fp32 anchor C_c (bounding-box centre) and a
+//    conservative radius; each kernel stores delta = c_i - C_c.
+// 2. Regions: runs of cells processed by one forward CTA (partial traces) or
+//    one adjoint CTA (staged residual windows).  For every (region, sensor)
+//    the conservative sample window [lo, hi] of all its pairs is computed in
+//    fp64 from the cell anchors and radii (triangle inequality), together with
+//    the far-field geometry check r_ij > k sigma (reading R2).
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sequence.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "gpair_ctx.h"
+
+namespace gpair {
+
+namespace {
+
+#define SETUP_CHECK(x)                          \
+    do {                                        \
+        cudaError_t e_ = (x);                   \
+        if (e_ != cudaSuccess) return e_;       \
+    } while (0)
+
+__global__ void k_check_finite(const float* __restrict__ c, int64_t n, int* flag) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !isfinite(c[i])) atomicOr(flag, 1);
+}
+
+__device__ __forceinline__ uint64_t spread3(uint64_t x) {
+    x &= 0x1fffffULL;
+    x = (x | x << 32) & 0x1f00000000ffffULL;
+    x = (x | x << 16) & 0x1f0000ff0000ffULL;
+    x = (x | x << 8) & 0x100f00f00f00f00fULL;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+    x = (x | x << 2) & 0x1249249249249249ULL;
+    return x;
+}
+
+// Morton key of the quantised coordinates; grid mode flags non-integer ones.
+__global__ void k_keys(const float* __restrict__ c, int64_t M, double mnx, double mny, double mnz,
+                       double stx, double sty, double stz, int grid_mode, uint64_t* keys,
+                       int32_t* vals, int* nonint) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double u[3] = {((double)c[i] - mnx) / stx, ((double)c[M + i] - mny) / sty,
+                   ((double)c[2 * M + i] - mnz) / stz};
+    uint64_t key = 0;
+    for (int a = 0; a < 3; ++a) {
+        double q = grid_mode ? rint(u[a]) : floor(u[a]);
+        if (grid_mode && fabs(u[a] - q) > 1e-3) atomicOr(nonint, 1);
+        q = fmin(fmax(q, 0.0), 2097151.0);
+        key |= spread3((uint64_t)q) << a;
+    }
+    keys[i] = key;
+    vals[i] = (int32_t)i;
+}
+
+// One warp per 32-kernel cell: anchor, radius, per-kernel offsets.
+__global__ void k_cells(const float* __restrict__ c, int64_t M, const int32_t* __restrict__ sorted,
+                        int32_t ncells, float4* kd, float4* cell, float* orig, int32_t* perm) {
+    int cid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int lane = threadIdx.x & 31;
+    if (cid >= ncells) return;
+    int64_t i = (int64_t)cid * CELL + lane;
+    int64_t Mpad = (int64_t)ncells * CELL;
+    bool real = i < M;
+    int32_t idx = real ? sorted[i] : -1;
+    int32_t idx0 = __shfl_sync(0xffffffffu, idx, 0);
+    int32_t src = real ? idx : idx0;
+    float x = c[src], y = c[M + src], z = c[2 * M + src];
+    float mnx = x, mny = y, mnz = z, mxx = x, mxy = y, mxz = z;
+    for (int o = 16; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+    }
+    float Cx = (float)(0.5 * ((double)mnx + (double)mxx));
+    float Cy = (float)(0.5 * ((double)mny + (double)mxy));
+    float Cz = (float)(0.5 * ((double)mnz + (double)mxz));
+    if (!real) { x = Cx; y = Cy; z = Cz; }
+    double dx = (double)x - (double)Cx, dy = (double)y - (double)Cy, dz = (double)z - (double)Cz;
+    double rad = sqrt(dx * dx + dy * dy + dz * dz);
+    for (int o = 16; o > 0; o >>= 1) rad = fmax(rad, __shfl_xor_sync(0xffffffffu, rad, o));
+    float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
+    double d2 = (double)fdx * fdx + (double)fdy * fdy + (double)fdz * fdz;
+    kd[i] = make_float4(fdx, fdy, fdz, (float)d2);
+    orig[i] = x;
+    orig[Mpad + i] = y;
+    orig[2 * Mpad + i] = z;
+    perm[i] = idx;
+    if (lane == 0) {
+        // conservative radius: round up and add a relative + absolute margin
+        float r32 = (float)(rad * (1.0 + 1e-6) + 1e-12);
+        cell[cid] = make_float4(Cx, Cy, Cz, r32);
+    }
+}
+
+// fp64 conservative sample window of all pairs of a cell with one sensor.
+__device__ __forceinline__ bool cell_window(float4 C, float sx, float sy, float sz, const OpConst& k,
+                                            int& lo, int& hi, double& R) {
+    double dx = (double)C.x - sx, dy = (double)C.y - sy, dz = (double)C.z - sz;
+    R = sqrt(dx * dx + dy * dy + dz * dz);
+    double rad = C.w;
+    double a = floor(((R - rad - k.ks) / k.v - k.t0) * k.fs) - 1.0;
+    double b = ceil(((R + rad + k.ks) / k.v - k.t0) * k.fs) + 1.0;
+    a = fmax(a, 0.0);
+    b = fmin(b, (double)(k.Nt - 1));
+    if (a > b) return false;
+    lo = (int)a;
+    hi = (int)b;
+    return true;
+}
+
+// Thread per (region, sensor): union window over the region's cells.
+// check != 0 also performs the geometry check and the anchor-expansion bound.
+__global__ void k_region_windows(const float4* __restrict__ cell, int32_t ncells,
+                                 const float* __restrict__ sens, int32_t cpr, int32_t nregions,
+                                 OpConst k, int32_t* wlo, int* maxlen, int check, int* geom_bad,
+                                 unsigned int* max_eps_bits) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= (int64_t)nregions * k.Nd) return;
+    int j = (int)(t % k.Nd);
+    int r = (int)(t / k.Nd);
+    float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
+    int lo = INT_MAX, hi = INT_MIN;
+    float eps_max = 0.f;
+    int bad = 0;
+    int c1 = min((r + 1) * cpr, ncells);
+    for (int cc = r * cpr; cc < c1; ++cc) {
+        float4 C = cell[cc];
+        int a, b;
+        double R;
+        if (cell_window(C, sx, sy, sz, k, a, b, R)) {
+            lo = min(lo, a);
+            hi = max(hi, b);
+        }
+        if (check) {
+            if (!(R - (double)C.w > k.ks)) bad = 1;
+            double e = (2.0 * R * C.w + (double)C.w * C.w) / (R * R);
+            eps_max = fmaxf(eps_max, (float)e);
+        }
+    }
+    int len = 0;
+    if (lo <= hi) {
+        wlo[(int64_t)r * k.Nd + j] = lo;
+        len = hi - lo + 1;
+    } else {
+        wlo[(int64_t)r * k.Nd + j] = -1;
+    }
+    atomicMax(maxlen, len);
+    if (check) {
+        if (bad) atomicOr(geom_bad, 1);
+        atomicMax(max_eps_bits, __float_as_uint(eps_max));
+    }
+}
+
+// Thread per sensor: live range of the forward partial windows (reducer) and
+// the transposed window table.
+__global__ void k_reducer_tables(const int32_t* __restrict__ wlo, int32_t nregions, int32_t Nd,
+                                 int32_t Nt, int32_t Lf, int32_t* wloT, int32_t* jlo, int32_t* jlen,
+                                 int* jlen_max) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Nd) return;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (int r = 0; r < nregions; ++r) {
+        int a = wlo[(int64_t)r * Nd + j];
+        wloT[(int64_t)j * nregions + r] = a;
+        if (a >= 0) {
+            lo = min(lo, a);
+            hi = max(hi, min(a + Lf - 1, Nt - 1));
+        }
+    }
+    if (lo > hi) {
+        jlo[j] = 0;
+        jlen[j] = 0;
+    } else {
+        jlo[j] = lo;
+        jlen[j] = hi - lo + 1;
+        atomicMax(jlen_max, hi - lo + 1);
+    }
+}
+
+template <class T>
+cudaError_t dmalloc(gpair_ctx* c, T** p, size_t n) {
+    size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc((void**)p, bytes);
+    if (e == cudaSuccess) c->workspace_bytes += (int64_t)bytes;
+    return e;
+}
+
+}  // namespace
+
+cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sensors, cudaStream_t st,
+                           std::string& why, int& geom_err) {
+    geom_err = 0;
+    const int64_t M = c->M;
+    const int Nd = c->Nd;
+    auto pol = thrust::cuda::par.on(st);
+
+    SETUP_CHECK(dmalloc(c, &c->d_flags, 8));
+    SETUP_CHECK(cudaMemsetAsync(c->d_flags, 0, 8 * sizeof(int32_t), st));
+    SETUP_CHECK(dmalloc(c, &c->d_sens, (size_t)3 * Nd));
+    SETUP_CHECK(cudaMemcpyAsync(c->d_sens, sensors, sizeof(float) * 3 * Nd, cudaMemcpyDeviceToDevice, st));
+    k_check_finite<<<(unsigned)((3 * M + 255) / 256), 256, 0, st>>>(centers, 3 * M, c->d_flags);
+    k_check_finite<<<(unsigned)((3 * Nd + 255) / 256), 256, 0, st>>>(c->d_sens, 3 * Nd, c->d_flags);
+    SETUP_CHECK(cudaGetLastError());
+    int h_flags[8];
+    SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+    SETUP_CHECK(cudaStreamSynchronize(st));
+    if (h_flags[0]) {
+        why = "non-finite centre or sensor coordinate";
+        geom_err = GPAIR_ERR_INVALID_ARGUMENT;
+        return cudaSuccess;
+    }
+
+    // ---- per-axis unique values -> grid detection
+    float* tmp = nullptr;
+    SETUP_CHECK(cudaMalloc(&tmp, sizeof(float) * M));
+    double mn[3], st3[3];
+    int64_t nu[3];
+    for (int a = 0; a < 3; ++a) {
+        SETUP_CHECK(cudaMemcpyAsync(tmp, centers + a * M, sizeof(float) * M, cudaMemcpyDeviceToDevice, st));
+        thrust::device_ptr<float> p(tmp);
+        thrust::sort(pol, p, p + M);
+        int64_t n = thrust::unique(pol, p, p + M) - p;
+        float lo_hi[2];
+        SETUP_CHECK(cudaMemcpyAsync(&lo_hi[0], tmp, sizeof(float), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaMemcpyAsync(&lo_hi[1], tmp + n - 1, sizeof(float), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        nu[a] = n;
+        mn[a] = lo_hi[0];
+        double ext = (double)lo_hi[1] - (double)lo_hi[0];
+        st3[a] = ext;  // extent for now
+    }
+    cudaFree(tmp);
+    int grid_mode = (nu[0] * nu[1] * nu[2] == M) ? 1 : 0;
+    double step[3];
+    double ext_max = std::max(st3[0], std::max(st3[1], st3[2]));
+    for (int a = 0; a < 3; ++a) {
+        if (grid_mode)
+            step[a] = nu[a] > 1 ? st3[a] / (double)(nu[a] - 1) : 1.0;
+        else
+            step[a] = ext_max > 0 ? ext_max / 1023.0 : 1.0;
+    }
+
+    uint64_t* keys = nullptr;
+    int32_t* vals = nullptr;
+    SETUP_CHECK(cudaMalloc(&keys, sizeof(uint64_t) * M));
+    SETUP_CHECK(cudaMalloc(&vals, sizeof(int32_t) * M));
+    unsigned nb = (unsigned)((M + 255) / 256);
+    k_keys<<<nb, 256, 0, st>>>(centers, M, mn[0], mn[1], mn[2], step[0], step[1], step[2], grid_mode,
+                               keys, vals, c->d_flags + 1);
+    SETUP_CHECK(cudaGetLastError());
+    if (grid_mode) {
+        int nonint = 0;
+        SETUP_CHECK(cudaMemcpyAsync(&nonint, c->d_flags + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        if (nonint) {
+            grid_mode = 0;
+            for (int a = 0; a < 3; ++a) step[a] = ext_max > 0 ? ext_max / 1023.0 : 1.0;
+            k_keys<<<nb, 256, 0, st>>>(centers, M, mn[0], mn[1], mn[2], step[0], step[1], step[2], 0,
+                                       keys, vals, c->d_flags + 1);
+            SETUP_CHECK(cudaGetLastError());
+        }
+    }
+    c->grid_detected = grid_mode;
+    {
+        thrust::device_ptr<uint64_t> kp(keys);
+        thrust::device_ptr<int32_t> vp(vals);
+        thrust::stable_sort_by_key(pol, kp, kp + M, vp);
+    }
+
+    // ---- cells
+    c->ncells = (int32_t)((M + CELL - 1) / CELL);
+    c->Mpad = (int64_t)c->ncells * CELL;
+    SETUP_CHECK(dmalloc(c, &c->d_kd, c->Mpad));
+    SETUP_CHECK(dmalloc(c, &c->d_cell, c->ncells));
+    SETUP_CHECK(dmalloc(c, &c->d_orig, 3 * c->Mpad));
+    SETUP_CHECK(dmalloc(c, &c->d_perm, c->Mpad));
+    k_cells<<<(c->ncells + 7) / 8, 256, 0, st>>>(centers, M, vals, c->ncells, c->d_kd, c->d_cell, c->d_orig,
+                                                 c->d_perm);
+    SETUP_CHECK(cudaGetLastError());
+    cudaFree(keys);
+    cudaFree(vals);
+
+    // ---- forward regions: sized for >= ~4 CTAs per SM of work and smem fit
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->f_warps = std::min(8, (Nd + 31) / 32);
+    c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
+    int cpr = 128;
+    while (cpr > 1 && (int64_t)((c->ncells + cpr - 1) / cpr) * c->f_sgroups < 4LL * dev_sms) cpr /= 2;
+    const size_t smem_limit = 220 * 1024;
+    for (;;) {
+        int nreg = (c->ncells + cpr - 1) / cpr;
+        int32_t* wlo = nullptr;
+        SETUP_CHECK(cudaMalloc(&wlo, sizeof(int32_t) * (size_t)nreg * Nd));
+        SETUP_CHECK(cudaMemsetAsync(c->d_flags + 2, 0, 6 * sizeof(int32_t), st));
+        int64_t nt = (int64_t)nreg * Nd;
+        k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+            c->d_cell, c->ncells, c->d_sens, cpr, nreg, c->k, wlo, c->d_flags + 2, 1, c->d_flags + 3,
+            (unsigned int*)(c->d_flags + 4));
+        SETUP_CHECK(cudaGetLastError());
+        SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        if (h_flags[3]) {
+            cudaFree(wlo);
+            why = "some kernel-sensor distance r_ij <= k*sigma (checked per 32-kernel cell): the far-field "
+                  "Eq. 7 model does not apply";
+            geom_err = GPAIR_ERR_GEOMETRY;
+            return cudaSuccess;
+        }
+        float me;
+        unsigned bits = (unsigned)h_flags[4];
+        memcpy(&me, &bits, 4);
+        c->max_eps = me;
+        if (me > 0.08f) {
+            cudaFree(wlo);
+            why = "kernel cells too large relative to the sensor distance for the anchored time-of-flight "
+                  "expansion (max |q|/R^2 > 0.08)";
+            geom_err = GPAIR_ERR_GEOMETRY;
+            return cudaSuccess;
+        }
+        int L = std::max(h_flags[2], 1);
+        int Lf = (L + 31) / 32 * 32;
+        size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * 16;
+        if (smem > smem_limit && cpr > 1) {
+            cudaFree(wlo);
+            cpr /= 2;
+            continue;
+        }
+        if (smem > smem_limit) {
+            cudaFree(wlo);
+            why = "per-sensor sample window of a single cell does not fit in shared memory";
+            geom_err = GPAIR_ERR_RESOURCE;
+            return cudaSuccess;
+        }
+        c->f_cpr = cpr;
+        c->f_regions = nreg;
+        c->Lf = Lf;
+        c->d_wlo_f = wlo;
+        c->workspace_bytes += sizeof(int32_t) * (int64_t)nreg * Nd;
+        break;
+    }
+    // reducer tables
+    SETUP_CHECK(dmalloc(c, &c->d_wlo_fT, (size_t)c->f_regions * Nd));
+    SETUP_CHECK(dmalloc(c, &c->d_jlo, Nd));
+    SETUP_CHECK(dmalloc(c, &c->d_jlen, Nd));
+    SETUP_CHECK(cudaMemsetAsync(c->d_flags + 5, 0, sizeof(int32_t), st));
+    k_reducer_tables<<<(Nd + 127) / 128, 128, 0, st>>>(c->d_wlo_f, c->f_regions, Nd, c->Nt, c->Lf,
+                                                       c->d_wlo_fT, c->d_jlo, c->d_jlen, c->d_flags + 5);
+    SETUP_CHECK(cudaGetLastError());
+
+    // ---- adjoint regions
+    int acpr = 8;
+    while (acpr > 1 && (c->ncells + acpr - 1) / acpr < 4 * dev_sms) acpr /= 2;
+    for (;;) {
+        int nreg = (c->ncells + acpr - 1) / acpr;
+        int32_t* wlo = nullptr;
+        SETUP_CHECK(cudaMalloc(&wlo, sizeof(int32_t) * (size_t)nreg * Nd));
+        SETUP_CHECK(cudaMemsetAsync(c->d_flags + 6, 0, sizeof(int32_t), st));
+        int64_t nt = (int64_t)nreg * Nd;
+        k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
+            c->d_cell, c->ncells, c->d_sens, acpr, nreg, c->k, wlo, c->d_flags + 6, 0, nullptr, nullptr);
+        SETUP_CHECK(cudaGetLastError());
+        SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        int La = (std::max(h_flags[6], 1) + 3) / 4 * 4;
+        size_t smem = (size_t)32 * La * 4 + (size_t)acpr * 32 * sizeof(Anchor) + 32 * 4;
+        if (smem > 96 * 1024 && acpr > 1) {
+            cudaFree(wlo);
+            acpr /= 2;
+            continue;
+        }
+        if (smem > smem_limit) {
+            cudaFree(wlo);
+            why = "per-sensor residual window of a cell does not fit in shared memory";
+            geom_err = GPAIR_ERR_RESOURCE;
+            return cudaSuccess;
+        }
+        c->a_cpr = acpr;
+        c->a_regions = nreg;
+        c->La = La;
+        c->d_wlo_a = wlo;
+        c->workspace_bytes += sizeof(int32_t) * (int64_t)nreg * Nd;
+        c->jlen_max = h_flags[5];
+        break;
+    }
+
+    // ---- workspaces
+    SETUP_CHECK(dmalloc(c, &c->d_partial, (size_t)c->f_regions * Nd * c->Lf));
+    SETUP_CHECK(dmalloc(c, &c->d_amp, c->Mpad));
+    SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
+    SETUP_CHECK(dmalloc(c, &c->d_delta, (size_t)Nd * c->Nt));
+    SETUP_CHECK(dmalloc(c, &c->d_loss_part, Nd));
+    SETUP_CHECK(dmalloc(c, &c->d_count, 1));
+    SETUP_CHECK(cudaStreamSynchronize(st));
+    return cudaSuccess;
+}
+
+}  // namespace gpair

@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle.
+
+Gate (north_star / SURVEY 8c): relative L2 <= 1e-5 on signals and gradients
+and max elementwise relative error <= 1e-4 over entries with
+|oracle| >= 1e-3 max|oracle|.  Forward rows (sensors) and adjoint columns
+(kernels) of the operator are independent, so at full size the oracle is run
+on exact row / column subsets with the context built exactly as bench.py
+builds it.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from oracle import ir  # noqa: E402
+from paper_2602_03893_b200 import gpair, inputs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 1e-5
+REL_ELEM = 1e-4
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_03893_b200 import build
+
+    build.build()
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def compare(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    nref = np.linalg.norm(ref)
+    rel = np.linalg.norm(got - ref) / nref if nref > 0 else np.linalg.norm(got)
+    big = np.abs(ref) >= 1e-3 * np.abs(ref).max() if nref > 0 else np.zeros(ref.shape, bool)
+    elem = float(np.max(np.abs(got[big] - ref[big]) / np.abs(ref[big]))) if big.any() else 0.0
+    return rel, elem
+
+
+def assert_parity(got, ref, what):
+    rel, elem = compare(got, ref)
+    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e}"
+    assert elem <= REL_ELEM, f"{what}: max elementwise rel {elem:.3e}"
+    return rel, elem
+
+
+def make_ctx(c, s, op):
+    return gpair.Context(T(c), T(s), sigma=op["sigma"], v=op["v"], fs=op["fs"], n_samples=op["n_samples"],
+                         t0=op["t0"], k=op["k"])
+
+
+def adj_kw(op):
+    return {k: v for k, v in op.items() if k != "n_samples"}
+
+
+# ----------------------------------------------------------------- config 1
+def test_cfg1_forward_adjoint_full():
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    x = inputs.dense_amplitudes(cfg.M)
+    y = ctx.forward(T(x)).cpu().numpy()
+    assert_parity(y, oracle.forward(c, x, s, **op), "cfg1 forward")
+    d = inputs.residual(cfg.n_sensors, cfg.n_samples)
+    g = ctx.adjoint(T(d)).cpu().numpy()
+    assert_parity(g, oracle.adjoint(c, d, s, **adj_kw(op)), "cfg1 adjoint")
+    assert ctx.count_pair_samples() == oracle.count_pair_samples(c, s, **op)
+
+
+def test_cfg1_vessel_phantom_and_single_kernel():
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    for x in (inputs.vessel_phantom(*cfg.grid), np.eye(1, cfg.M, 137, dtype=np.float32)[0]):
+        if not np.any(x):
+            continue
+        y = ctx.forward(T(x)).cpu().numpy()
+        assert_parity(y, oracle.forward(c, x, s, **op), "cfg1 forward phantom")
+
+
+# ----------------------------------------------------------------- random suite
+@pytest.mark.parametrize("seed", range(20))
+def test_random_suite(seed):
+    c, s, op = inputs.random_suite_case(seed)
+    rng = np.random.default_rng(seed)
+    ctx = make_ctx(c, s, op)
+    x = rng.random(c.shape[1]).astype(np.float32)
+    y_ref = oracle.forward(c, x, s, **op)
+    if np.linalg.norm(y_ref) > 0:
+        assert_parity(ctx.forward(T(x)).cpu().numpy(), y_ref, f"seed {seed} forward")
+    d = rng.standard_normal((s.shape[1], op["n_samples"])).astype(np.float32)
+    g_ref = oracle.adjoint(c, d, s, **adj_kw(op))
+    if np.linalg.norm(g_ref) > 0:
+        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_ref, f"seed {seed} adjoint")
+    assert ctx.count_pair_samples() == oracle.count_pair_samples(c, s, **op)
+
+
+# ----------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("M", [1, 31, 33, 100])
+def test_ragged_kernel_counts(M):
+    rng = np.random.default_rng(M)
+    c = (rng.uniform(-0.4e-3, 0.4e-3, (3, M))).astype(np.float32)
+    s = inputs.hemisphere(37, 12.8e-3)
+    op = dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=400, t0=0.5e-6, k=3.0)
+    ctx = make_ctx(c, s, op)
+    x = rng.random(M).astype(np.float32)
+    assert_parity(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), "ragged forward")
+    d = rng.standard_normal((37, 400)).astype(np.float32)
+    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "ragged adjoint")
+
+
+def test_windows_clipped_by_record_and_empty_sensors():
+    """Record shorter than some windows (clip, reading R8) and sensors whose
+    windows lie entirely outside the record (empty rows)."""
+    c = inputs.grid_centers(6, 6, 6, 1e-4)
+    s = np.concatenate([inputs.hemisphere(40, 10e-3), inputs.hemisphere(9, 20e-3)], axis=1)
+    op = dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=int(10e-3 / 1500 * 40e6), t0=0.0, k=3.0)
+    ctx = make_ctx(c, s, op)
+    x = inputs.dense_amplitudes(c.shape[1])
+    y = ctx.forward(T(x)).cpu().numpy()
+    y_ref = oracle.forward(c, x, s, **op)
+    assert np.all(y[40:] == 0)
+    assert_parity(y, y_ref, "clipped forward")
+    d = inputs.residual(s.shape[1], op["n_samples"])
+    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "clipped adjoint")
+
+
+def test_geometry_error():
+    c = inputs.grid_centers(4, 4, 4, 1e-4)
+    s = np.array([[0.0], [0.0], [2e-4]], np.float32)  # inside k sigma of a kernel
+    with pytest.raises(gpair.GpairError) as ei:
+        make_ctx(c, s, dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=100, t0=0.0, k=3.0))
+    assert ei.value.status == gpair.ERR_GEOMETRY
+
+
+# ----------------------------------------------------------------- self-consistency
+def test_gpu_dot_test_and_determinism():
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    rng = np.random.default_rng(5)
+    x = T(rng.standard_normal(cfg.M).astype(np.float32))
+    d = T(rng.standard_normal((cfg.n_sensors, cfg.n_samples)).astype(np.float32))
+    Ax = ctx.forward(x)
+    ATd = ctx.adjoint(d)
+    lhs = float((Ax.double() * d.double()).sum())
+    rhs = float((x.double() * ATd.double()).sum())
+    assert abs(lhs - rhs) / (Ax.double().norm() * d.double().norm()) <= 1e-6
+    assert torch.equal(ctx.forward(x), Ax)
+    assert torch.equal(ctx.adjoint(d), ATd)
+
+
+def test_shard_sum_invariance():
+    """Kernel sharding emulated on one device: forward of the two
+    shards sums to the full forward; adjoint shards are slices of the full one."""
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    x = inputs.dense_amplitudes(cfg.M)
+    d = inputs.residual(cfg.n_sensors, cfg.n_samples)
+    full = make_ctx(c, s, op)
+    y_full = full.forward(T(x)).cpu().numpy().astype(np.float64)
+    g_full = full.adjoint(T(d)).cpu().numpy()
+    half = cfg.M // 2
+    y_sum = np.zeros_like(y_full)
+    for sl in (slice(0, half), slice(half, None)):
+        ctx = make_ctx(np.ascontiguousarray(c[:, sl]), s, op)
+        y_sum += ctx.forward(T(x[sl])).cpu().numpy()
+        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_full[sl], "shard adjoint")
+    assert_parity(y_sum, y_full, "shard forward sum")
+
+
+# ----------------------------------------------------------------- IR iteration
+@pytest.mark.parametrize("mode", [0, 1])
+def test_iterate_one_step_teacher_forced(mode):
+    """One Algorithm-2 iteration from an oracle state (reading R12): loss,
+    signals, and the updated state (z, m, v) match the oracle."""
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    rng = np.random.default_rng(11)
+    x_true = inputs.vessel_phantom(*cfg.grid) + 0.1 * rng.random(cfg.M).astype(np.float32)
+    b = oracle.forward(c, x_true, s, **op).astype(np.float32)
+    z0 = rng.uniform(0.2, 0.9, cfg.M).astype(np.float32)
+    m0 = (1e-3 * rng.standard_normal(cfg.M)).astype(np.float32)
+    v0 = (1e-6 * rng.random(cfg.M)).astype(np.float32)
+    t_step = 7
+    lr = gpair.cawr_lr(t_step - 1, 1e-4, 0.1, 50, 1)
+    zt, mt, vt = T(z0), T(m0), T(v0)
+    y_out = torch.empty((cfg.n_sensors, cfg.n_samples), device=dev())
+    x_out = torch.empty(cfg.M, device=dev())
+    loss = torch.empty(1, device=dev())
+    ctx.iterate(zt, mt, vt, T(b), lr=lr, step=t_step, mode=mode, signals_out=y_out, x_out=x_out, loss_out=loss)
+    torch.cuda.synchronize()
+    geom = {"centers": c, "sensors": s, "op": op}
+    hp = ir.Hyper(mode="npc" if mode == 0 else "clamp")
+    L_ref, gz_ref, y_ref = ir.loss_and_grad(z0.astype(np.float64), b.astype(np.float64), geom, hp)
+    assert_parity(y_out.cpu().numpy(), y_ref, "iterate signals")
+    assert abs(loss.item() - L_ref) / L_ref <= 1e-5
+    if mode == 0:
+        z_ref, m_ref, v_ref = ir.adam_update(z0.astype(np.float64), m0.astype(np.float64),
+                                             v0.astype(np.float64), gz_ref, lr, t_step, hp)
+        assert_parity(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, "Adam m increment (= 0.1 dL/dz)")
+        assert_parity(vt.cpu().numpy(), v_ref, "Adam v")
+        assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "Adam z step")
+        assert_parity(x_out.cpu().numpy(), ir.npc(z_ref), "x_out")
+    else:
+        x_ref = np.maximum(z0 - lr * gz_ref, 0.0)
+        assert_parity(zt.cpu().numpy(), x_ref, "clamp step")
+
+
+def test_iterate_trajectory_cfg1_reports_loss_decrease():
+    """Multi-iteration run (reported, not gated at 1e-5; reading R12): the GPU
+    loss trajectory tracks the oracle's and decreases."""
+    cfg = inputs.CONFIGS["cfg1"]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    x_true = inputs.vessel_phantom(*cfg.grid)
+    b = oracle.forward(c, x_true, s, **op).astype(np.float32)
+    hp = ir.Hyper(eta_max=0.05, T0=20)
+    zt = torch.zeros(cfg.M, device=dev())
+    mt = torch.zeros_like(zt)
+    vt = torch.zeros_like(zt)
+    bt = T(b)
+    loss = torch.empty(1, device=dev())
+    gl = []
+    for t in range(20):
+        lr = gpair.cawr_lr(t, hp.eta_min, hp.eta_max, hp.T0, hp.Tmult)
+        ctx.iterate(zt, mt, vt, bt, lr=lr, step=t + 1, loss_out=loss)
+        gl.append(loss.item())
+    _, st = ir.run(b.astype(np.float64), {"centers": c, "sensors": s, "op": op}, hp, 20)
+    ol = np.array(st.losses)
+    gl = np.array(gl)
+    assert gl[-1] <= gl[0]
+    assert np.max(np.abs(gl - ol) / ol) < 1e-2
+
+
+# ----------------------------------------------------------------- full size, sampled
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_full_size_sampled_rows(name):
+    """At the bench's size and launch configuration: exact oracle rows for a
+    sensor subset (forward) and exact columns for a kernel subset (adjoint)."""
+    cfg = inputs.CONFIGS[name]
+    c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+    ctx = make_ctx(c, s, op)
+    x = inputs.dense_amplitudes(cfg.M)
+    y = ctx.forward(T(x)).cpu().numpy()
+    rows = np.array(sorted({0, 1, cfg.n_sensors // 3, cfg.n_sensors // 2, cfg.n_sensors - 1}), np.int32)
+    assert_parity(y[rows], oracle.forward(c, x, s, rows=rows, **op), f"{name} forward rows")
+    d = inputs.residual(cfg.n_sensors, cfg.n_samples)
+    g = ctx.adjoint(T(d)).cpu().numpy()
+    cols = np.random.default_rng(4).choice(cfg.M, 2048, replace=False).astype(np.int64)
+    assert_parity(g[cols], oracle.adjoint(c, d, s, cols=cols, **adj_kw(op)), f"{name} adjoint cols")
+    info = ctx.info()
+    assert info["grid_detected"] == 1
