@@ -119,6 +119,7 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_sens);
     cudaFree(c->d_kd);
     cudaFree(c->d_cell);
+    cudaFree(c->d_grp);
     cudaFree(c->d_orig);
     cudaFree(c->d_perm);
     cudaFree(c->d_wlo_f);
@@ -233,13 +234,9 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     double Lr = std::nearbyint(Lw);
     int wmax = (std::fabs(Lw - Lr) < 1e-6 * std::max(1.0, Lw)) ? (int)Lr : (int)std::ceil(Lw);
     k.wmax = std::max(wmax, 1);
-    k.h = (float)h;
-    k.inv_h = (float)(1.0 / h);
-    k.ksf = (float)k.ks;
-    k.K1 = (float)(-log2e / (2.0 * s * s));
-    k.K2 = (float)(log2e * h / (s * s));
-    k.K3 = (float)(-log2e * h * h / (2.0 * s * s));
-    k.cq = (float)std::exp(-h * h / (s * s));
+    k.h = h;
+    k.ku = (float)(k.ks / h);
+    k.K1u = (float)(-log2e * h * h / (2.0 * s * s));
 
     gpair_ctx* c = new (std::nothrow) gpair_ctx();
     if (!c) return fail(nullptr, GPAIR_ERR_RESOURCE, "host allocation failed");

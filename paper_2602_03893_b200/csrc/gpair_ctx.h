@@ -27,7 +27,8 @@ struct gpair_ctx_s {
     // geometry in the internal (spatially sorted) order
     float* d_sens = nullptr;   // [3][Nd]
     float4* d_kd = nullptr;    // [Mpad] (dx, dy, dz, |d|^2) relative to the cell anchor
-    float4* d_cell = nullptr;  // [ncells] (Cx, Cy, Cz, radius) fp32 anchor + conservative radius
+    float4* d_cell = nullptr;  // [ncells] (Cx, Cy, Cz, radius): 32-kernel cell bounds (windows)
+    float4* d_grp = nullptr;   // [ncells*4] (Cx, Cy, Cz, radius): 8-kernel group ToF anchors
     float* d_orig = nullptr;   // [3][Mpad] original fp32 centres (exact fp64 window fix-up)
     int32_t* d_perm = nullptr; // [Mpad] sorted -> caller index, -1 = padding
 

@@ -17,7 +17,7 @@
 //                   shared memory and read per lane (gather only, no atomics);
 //                   the epilogue writes g or applies the fused NPC chain rule
 //                   (Eq. 19) + Adam, or the projected clamp step.
-#include <cfloat>
+#include <algorithm>
 
 #include "gpair_ctx.h"
 
@@ -26,6 +26,12 @@ namespace gpair {
 namespace {
 
 constexpr int STAGE_CELLS = 8;  // cells staged per forward pipeline step
+
+__device__ __forceinline__ float ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 __global__ void k_gather(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t Mpad,
                          int npc, float eps, float* __restrict__ amp) {
@@ -43,14 +49,14 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 // ------------------------------------------------------------------ forward
 template <int WMAX>
 __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
-                                                 const float4* __restrict__ cell, const float* __restrict__ orig,
+                                                 const float4* __restrict__ grp, const float* __restrict__ orig,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  float* __restrict__ partial, int32_t cpr, int32_t ncells,
                                                  int32_t Lf, int64_t Mpad, OpConst k) {
     extern __shared__ float4 smem4[];
     float4* s_kd = smem4;                                   // [STAGE_CELLS*32]
-    float4* s_cell = s_kd + STAGE_CELLS * CELL;             // [STAGE_CELLS]
-    float* s_amp = (float*)(s_cell + STAGE_CELLS);          // [STAGE_CELLS*32]
+    float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
+    float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_acc = s_amp + STAGE_CELLS * CELL + (size_t)warp * Lf * 32;
 
@@ -74,43 +80,36 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
             s_kd[t] = kd[(int64_t)cb * CELL + t];
             s_amp[t] = amp[(int64_t)cb * CELL + t];
         }
-        if (threadIdx.x < nc) s_cell[threadIdx.x] = cell[cb + threadIdx.x];
+        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
         __syncthreads();
-        if (lo_j < 0) continue;
-        for (int cc = 0; cc < nc; ++cc) {
-            const float4 C = s_cell[cc];
-            const Anchor a = make_anchor(C.x, C.y, C.z, sx, sy, sz, k);
-            for (int t = 0; t < CELL; ++t) {
-                const float4 d4 = s_kd[cc * CELL + t];
-                const float A = s_amp[cc * CELL + t];
-                PairWin p = pair_setup(a, d4, A, k);
-                if (p.amb) {
-                    const int64_t gi = (int64_t)(cb + cc) * CELL + t;
-                    int nlo, cnt;
-                    exact_window(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, p.g_first,
-                                 p.g_last, k, nlo, cnt);
-                    if (cnt > 0) p.e_lo = e_at(a, d4, nlo, k);
-                    p.n_lo = nlo;
-                    p.cnt = cnt;
-                }
+        for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            for (int t = 0; t < GROUP; ++t) {
+                const int li = gq * GROUP + t;
+                const PairWin p = pair_setup(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy,
+                                             sz, k);
                 if (p.cnt <= 0) continue;
                 float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
-                float P = p.w * exp2f(p.e_lo * p.e_lo * k.K1);
-                float q = exp2f(fmaf(p.e_lo, k.K2, k.K3));
+                if (p.cnt == WMAX) {  // common case: no per-sample predicates
 #pragma unroll
-                for (int m = 0; m < WMAX; ++m) {
-                    if (m < p.cnt) {
-                        const float dm = fmaf(-(float)m, k.h, p.e_lo);
-                        ap[m * 32] = fmaf(dm, P, ap[m * 32]);
+                    for (int m = 0; m < WMAX; ++m) {
+                        const float um = p.u_lo - (float)m;
+                        const float g = ex2((um * k.K1u) * um);
+                        ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
                     }
-                    P *= q;
-                    q *= k.cq;
-                }
-                for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
-                    const float dm = fmaf(-(float)m, k.h, p.e_lo);
-                    ap[m * 32] = fmaf(dm, P, ap[m * 32]);
-                    P *= q;
-                    q *= k.cq;
+                } else {
+#pragma unroll
+                    for (int m = 0; m < WMAX; ++m) {
+                        if (m < p.cnt) {
+                            const float um = p.u_lo - (float)m;
+                            const float g = ex2((um * k.K1u) * um);
+                            ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
+                        }
+                    }
+                    for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
+                        const float um = p.u_lo - (float)m;
+                        ap[m * 32] = fmaf(p.w * um, ex2((um * k.K1u) * um), ap[m * 32]);
+                    }
                 }
             }
         }
@@ -238,40 +237,43 @@ __global__ void k_loss(const double* __restrict__ part, int32_t n, double inv_N,
 }
 
 // ------------------------------------------------------------------ adjoint
+constexpr int MODE_COUNT = 3;
+
 template <int WMAX, int MODE>
-__global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, const float4* __restrict__ cell,
+__global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                  const float* __restrict__ orig, const int32_t* __restrict__ perm,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  const float* __restrict__ resid, int32_t cpr, int32_t ncells,
                                                  int32_t La, int64_t Mpad, OpConst k, EpiParams ep,
                                                  unsigned long long* count) {
     extern __shared__ float4 smem4[];
-    Anchor* s_anc = (Anchor*)smem4;                          // [nw][32]
+    Anchor* s_anc = (Anchor*)smem4;                          // [nw][GPC][33]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t* s_wlo = (int32_t*)(s_anc + nw * 32);           // [32]
+    int32_t* s_wlo = (int32_t*)(s_anc + nw * GPC * 33);     // [32]
     float* s_res = (float*)(s_wlo + 32);                     // [32][La]
 
     const int cid = blockIdx.x * cpr + warp;
     const bool cok = (warp < cpr) && (cid < ncells);
     const int64_t gi = (int64_t)cid * CELL + lane;
     float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 C = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (cok) {
-        d4 = kd[gi];
-        C = cell[cid];
-    }
+    if (cok) d4 = kd[gi];
+    const Anchor* my_anc = s_anc + (warp * GPC + lane / GROUP) * 33;
     float acc = 0.f;
     unsigned long long npairs = 0;
+    const bool real = cok && perm[gi] >= 0;
     for (int jb = 0; jb < k.Nd; jb += 32) {
         const int nj = min(32, k.Nd - jb);
         __syncthreads();
         if (threadIdx.x < 32) s_wlo[threadIdx.x] = threadIdx.x < nj ? wlo[(int64_t)blockIdx.x * k.Nd + jb + threadIdx.x] : -1;
         if (cok && lane < nj) {
             const int j = jb + lane;
-            s_anc[warp * 32 + lane] = make_anchor(C.x, C.y, C.z, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+            const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
+#pragma unroll
+            for (int gq = 0; gq < GPC; ++gq)
+                s_anc[(warp * GPC + gq) * 33 + lane] = make_anchor(grp[(int64_t)cid * GPC + gq], sx, sy, sz, k);
         }
         __syncthreads();
-        if (MODE != 3) {
+        if (MODE != MODE_COUNT) {
             for (int t = threadIdx.x; t < 32 * La; t += blockDim.x) {
                 const int jj = t / La, m = t - jj * La;
                 const int lo = s_wlo[jj];
@@ -285,47 +287,43 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
         for (int jj = 0; jj < nj; ++jj) {
             const int lo = s_wlo[jj];
             if (lo < 0) continue;
-            const Anchor a = s_anc[warp * 32 + jj];
-            PairWin p = pair_setup(a, d4, 1.f, k);
-            if (p.amb) {
-                const int j = jb + jj;
-                int nlo, cnt;
-                exact_window(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sens[j], sens[k.Nd + j],
-                             sens[2 * k.Nd + j], p.g_first, p.g_last, k, nlo, cnt);
-                if (cnt > 0) p.e_lo = e_at(a, d4, nlo, k);
-                p.n_lo = nlo;
-                p.cnt = cnt;
-            }
+            const int j = jb + jj;
+            const Anchor a = my_anc[jj];
+            const PairWin p = pair_setup(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
             if (p.cnt <= 0) continue;
-            if (MODE == 3) {
-                npairs += (perm[gi] >= 0) ? (unsigned long long)p.cnt : 0ull;
+            if (MODE == MODE_COUNT) {
+                npairs += real ? (unsigned long long)p.cnt : 0ull;
                 continue;
             }
             const float* rp = s_res + jj * La + (p.n_lo - lo);
-            float P = exp2f(p.e_lo * p.e_lo * k.K1);
-            float q = exp2f(fmaf(p.e_lo, k.K2, k.K3));
             float part = 0.f;
+            if (p.cnt == WMAX) {
 #pragma unroll
-            for (int m = 0; m < WMAX; ++m) {
-                if (m < p.cnt) {
-                    const float dm = fmaf(-(float)m, k.h, p.e_lo);
-                    part = fmaf(dm * P, rp[m], part);
+                for (int m = 0; m < WMAX; ++m) {
+                    const float um = p.u_lo - (float)m;
+                    const float g = ex2((um * k.K1u) * um);
+                    part = fmaf(um * g, rp[m], part);
                 }
-                P *= q;
-                q *= k.cq;
-            }
-            for (int m = WMAX; m < p.cnt; ++m) {
-                const float dm = fmaf(-(float)m, k.h, p.e_lo);
-                part = fmaf(dm * P, rp[m], part);
-                P *= q;
-                q *= k.cq;
+            } else {
+#pragma unroll
+                for (int m = 0; m < WMAX; ++m) {
+                    if (m < p.cnt) {
+                        const float um = p.u_lo - (float)m;
+                        const float g = ex2((um * k.K1u) * um);
+                        part = fmaf(um * g, rp[m], part);
+                    }
+                }
+                for (int m = WMAX; m < p.cnt; ++m) {
+                    const float um = p.u_lo - (float)m;
+                    part = fmaf(um * ex2((um * k.K1u) * um), rp[m], part);
+                }
             }
             accb = fmaf(p.w, part, accb);
         }
         acc += accb;
     }
     if (!cok) return;
-    if (MODE == 3) {
+    if (MODE == MODE_COUNT) {
         for (int o = 16; o > 0; o >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, o);
         if (lane == 0) atomicAdd(count, npairs);
         return;
@@ -362,11 +360,11 @@ int pick_wmax(int w) {
 
 template <int W>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
-    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * 16 + (size_t)c->f_warps * c->Lf * 32 * 4;
+    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 + (size_t)c->f_warps * c->Lf * 32 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_forward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->f_sgroups);
-    k_forward<W><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_cell, c->d_orig, c->d_sens,
+    k_forward<W><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
                                                       c->Mpad, c->k);
     return cudaGetLastError();
@@ -374,11 +372,12 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
 
 template <int W, int MODE>
 cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
-    size_t smem = (size_t)c->a_cpr * 32 * sizeof(Anchor) + 32 * 4 + (MODE == 3 ? 0 : (size_t)32 * c->La * 4);
+    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 +
+                  (MODE == MODE_COUNT ? 0 : (size_t)32 * c->La * 4);
     cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int threads = 32 * std::max(c->a_cpr, 1);
-    k_adjoint<W, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_cell, c->d_orig, c->d_perm, c->d_sens,
+    k_adjoint<W, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                            c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
                                                            c->k, ep, c->d_count);
     return cudaGetLastError();
@@ -451,7 +450,7 @@ cudaError_t launch_count(gpair_ctx* c, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     EpiParams ep{};
-    return adj_dispatch<3>(c, nullptr, ep, st);
+    return adj_dispatch<MODE_COUNT>(c, nullptr, ep, st);
 }
 
 }  // namespace gpair

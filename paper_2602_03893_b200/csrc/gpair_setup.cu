@@ -68,9 +68,35 @@ __global__ void k_keys(const float* __restrict__ c, int64_t M, double mnx, doubl
     vals[i] = (int32_t)i;
 }
 
-// One warp per 32-kernel cell: anchor, radius, per-kernel offsets.
+// One warp per 32-kernel cell: fp32 anchors (bounding-box centres) and
+// conservative radii of the cell (windows) and of its four 8-kernel groups
+// (time-of-flight anchors), and per-kernel offsets from the group anchor.
+// Padding lanes (past M) sit on lane 0's kernel with zero amplitude.
+__device__ __forceinline__ void bbox_centre(float x, float y, float z, int width, float& Cx, float& Cy,
+                                            float& Cz) {
+    float mnx = x, mny = y, mnz = z, mxx = x, mxy = y, mxz = z;
+    for (int o = width / 2; o > 0; o >>= 1) {
+        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
+        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
+        mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
+    }
+    Cx = (float)(0.5 * ((double)mnx + (double)mxx));
+    Cy = (float)(0.5 * ((double)mny + (double)mxy));
+    Cz = (float)(0.5 * ((double)mnz + (double)mxz));
+}
+
+__device__ __forceinline__ double radius(float x, float y, float z, float Cx, float Cy, float Cz, int width) {
+    double dx = (double)x - Cx, dy = (double)y - Cy, dz = (double)z - Cz;
+    double rad = sqrt(dx * dx + dy * dy + dz * dz);
+    for (int o = width / 2; o > 0; o >>= 1) rad = fmax(rad, __shfl_xor_sync(0xffffffffu, rad, o));
+    return rad * (1.0 + 1e-6) + 1e-12;  // conservative margin
+}
+
 __global__ void k_cells(const float* __restrict__ c, int64_t M, const int32_t* __restrict__ sorted,
-                        int32_t ncells, float4* kd, float4* cell, float* orig, int32_t* perm) {
+                        int32_t ncells, float4* kd, float4* cell, float4* grp, float* orig, int32_t* perm) {
     int cid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     int lane = threadIdx.x & 31;
     if (cid >= ncells) return;
@@ -81,22 +107,12 @@ __global__ void k_cells(const float* __restrict__ c, int64_t M, const int32_t* _
     int32_t idx0 = __shfl_sync(0xffffffffu, idx, 0);
     int32_t src = real ? idx : idx0;
     float x = c[src], y = c[M + src], z = c[2 * M + src];
-    float mnx = x, mny = y, mnz = z, mxx = x, mxy = y, mxz = z;
-    for (int o = 16; o > 0; o >>= 1) {
-        mnx = fminf(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
-        mny = fminf(mny, __shfl_xor_sync(0xffffffffu, mny, o));
-        mnz = fminf(mnz, __shfl_xor_sync(0xffffffffu, mnz, o));
-        mxx = fmaxf(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
-        mxy = fmaxf(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
-        mxz = fmaxf(mxz, __shfl_xor_sync(0xffffffffu, mxz, o));
-    }
-    float Cx = (float)(0.5 * ((double)mnx + (double)mxx));
-    float Cy = (float)(0.5 * ((double)mny + (double)mxy));
-    float Cz = (float)(0.5 * ((double)mnz + (double)mxz));
-    if (!real) { x = Cx; y = Cy; z = Cz; }
-    double dx = (double)x - (double)Cx, dy = (double)y - (double)Cy, dz = (double)z - (double)Cz;
-    double rad = sqrt(dx * dx + dy * dy + dz * dz);
-    for (int o = 16; o > 0; o >>= 1) rad = fmax(rad, __shfl_xor_sync(0xffffffffu, rad, o));
+    float Cx, Cy, Cz, Gx, Gy, Gz;
+    bbox_centre(x, y, z, CELL, Cx, Cy, Cz);
+    bbox_centre(x, y, z, GROUP, Gx, Gy, Gz);
+    double crad = radius(x, y, z, Cx, Cy, Cz, CELL);
+    double grad = radius(x, y, z, Gx, Gy, Gz, GROUP);
+    double dx = (double)x - Gx, dy = (double)y - Gy, dz = (double)z - Gz;
     float fdx = (float)dx, fdy = (float)dy, fdz = (float)dz;
     double d2 = (double)fdx * fdx + (double)fdy * fdy + (double)fdz * fdz;
     kd[i] = make_float4(fdx, fdy, fdz, (float)d2);
@@ -104,11 +120,8 @@ __global__ void k_cells(const float* __restrict__ c, int64_t M, const int32_t* _
     orig[Mpad + i] = y;
     orig[2 * Mpad + i] = z;
     perm[i] = idx;
-    if (lane == 0) {
-        // conservative radius: round up and add a relative + absolute margin
-        float r32 = (float)(rad * (1.0 + 1e-6) + 1e-12);
-        cell[cid] = make_float4(Cx, Cy, Cz, r32);
-    }
+    if (lane == 0) cell[cid] = make_float4(Cx, Cy, Cz, (float)crad);
+    if ((lane & (GROUP - 1)) == 0) grp[i / GROUP] = make_float4(Gx, Gy, Gz, (float)grad);
 }
 
 // fp64 conservative sample window of all pairs of a cell with one sensor.
@@ -291,10 +304,11 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     c->Mpad = (int64_t)c->ncells * CELL;
     SETUP_CHECK(dmalloc(c, &c->d_kd, c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_cell, c->ncells));
+    SETUP_CHECK(dmalloc(c, &c->d_grp, (size_t)c->ncells * GPC));
     SETUP_CHECK(dmalloc(c, &c->d_orig, 3 * c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_perm, c->Mpad));
-    k_cells<<<(c->ncells + 7) / 8, 256, 0, st>>>(centers, M, vals, c->ncells, c->d_kd, c->d_cell, c->d_orig,
-                                                 c->d_perm);
+    k_cells<<<(c->ncells + 7) / 8, 256, 0, st>>>(centers, M, vals, c->ncells, c->d_kd, c->d_cell, c->d_grp,
+                                                 c->d_orig, c->d_perm);
     SETUP_CHECK(cudaGetLastError());
     cudaFree(keys);
     cudaFree(vals);
@@ -304,7 +318,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     c->f_warps = std::min(8, (Nd + 31) / 32);
     c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
-    int cpr = 128;
+    int cpr = 16;  // 512 kernels (8x8x8 on a grid): bounds fp32 accumulation chains
     while (cpr > 1 && (int64_t)((c->ncells + cpr - 1) / cpr) * c->f_sgroups < 4LL * dev_sms) cpr /= 2;
     const size_t smem_limit = 220 * 1024;
     for (;;) {
@@ -330,16 +344,9 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         unsigned bits = (unsigned)h_flags[4];
         memcpy(&me, &bits, 4);
         c->max_eps = me;
-        if (me > 0.08f) {
-            cudaFree(wlo);
-            why = "kernel cells too large relative to the sensor distance for the anchored time-of-flight "
-                  "expansion (max |q|/R^2 > 0.08)";
-            geom_err = GPAIR_ERR_GEOMETRY;
-            return cudaSuccess;
-        }
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 31) / 32 * 32;
-        size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * 16;
+        size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
         if (smem > smem_limit && cpr > 1) {
             cudaFree(wlo);
             cpr /= 2;
@@ -382,7 +389,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
         SETUP_CHECK(cudaStreamSynchronize(st));
         int La = (std::max(h_flags[6], 1) + 3) / 4 * 4;
-        size_t smem = (size_t)32 * La * 4 + (size_t)acpr * 32 * sizeof(Anchor) + 32 * 4;
+        size_t smem = (size_t)32 * La * 4 + (size_t)acpr * GPC * 33 * sizeof(Anchor) + 32 * 4;
         if (smem > 96 * 1024 && acpr > 1) {
             cudaFree(wlo);
             acpr /= 2;

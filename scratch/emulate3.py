@@ -1,0 +1,96 @@
+import sys, numpy as np
+sys.path.insert(0, '.')
+import oracle
+from paper_2602_03893_b200 import inputs
+f32 = np.float32
+name = sys.argv[1] if len(sys.argv) > 1 else 'cfg1'
+cfg = inputs.CONFIGS[name]
+c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
+if name != 'cfg1':
+    s = s[:, :8]
+x = inputs.dense_amplitudes(cfg.M)
+M, Nd, Nt = c.shape[1], s.shape[1], cfg.n_samples
+y_ref = oracle.forward(c, x, s, **op)
+v, fs, sig, k, t0 = cfg.v, cfg.fs, cfg.sig, cfg.k, cfg.t0
+ks = k*sig; h = v/fs
+log2e = 1.4426950408889634
+K1 = f32(-log2e/(2*sig*sig)); K2 = f32(log2e*h/(sig*sig)); K3 = f32(-log2e*h*h/(2*sig*sig)); cq = f32(np.exp(-h*h/(sig*sig)))
+hf = f32(h); inv_h = f32(1/h); ksf = f32(ks)
+# cells: 4x4x2 blocks of the grid (Morton cells)
+nx, ny, nz = cfg.grid
+ix, iy, iz = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing='ij')
+idx = (ix + nx*(iy + ny*iz)).ravel()
+cellid = ((ix//4) + (nx//4)*((iy//4) + (ny//4)*(iz//2))).ravel()
+cell_of = np.empty(M, int); cell_of[idx] = cellid
+ncell = cell_of.max()+1
+C = np.zeros((3, ncell), f32)
+for cc in range(ncell):
+    mem = c[:, cell_of == cc].astype(np.float64)
+    C[:, cc] = (0.5*(mem.min(1) + mem.max(1))).astype(f32)
+rng = np.random.default_rng(0)
+def ex2(a, approx=True):
+    r = np.exp2(a.astype(np.float64)).astype(f32)
+    if approx:
+        r = (r * (1 + 1.2e-7*rng.uniform(-1, 1, r.shape))).astype(f32)
+    return r
+def run(variant, acc_dtype=np.float64):
+    y = np.zeros((Nd, Nt), acc_dtype)
+    Cc = C[:, cell_of]  # 3 x M
+    dlt = (c.astype(np.float64) - Cc.astype(np.float64)).astype(f32)
+    d2 = (dlt.astype(np.float64)**2).sum(0).astype(f32)
+    for j in range(Nd):
+        sj = s[:, j].astype(np.float64)
+        D = Cc.astype(np.float64) - sj[:, None]
+        R2 = (D**2).sum(0); R = np.sqrt(R2)
+        na = np.floor((R/v - t0)*fs)
+        E = (R - v*(t0 + na/fs)).astype(f32)
+        U = (2*D).astype(f32)
+        invR2 = (1/R2).astype(f32); inv2R = (0.5/R).astype(f32); R2f = R2.astype(f32)
+        q = (U[0]*dlt[0]).astype(f32)
+        q = np.fma = None
+        # fma chain approximated with fp64 then round (fma = single rounding)
+        q = (U[2].astype(np.float64)*dlt[2] + d2).astype(f32)
+        q = (U[1].astype(np.float64)*dlt[1] + q).astype(f32)
+        q = (U[0].astype(np.float64)*dlt[0] + q).astype(f32)
+        eps = (q*invR2).astype(f32)
+        poly = np.ones(M, f32)
+        p = (eps.astype(np.float64)*(-21/512) + 7/128).astype(f32)
+        for co in [-5/64, 1/8, -0.25, 1.0]:
+            p = (eps.astype(np.float64)*p + co).astype(f32)
+        dr = ((q*inv2R).astype(f32)*p).astype(f32)
+        e = (E + dr).astype(f32)
+        w = (x.astype(f32)*f32(0.5)*(1/np.sqrt((R2f+q).astype(f32).astype(np.float64))).astype(f32)).astype(f32)
+        alpha = ((e - ksf)*inv_h).astype(f32); beta = ((e + ksf)*inv_h).astype(f32)
+        nlo = (na + np.floor(alpha) + 1).astype(int); nhi = (na + np.ceil(beta) - 1).astype(int)
+        nlo_c = np.maximum(nlo, 0); nhi_c = np.minimum(nhi, Nt-1)
+        e_lo = ((-(nlo_c - na)).astype(np.float64)*hf + e).astype(f32)
+        W = int(np.max(nhi_c - nlo_c + 1))
+        if variant == 'rec':
+            P = (w*ex2((e_lo*e_lo).astype(f32)*K1)).astype(f32)
+            qq = ex2((e_lo.astype(np.float64)*K2 + K3).astype(f32))
+        for m in range(W):
+            dm = ((-m)*np.float64(hf) + e_lo).astype(f32)
+            valid = m < (nhi_c - nlo_c + 1)
+            if variant == 'rec':
+                val = (dm*P).astype(f32)
+                P = (P*qq).astype(f32); qq = (qq*cq).astype(f32)
+            elif variant == 'mufu':
+                t = (dm*K1).astype(f32)
+                g = ex2((t*dm).astype(f32))
+                val = ((w*dm).astype(f32)*g).astype(f32)
+            elif variant == 'mufu_fma':   # arg = fma(dm*K1, dm, 0) same; try exact product
+                g = ex2((dm.astype(np.float64)**2*K1).astype(f32))
+                val = ((w*dm).astype(f32)*g).astype(f32)
+            n = nlo_c + m
+            sel = valid
+            np.add.at(y[j], n[sel], val[sel].astype(acc_dtype))
+    return y
+def metric(y):
+    big = np.abs(y_ref) >= 1e-3*np.abs(y_ref).max()
+    return np.linalg.norm(y-y_ref)/np.linalg.norm(y_ref), np.max(np.abs(y[big]-y_ref[big])/np.abs(y_ref[big]))
+APPROX=True
+print('mufu acc32', metric(run('mufu', np.float32)))
+_ex2 = ex2
+ex2 = lambda a, approx=True: _ex2(a, False)
+print('exact-exp acc64', metric(run('mufu')))
+print('exact-exp acc32', metric(run('mufu', np.float32)))
