@@ -235,6 +235,8 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     int wmax = (std::fabs(Lw - Lr) < 1e-6 * std::max(1.0, Lw)) ? (int)Lr : (int)std::ceil(Lw);
     k.wmax = std::max(wmax, 1);
     k.h = h;
+    k.inv_h = 1.0 / h;
+    k.t0fs = d->t0 * fs;
     k.ku = (float)(k.ks / h);
     k.K1u = (float)(-log2e * h * h / (2.0 * s * s));
 

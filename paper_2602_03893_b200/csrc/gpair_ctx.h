@@ -23,6 +23,7 @@ struct gpair_ctx_s {
     int32_t flags = 0;
     int grid_detected = 0;
     double max_eps = 0.0;
+    int series_small = 0;  // 1: every group's |eps| <= EPS_SMALL -> degree-2 series
 
     // geometry in the internal (spatially sorted) order
     float* d_sens = nullptr;   // [3][Nd]

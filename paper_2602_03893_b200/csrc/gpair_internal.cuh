@@ -33,11 +33,14 @@ constexpr int GPC = CELL / GROUP; // groups per cell
 constexpr float GAMMA = 4e-5f;    // ambiguity band of the fp32 window edges [samples]
 constexpr double EPS_FAST = 0.03; // max |eps| of the series path (else exact fp64 per pair)
 constexpr double MAX_DR_SAMPLES = 4.0; // max group radius [samples] of the series path
+constexpr double EPS_SMALL = 0.006;    // max |eps| for the degree-2 series (SER = 2)
 
 // Operator constants, computed once on the host in fp64 and passed by value.
 struct OpConst {
     double v, fs, t0, ks;  // ks = k * sigma (fp64, same bits as the oracle's k*sigma)
     double h;              // v / f_s [m]
+    double inv_h;          // f_s / v
+    double t0fs;           // t0 * f_s
     int32_t Nt, Nd;
     int32_t wmax;          // max in-window count of any pair
     float ku;              // k sigma / h  [samples]
@@ -58,24 +61,25 @@ struct __align__(16) Anchor {
 constexpr int32_t NA_EXACT = -2147483647 - 1;
 
 __device__ __forceinline__ Anchor make_anchor(float4 C, float sx, float sy, float sz, const OpConst& k) {
-    double dx = (double)C.x - (double)sx;
-    double dy = (double)C.y - (double)sy;
-    double dz = (double)C.z - (double)sz;
-    double R2 = dx * dx + dy * dy + dz * dz;
-    double R = sqrt(R2);
-    double na = floor((R / k.v - k.t0) * k.fs);
-    double Eu = (R - k.v * (k.t0 + na / k.fs)) / k.h;
+    const double dx = (double)C.x - (double)sx;
+    const double dy = (double)C.y - (double)sy;
+    const double dz = (double)C.z - (double)sz;
+    const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
+    const double invR = rsqrt(R2);
+    const double R = R2 * invR;
+    const double tf = fma(R, k.inv_h, -k.t0fs);  // (R/v - t0) f_s in samples
+    const double na = floor(tf);
     Anchor a;
     a.Ux = (float)(2.0 * dx);
     a.Uy = (float)(2.0 * dy);
     a.Uz = (float)(2.0 * dz);
-    a.Eu = (float)Eu;
-    a.invR2 = (float)(1.0 / R2);
-    a.inv2Rh = (float)(0.5 / (R * k.h));
-    a.h2R = (float)(0.5 * k.h / R);
+    a.Eu = (float)(tf - na);  // exact fp64 subtraction
+    a.invR2 = (float)(invR * invR);
+    a.inv2Rh = (float)(0.5 * invR * k.inv_h);
+    a.h2R = (float)(0.5 * k.h * invR);
     // series accuracy: |eps| <= (2 R rad + rad^2) / R^2 (C.w = group radius)
-    double rad = C.w;
-    const bool series_ok = (2.0 * R * rad + rad * rad) <= EPS_FAST * R2 && rad <= MAX_DR_SAMPLES * k.h;
+    const double rad = C.w;
+    const bool series_ok = fma(2.0 * R, rad, rad * rad) <= EPS_FAST * R2 && rad <= MAX_DR_SAMPLES * k.h;
     a.na = series_ok ? (int32_t)na : NA_EXACT;
     return a;
 }
@@ -133,7 +137,10 @@ struct PairWin {
 };
 
 // Per-pair window and weight.  kd = (dx, dy, dz, |d|^2) relative to the group
-// anchor; (cx, cy, cz) = original centre, read only on the rare exact paths.
+// anchor; orig = original centres, read only on the rare exact paths.
+// SER = 5: series to eps^5 / eps^4 (|eps| <= EPS_FAST); SER = 2: to eps^2
+// (|eps| <= EPS_SMALL, truncation <= 7e-8 relative; chosen at create).
+template <int SER>
 __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float A, const float* __restrict__ orig,
                                               int64_t gi, int64_t Mpad, float sx, float sy, float sz,
                                               const OpConst& k) {
@@ -141,17 +148,23 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
     float eu;
     int na;
     if (a.na != NA_EXACT) {
-        float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
-        float eps = q * a.invR2;
-        float S = fmaf(eps, -21.f / 512.f, 7.f / 128.f);
-        S = fmaf(eps, S, -5.f / 64.f);
-        S = fmaf(eps, S, 1.f / 8.f);
-        S = fmaf(eps, S, -0.25f);
-        S = fmaf(eps, S, 1.f);
-        float Tw = fmaf(eps, 35.f / 128.f, -5.f / 16.f);
-        Tw = fmaf(eps, Tw, 3.f / 8.f);
-        Tw = fmaf(eps, Tw, -0.5f);
-        Tw = fmaf(eps, Tw, 1.f);
+        const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+        const float eps = q * a.invR2;
+        float S, Tw;
+        if (SER == 2) {
+            S = fmaf(eps, fmaf(eps, 1.f / 8.f, -0.25f), 1.f);
+            Tw = fmaf(eps, fmaf(eps, 3.f / 8.f, -0.5f), 1.f);
+        } else {
+            S = fmaf(eps, -21.f / 512.f, 7.f / 128.f);
+            S = fmaf(eps, S, -5.f / 64.f);
+            S = fmaf(eps, S, 1.f / 8.f);
+            S = fmaf(eps, S, -0.25f);
+            S = fmaf(eps, S, 1.f);
+            Tw = fmaf(eps, 35.f / 128.f, -5.f / 16.f);
+            Tw = fmaf(eps, Tw, 3.f / 8.f);
+            Tw = fmaf(eps, Tw, -0.5f);
+            Tw = fmaf(eps, Tw, 1.f);
+        }
         eu = fmaf(q * a.inv2Rh, S, a.Eu);  // u at sample n_a
         p.w = A * (a.h2R * Tw);
         na = a.na;
@@ -160,22 +173,61 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
     }
     const float alpha = eu - k.ku;  // in-window m satisfy alpha < m < beta
     const float beta = eu + k.ku;
-    const bool amb = (fabsf(alpha - rintf(alpha)) < GAMMA) || (fabsf(beta - rintf(beta)) < GAMMA);
     int n_lo = na + (int)floorf(alpha) + 1;
     int n_hi = na + (int)ceilf(beta) - 1;
-    if (amb) {
-        const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
-        int cnt;
-        exact_window(r, n_lo, n_hi, k, n_lo, cnt);
-        n_hi = n_lo + cnt - 1;
-    } else {
-        if (n_lo < 0) n_lo = 0;
-        if (n_hi > k.Nt - 1) n_hi = k.Nt - 1;
+    const bool amb = (fabsf(alpha - rintf(alpha)) < GAMMA) || (fabsf(beta - rintf(beta)) < GAMMA);
+    if (amb || n_lo < 0 || n_hi > k.Nt - 1) {  // rare: exact edges and/or record clipping
+        if (amb) {
+            const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
+            int cnt;
+            exact_window(r, n_lo, n_hi, k, n_lo, cnt);
+            n_hi = n_lo + cnt - 1;
+        } else {
+            n_lo = max(n_lo, 0);
+            n_hi = min(n_hi, k.Nt - 1);
+        }
     }
     p.n_lo = n_lo;
     p.cnt = max(n_hi - n_lo + 1, 0);
     p.u_lo = eu - (float)(n_lo - na);  // exact: integer shift of a small float
     return p;
+}
+
+// ---- packed fp32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2)
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t pk2(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk2(f2_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+    f2_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
+    f2_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+    f2_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ float ex2f(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// g = exp2(K1u u^2) for both halves (two MUFU.EX2)
+__device__ __forceinline__ f2_t gauss2(f2_t u2, f2_t K2) {
+    float a0, a1;
+    upk2(mul2(mul2(u2, K2), u2), a0, a1);
+    return pk2(ex2f(a0), ex2f(a1));
 }
 
 }  // namespace gpair

@@ -27,12 +27,6 @@ namespace {
 
 constexpr int STAGE_CELLS = 8;  // cells staged per forward pipeline step
 
-__device__ __forceinline__ float ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
 __global__ void k_gather(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t Mpad,
                          int npc, float eps, float* __restrict__ amp) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -47,7 +41,7 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 }
 
 // ------------------------------------------------------------------ forward
-template <int WMAX>
+template <int WMAX, int SER>
 __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
@@ -86,29 +80,34 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             for (int t = 0; t < GROUP; ++t) {
                 const int li = gq * GROUP + t;
-                const PairWin p = pair_setup(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy,
+                const PairWin p = pair_setup<SER>(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy,
                                              sz, k);
                 if (p.cnt <= 0) continue;
                 float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
-                if (p.cnt == WMAX) {  // common case: no per-sample predicates
+                if (p.cnt == WMAX && (WMAX & 1) == 0) {  // common case: packed pairs, no predicates
+                    const f2_t K2 = pk2(k.K1u, k.K1u), W2 = pk2(p.w, p.w), step = pk2(-2.f, -2.f);
+                    f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
 #pragma unroll
-                    for (int m = 0; m < WMAX; ++m) {
-                        const float um = p.u_lo - (float)m;
-                        const float g = ex2((um * k.K1u) * um);
-                        ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
+                    for (int m = 0; m < WMAX; m += 2) {
+                        const f2_t val = mul2(mul2(W2, u2), gauss2(u2, K2));
+                        float v0, v1;
+                        upk2(val, v0, v1);
+                        ap[m * 32] += v0;
+                        ap[(m + 1) * 32] += v1;
+                        u2 = add2(u2, step);
                     }
                 } else {
 #pragma unroll
                     for (int m = 0; m < WMAX; ++m) {
                         if (m < p.cnt) {
                             const float um = p.u_lo - (float)m;
-                            const float g = ex2((um * k.K1u) * um);
+                            const float g = ex2f((um * k.K1u) * um);
                             ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
                         }
                     }
                     for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
                         const float um = p.u_lo - (float)m;
-                        ap[m * 32] = fmaf(p.w * um, ex2((um * k.K1u) * um), ap[m * 32]);
+                        ap[m * 32] = fmaf(p.w * um, ex2f((um * k.K1u) * um), ap[m * 32]);
                     }
                 }
             }
@@ -142,12 +141,12 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
                                                 int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
                                                 const float* __restrict__ b, float* __restrict__ delta,
                                                 double* __restrict__ loss_part) {
-    extern __shared__ float s_copy[];
+    extern __shared__ double s_copy[];
     const int j = blockIdx.x;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int jlo = jlo_a[j], jlen = jlen_a[j];
-    float* mine = s_copy + (size_t)warp * jlen;
-    for (int t = lane; t < jlen; t += 32) mine[t] = 0.f;
+    double* mine = s_copy + (size_t)warp * jlen;
+    for (int t = lane; t < jlen; t += 32) mine[t] = 0.0;
     __syncwarp();
     const int32_t* wl = wloT + (int64_t)j * nregions;
     for (int r0 = warp; r0 < nregions; r0 += nw * RED_BATCH) {
@@ -175,11 +174,12 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
     double lsum = 0.0;
     const int64_t row = (int64_t)j * k.Nt;
     for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
-        float yv = 0.f;
+        double ys = 0.0;
         int t = n - jlo;
         if (t >= 0 && t < jlen) {
-            for (int w = 0; w < nw; ++w) yv += s_copy[(size_t)w * jlen + t];
+            for (int w = 0; w < nw; ++w) ys += s_copy[(size_t)w * jlen + t];
         }
+        const float yv = (float)ys;
         if (y) y[row + n] = yv;
         if (b) {
             float dv = yv - b[row + n];
@@ -239,7 +239,7 @@ __global__ void k_loss(const double* __restrict__ part, int32_t n, double inv_N,
 // ------------------------------------------------------------------ adjoint
 constexpr int MODE_COUNT = 3;
 
-template <int WMAX, int MODE>
+template <int WMAX, int SER, int MODE>
 __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                  const float* __restrict__ orig, const int32_t* __restrict__ perm,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             if (lo < 0) continue;
             const int j = jb + jj;
             const Anchor a = my_anc[jj];
-            const PairWin p = pair_setup(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+            const PairWin p = pair_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
             if (p.cnt <= 0) continue;
             if (MODE == MODE_COUNT) {
                 npairs += real ? (unsigned long long)p.cnt : 0ull;
@@ -297,25 +297,30 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             }
             const float* rp = s_res + jj * La + (p.n_lo - lo);
             float part = 0.f;
-            if (p.cnt == WMAX) {
+            if (p.cnt == WMAX && (WMAX & 1) == 0) {  // packed pairs, no predicates
+                const f2_t K2 = pk2(k.K1u, k.K1u), step = pk2(-2.f, -2.f);
+                f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
+                f2_t part2 = 0ull;
 #pragma unroll
-                for (int m = 0; m < WMAX; ++m) {
-                    const float um = p.u_lo - (float)m;
-                    const float g = ex2((um * k.K1u) * um);
-                    part = fmaf(um * g, rp[m], part);
+                for (int m = 0; m < WMAX; m += 2) {
+                    part2 = fma2(mul2(u2, gauss2(u2, K2)), pk2(rp[m], rp[m + 1]), part2);
+                    u2 = add2(u2, step);
                 }
+                float p0, p1;
+                upk2(part2, p0, p1);
+                part = p0 + p1;
             } else {
 #pragma unroll
                 for (int m = 0; m < WMAX; ++m) {
                     if (m < p.cnt) {
                         const float um = p.u_lo - (float)m;
-                        const float g = ex2((um * k.K1u) * um);
+                        const float g = ex2f((um * k.K1u) * um);
                         part = fmaf(um * g, rp[m], part);
                     }
                 }
                 for (int m = WMAX; m < p.cnt; ++m) {
                     const float um = p.u_lo - (float)m;
-                    part = fmaf(um * ex2((um * k.K1u) * um), rp[m], part);
+                    part = fmaf(um * ex2f((um * k.K1u) * um), rp[m], part);
                 }
             }
             accb = fmaf(p.w, part, accb);
@@ -358,43 +363,63 @@ int pick_wmax(int w) {
     return 64;
 }
 
-template <int W>
+template <int W, int SER>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
     size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 + (size_t)c->f_warps * c->Lf * 32 * 4;
-    cudaError_t e = cudaFuncSetAttribute(k_forward<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->f_sgroups);
-    k_forward<W><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
+    k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
                                                       c->Mpad, c->k);
     return cudaGetLastError();
 }
 
-template <int W, int MODE>
+template <int W, int SER, int MODE>
 cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 +
                   (MODE == MODE_COUNT ? 0 : (size_t)32 * c->La * 4);
-    cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int threads = 32 * std::max(c->a_cpr, 1);
-    k_adjoint<W, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
+    k_adjoint<W, SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                            c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
                                                            c->k, ep, c->d_count);
     return cudaGetLastError();
 }
 
+template <int SER, int MODE>
+cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    switch (pick_wmax(c->k.wmax)) {
+        case 5: return adj_launch<5, SER, MODE>(c, resid, ep, st);
+        case 8: return adj_launch<8, SER, MODE>(c, resid, ep, st);
+        case 12: return adj_launch<12, SER, MODE>(c, resid, ep, st);
+        case 16: return adj_launch<16, SER, MODE>(c, resid, ep, st);
+        case 20: return adj_launch<20, SER, MODE>(c, resid, ep, st);
+        case 24: return adj_launch<24, SER, MODE>(c, resid, ep, st);
+        case 32: return adj_launch<32, SER, MODE>(c, resid, ep, st);
+        case 48: return adj_launch<48, SER, MODE>(c, resid, ep, st);
+        default: return adj_launch<64, SER, MODE>(c, resid, ep, st);
+    }
+}
+
 template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    return c->series_small ? adj_dispatch2<2, MODE>(c, resid, ep, st) : adj_dispatch2<5, MODE>(c, resid, ep, st);
+}
+
+template <int SER>
+cudaError_t fwd_dispatch(gpair_ctx* c, cudaStream_t st) {
     switch (pick_wmax(c->k.wmax)) {
-        case 5: return adj_launch<5, MODE>(c, resid, ep, st);
-        case 8: return adj_launch<8, MODE>(c, resid, ep, st);
-        case 12: return adj_launch<12, MODE>(c, resid, ep, st);
-        case 16: return adj_launch<16, MODE>(c, resid, ep, st);
-        case 20: return adj_launch<20, MODE>(c, resid, ep, st);
-        case 24: return adj_launch<24, MODE>(c, resid, ep, st);
-        case 32: return adj_launch<32, MODE>(c, resid, ep, st);
-        case 48: return adj_launch<48, MODE>(c, resid, ep, st);
-        default: return adj_launch<64, MODE>(c, resid, ep, st);
+        case 5: return fwd_launch<5, SER>(c, st);
+        case 8: return fwd_launch<8, SER>(c, st);
+        case 12: return fwd_launch<12, SER>(c, st);
+        case 16: return fwd_launch<16, SER>(c, st);
+        case 20: return fwd_launch<20, SER>(c, st);
+        case 24: return fwd_launch<24, SER>(c, st);
+        case 32: return fwd_launch<32, SER>(c, st);
+        case 48: return fwd_launch<48, SER>(c, st);
+        default: return fwd_launch<64, SER>(c, st);
     }
 }
 
@@ -406,23 +431,13 @@ cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cu
 }
 
 cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
-    switch (pick_wmax(c->k.wmax)) {
-        case 5: return fwd_launch<5>(c, st);
-        case 8: return fwd_launch<8>(c, st);
-        case 12: return fwd_launch<12>(c, st);
-        case 16: return fwd_launch<16>(c, st);
-        case 20: return fwd_launch<20>(c, st);
-        case 24: return fwd_launch<24>(c, st);
-        case 32: return fwd_launch<32>(c, st);
-        case 48: return fwd_launch<48>(c, st);
-        default: return fwd_launch<64>(c, st);
-    }
+    return c->series_small ? fwd_dispatch<2>(c, st) : fwd_dispatch<5>(c, st);
 }
 
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {
     int nw = 8;
-    while (nw > 1 && (size_t)nw * c->jlen_max * 4 > 200 * 1024) nw /= 2;
-    size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 4;
+    while (nw > 1 && (size_t)nw * c->jlen_max * 8 > 200 * 1024) nw /= 2;
+    size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 8;
     cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_wlo_fT, c->d_jlo, c->d_jlen, c->f_regions, c->Lf,

@@ -142,7 +142,7 @@ __device__ __forceinline__ bool cell_window(float4 C, float sx, float sy, float 
 
 // Thread per (region, sensor): union window over the region's cells.
 // check != 0 also performs the geometry check and the anchor-expansion bound.
-__global__ void k_region_windows(const float4* __restrict__ cell, int32_t ncells,
+__global__ void k_region_windows(const float4* __restrict__ cell, const float4* __restrict__ grp, int32_t ncells,
                                  const float* __restrict__ sens, int32_t cpr, int32_t nregions,
                                  OpConst k, int32_t* wlo, int* maxlen, int check, int* geom_bad,
                                  unsigned int* max_eps_bits) {
@@ -165,8 +165,13 @@ __global__ void k_region_windows(const float4* __restrict__ cell, int32_t ncells
         }
         if (check) {
             if (!(R - (double)C.w > k.ks)) bad = 1;
-            double e = (2.0 * R * C.w + (double)C.w * C.w) / (R * R);
-            eps_max = fmaxf(eps_max, (float)e);
+            for (int gq = 0; gq < GPC; ++gq) {  // anchor-expansion bound per 8-kernel group
+                const float4 G = grp[(int64_t)cc * GPC + gq];
+                double gx = (double)G.x - sx, gy = (double)G.y - sy, gz = (double)G.z - sz;
+                double Rg2 = gx * gx + gy * gy + gz * gz;
+                double e = (2.0 * sqrt(Rg2) * G.w + (double)G.w * G.w) / Rg2;
+                eps_max = fmaxf(eps_max, (float)e);
+            }
         }
     }
     int len = 0;
@@ -328,7 +333,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         SETUP_CHECK(cudaMemsetAsync(c->d_flags + 2, 0, 6 * sizeof(int32_t), st));
         int64_t nt = (int64_t)nreg * Nd;
         k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
-            c->d_cell, c->ncells, c->d_sens, cpr, nreg, c->k, wlo, c->d_flags + 2, 1, c->d_flags + 3,
+            c->d_cell, c->d_grp, c->ncells, c->d_sens, cpr, nreg, c->k, wlo, c->d_flags + 2, 1, c->d_flags + 3,
             (unsigned int*)(c->d_flags + 4));
         SETUP_CHECK(cudaGetLastError());
         SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
@@ -344,6 +349,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         unsigned bits = (unsigned)h_flags[4];
         memcpy(&me, &bits, 4);
         c->max_eps = me;
+        c->series_small = me <= EPS_SMALL ? 1 : 0;
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 31) / 32 * 32;
         size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
@@ -384,7 +390,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         SETUP_CHECK(cudaMemsetAsync(c->d_flags + 6, 0, sizeof(int32_t), st));
         int64_t nt = (int64_t)nreg * Nd;
         k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
-            c->d_cell, c->ncells, c->d_sens, acpr, nreg, c->k, wlo, c->d_flags + 6, 0, nullptr, nullptr);
+            c->d_cell, c->d_grp, c->ncells, c->d_sens, acpr, nreg, c->k, wlo, c->d_flags + 6, 0, nullptr, nullptr);
         SETUP_CHECK(cudaGetLastError());
         SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
         SETUP_CHECK(cudaStreamSynchronize(st));
