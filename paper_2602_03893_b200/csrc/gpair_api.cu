@@ -238,6 +238,17 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     k.inv_h = 1.0 / h;
     k.t0fs = d->t0 * fs;
     k.ku = (float)(k.ks / h);
+    {
+        // window length 2 k sigma / h an exact integer (the fp32 ku doubled is
+        // that integer): the fp32 fast path derives the upper edge from the
+        // lower one (gpair_internal.cuh pair_setup)
+        const double two = 2.0 * (double)k.ku;
+        k.cnt_int = (two == std::nearbyint(two) && std::fabs(Lw - two) < 1e-9 * std::max(1.0, Lw) && two >= 1.0)
+                        ? (int)two
+                        : 0;
+        k.c_lo = -k.ku - 0.5f;
+        k.c_u = k.ku - 0.5f;
+    }
     k.K1u = (float)(-log2e * h * h / (2.0 * s * s));
 
     gpair_ctx* c = new (std::nothrow) gpair_ctx();

@@ -24,6 +24,7 @@ struct gpair_ctx_s {
     int grid_detected = 0;
     double max_eps = 0.0;
     int series_small = 0;  // 1: every group's |eps| <= EPS_SMALL -> degree-2 series
+    int ser = 5;           // kernel path: 0 = pair_fast, 2 / 5 = pair_setup<SER> (gpair_kernels.cu)
 
     // geometry in the internal (spatially sorted) order
     float* d_sens = nullptr;   // [3][Nd]
@@ -89,5 +90,6 @@ struct EpiParams {
 enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
+int pick_wmax(int w);
 
 }  // namespace gpair

@@ -34,6 +34,8 @@ constexpr float GAMMA = 4e-5f;    // ambiguity band of the fp32 window edges [sa
 constexpr double EPS_FAST = 0.03; // max |eps| of the series path (else exact fp64 per pair)
 constexpr double MAX_DR_SAMPLES = 4.0; // max group radius [samples] of the series path
 constexpr double EPS_SMALL = 0.006;    // max |eps| for the degree-2 series (SER = 2)
+constexpr float RND_MAGIC = 12582912.f;      // 1.5 * 2^23
+constexpr int RND_MAGIC_BITS = 0x4B400000;   // __float_as_int(RND_MAGIC)
 
 // Operator constants, computed once on the host in fp64 and passed by value.
 struct OpConst {
@@ -43,6 +45,9 @@ struct OpConst {
     double t0fs;           // t0 * f_s
     int32_t Nt, Nd;
     int32_t wmax;          // max in-window count of any pair
+    int32_t cnt_int;       // 2 k sigma / h if it is an integer (fp32 ku exact), else 0
+    float c_lo;            // -ku - 1/2   (pair_fast)
+    float c_u;             // ku - 1/2    (pair_fast)
     float ku;              // k sigma / h  [samples]
     float K1u;             // -log2(e) h^2 / (2 sigma^2)
 };
@@ -171,11 +176,28 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
     } else {
         exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, p.w, na);
     }
-    const float alpha = eu - k.ku;  // in-window m satisfy alpha < m < beta
-    const float beta = eu + k.ku;
-    int n_lo = na + (int)floorf(alpha) + 1;
-    int n_hi = na + (int)ceilf(beta) - 1;
-    const bool amb = (fabsf(alpha - rintf(alpha)) < GAMMA) || (fabsf(beta - rintf(beta)) < GAMMA);
+    // In-window m satisfy alpha < m < beta (alpha = eu - ku, beta = eu + ku).
+    // floor() without the XU pipe: for |x| < 2^22, (x + 1.5*2^23) rounds x to
+    // the nearest integer, held in the low mantissa bits.  floor(alpha) =
+    // rint(alpha - 1/2) whenever alpha is not within GAMMA of an integer; the
+    // ambiguous case goes to the exact path anyway.
+    const float alpha = eu - k.ku;
+    const float ta = (alpha - 0.5f) + RND_MAGIC;
+    const float fla = ta - RND_MAGIC;
+    bool amb = fabsf((alpha - fla) - 0.5f) > 0.5f - GAMMA;
+    int n_lo = na + (__float_as_int(ta) - RND_MAGIC_BITS) + 1;
+    int n_hi;
+    float u_lo = eu - (fla + 1.f);  // exact: integer shift of a small float
+    if (k.cnt_int > 0) {
+        // 2 ku is an exact integer: frac(beta) = frac(alpha), so the window
+        // holds exactly cnt_int samples unless alpha is ambiguous
+        n_hi = n_lo + k.cnt_int - 1;
+    } else {
+        const float beta = eu + k.ku;
+        const float tb = (beta - 0.5f) + RND_MAGIC;
+        amb = amb || fabsf((beta - (tb - RND_MAGIC)) - 0.5f) > 0.5f - GAMMA;
+        n_hi = na + (__float_as_int(tb) - RND_MAGIC_BITS);  // ceil(beta) - 1 = floor(beta)
+    }
     if (amb || n_lo < 0 || n_hi > k.Nt - 1) {  // rare: exact edges and/or record clipping
         if (amb) {
             const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
@@ -186,10 +208,59 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
             n_lo = max(n_lo, 0);
             n_hi = min(n_hi, k.Nt - 1);
         }
+        u_lo = eu - (float)(n_lo - na);
     }
     p.n_lo = n_lo;
     p.cnt = max(n_hi - n_lo + 1, 0);
-    p.u_lo = eu - (float)(n_lo - na);  // exact: integer shift of a small float
+    p.u_lo = u_lo;
+    return p;
+}
+
+// Rare path of pair_fast(): exact window edges and/or record clipping.
+static __device__ __noinline__ PairWin pair_fix(PairWin p, float eu, int na, bool amb, const float* __restrict__ orig,
+                                                int64_t gi, int64_t Mpad, float sx, float sy, float sz, int cnt_guess,
+                                                const OpConst k) {
+    int n_lo = p.n_lo, n_hi = p.n_lo + cnt_guess - 1;
+    if (amb) {
+        const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
+        int cnt;
+        exact_window(r, n_lo, n_hi, k, n_lo, cnt);
+        n_hi = n_lo + cnt - 1;
+    } else {
+        n_lo = max(n_lo, 0);
+        n_hi = min(n_hi, k.Nt - 1);
+    }
+    p.n_lo = n_lo;
+    p.cnt = max(n_hi - n_lo + 1, 0);
+    p.u_lo = eu - (float)(n_lo - na);
+    return p;
+}
+
+// Fast per-pair setup for the common configuration (FAST): degree-2 series
+// (every |eps| <= EPS_SMALL), window length 2 k sigma / h an exact integer
+// (k.cnt_int), anchor not exact.  Same arithmetic as pair_setup<2> with the
+// constants folded: x = eu - ku - 1/2, fl = rint(x) = floor(alpha),
+// u_lo = eu - (fl + 1).
+__device__ __forceinline__ PairWin pair_fast(const Anchor& a, float4 kd, float A, const float* __restrict__ orig,
+                                             int64_t gi, int64_t Mpad, float sx, float sy, float sz,
+                                             const OpConst& k) {
+    PairWin p;
+    const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+    const float eps = q * a.invR2;
+    const float S = fmaf(eps, fmaf(eps, 1.f / 8.f, -0.25f), 1.f);
+    const float Tw = fmaf(eps, fmaf(eps, 3.f / 8.f, -0.5f), 1.f);
+    const float eu = fmaf(q * a.inv2Rh, S, a.Eu);
+    p.w = A * (a.h2R * Tw);
+    const float x = eu + k.c_lo;              // alpha - 1/2
+    const float t = x + RND_MAGIC;
+    const float fl = t - RND_MAGIC;           // floor(alpha) unless ambiguous
+    const float d = x - fl;                   // frac(alpha) - 1/2
+    p.n_lo = a.na + __float_as_int(t) - (RND_MAGIC_BITS - 1);
+    p.u_lo = eu - (fl + 1.f);                 // u at n_lo (exact: no rounding of x leaks in)
+    p.cnt = k.cnt_int;
+    const bool amb = fabsf(d) > 0.5f - GAMMA;
+    if (amb || (unsigned)p.n_lo > (unsigned)(k.Nt - k.cnt_int))
+        p = pair_fix(p, eu, a.na, amb, orig, gi, Mpad, sx, sy, sz, k.cnt_int, k);
     return p;
 }
 

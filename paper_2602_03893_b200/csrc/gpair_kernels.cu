@@ -78,10 +78,15 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
         __syncthreads();
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            const bool gexact = SER == 0 && __any_sync(__activemask(), a.na == NA_EXACT);
             for (int t = 0; t < GROUP; ++t) {
                 const int li = gq * GROUP + t;
-                const PairWin p = pair_setup<SER>(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy,
-                                             sz, k);
+                const int64_t gi = (int64_t)cb * CELL + li;
+                PairWin p;
+                if (SER == 0 && !gexact)
+                    p = pair_fast(a, s_kd[li], s_amp[li], orig, gi, Mpad, sx, sy, sz, k);
+                else
+                    p = pair_setup<SER == 0 ? 2 : SER>(a, s_kd[li], s_amp[li], orig, gi, Mpad, sx, sy, sz, k);
                 if (p.cnt <= 0) continue;
                 float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
                 if (p.cnt == WMAX && (WMAX & 1) == 0) {  // common case: packed pairs, no predicates
@@ -89,11 +94,12 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
                     f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
 #pragma unroll
                     for (int m = 0; m < WMAX; m += 2) {
-                        const f2_t val = mul2(mul2(W2, u2), gauss2(u2, K2));
+                        f2_t acc2 = pk2(ap[m * 32], ap[(m + 1) * 32]);
+                        acc2 = fma2(mul2(W2, u2), gauss2(u2, K2), acc2);
                         float v0, v1;
-                        upk2(val, v0, v1);
-                        ap[m * 32] += v0;
-                        ap[(m + 1) * 32] += v1;
+                        upk2(acc2, v0, v1);
+                        ap[m * 32] = v0;
+                        ap[(m + 1) * 32] = v1;
                         u2 = add2(u2, step);
                     }
                 } else {
@@ -289,7 +295,12 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             if (lo < 0) continue;
             const int j = jb + jj;
             const Anchor a = my_anc[jj];
-            const PairWin p = pair_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+            PairWin p;
+            if (SER == 0 && a.na != NA_EXACT)
+                p = pair_fast(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+            else
+                p = pair_setup<SER == 0 ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j],
+                                                   sens[2 * k.Nd + j], k);
             if (p.cnt <= 0) continue;
             if (MODE == MODE_COUNT) {
                 npairs += real ? (unsigned long long)p.cnt : 0ull;
@@ -356,12 +367,14 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     }
 }
 
+}  // namespace
 int pick_wmax(int w) {
     static const int opts[] = {5, 8, 12, 16, 20, 24, 32, 48, 64};
     for (int o : opts)
         if (w <= o) return o;
     return 64;
 }
+namespace {
 
 template <int W, int SER>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
@@ -405,7 +418,8 @@ cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep,
 
 template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
-    return c->series_small ? adj_dispatch2<2, MODE>(c, resid, ep, st) : adj_dispatch2<5, MODE>(c, resid, ep, st);
+    return c->ser == 0 ? adj_dispatch2<0, MODE>(c, resid, ep, st)
+                       : (c->ser == 2 ? adj_dispatch2<2, MODE>(c, resid, ep, st) : adj_dispatch2<5, MODE>(c, resid, ep, st));
 }
 
 template <int SER>
@@ -431,7 +445,7 @@ cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cu
 }
 
 cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
-    return c->series_small ? fwd_dispatch<2>(c, st) : fwd_dispatch<5>(c, st);
+    return c->ser == 0 ? fwd_dispatch<0>(c, st) : (c->ser == 2 ? fwd_dispatch<2>(c, st) : fwd_dispatch<5>(c, st));
 }
 
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {

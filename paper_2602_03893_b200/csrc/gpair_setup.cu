@@ -350,6 +350,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         memcpy(&me, &bits, 4);
         c->max_eps = me;
         c->series_small = me <= EPS_SMALL ? 1 : 0;
+        c->ser = c->series_small ? ((c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int) ? 0 : 2) : 5;
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 31) / 32 * 32;
         size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
