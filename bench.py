@@ -102,11 +102,11 @@ def cpu_oracle_sample(cfg, c, s, x, d, seconds):
     adj = {k: v for k, v in op.items() if k != "n_samples"}
     M, Nd = c.shape[1], s.shape[1]
     cores = oracle.threads()
-    # calibrate on one sensor row (M pairs)
+    # calibrate on one row per core (the oracle parallelises over sensor rows)
     t = time.perf_counter()
-    oracle.forward(c, x, s, rows=np.array([0], np.int32), **op)
-    t1 = max(time.perf_counter() - t, 1e-3)
-    n_rows = int(max(1, min(Nd, round(0.5 * seconds / t1))))
+    oracle.forward(c, x, s, rows=np.arange(min(cores, Nd), dtype=np.int32), **op)
+    t1 = max(time.perf_counter() - t, 1e-3)  # time for `cores` rows in parallel
+    n_rows = int(max(1, min(Nd, cores * round(0.5 * seconds / t1))))
     rows = np.linspace(0, Nd - 1, n_rows).astype(np.int32)
     t = time.perf_counter()
     oracle.forward(c, x, s, rows=rows, **op)
