@@ -177,6 +177,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2602_03893_b200 import build, gpair, inputs
+    from paper_2602_03893_b200.shard import kernel_shard, max_over_ranks, nccl_bootstrap
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -191,15 +192,13 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         dist.barrier()
-        obj = [gpair.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        comm = gpair.nccl_comm_init(world, obj[0], rank)
+        comm = nccl_bootstrap(dist, rank, world, gpair.nccl_unique_id, gpair.nccl_comm_init)
 
     cfg = inputs.CONFIGS[args.config]
     c_all = cfg.centers()
     s = cfg.sensors()
     M = cfg.M
-    lo, hi = rank * M // world, (rank + 1) * M // world  # contiguous z-slab shard
+    lo, hi = kernel_shard(M, world, rank)  # contiguous z-slab shard
     c = np.ascontiguousarray(c_all[:, lo:hi])
     Ml = hi - lo
     ctx = gpair.Context(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), sigma=cfg.sig, v=cfg.v,
@@ -244,9 +243,7 @@ def main():
     ctx.profile_enable(False)
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        tt = torch.tensor([ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks(dist, ms, dev)
     pairs_iter = 2.0 * M * cfg.n_sensors  # whole job: forward + adjoint pairs
     value = pairs_iter / (ms * 1e-3)
 
@@ -273,9 +270,7 @@ def main():
         _ = float(loss_host[0])
     e2e_s = (time.perf_counter() - t0) / args.steps
     if world > 1:
-        tt = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+        e2e_s = max_over_ranks(dist, e2e_s, dev)
 
     # ---- roofline of the dominant kernel (forward or adjoint) on this rank
     fwd_ms, fwd_n = prof["forward"]

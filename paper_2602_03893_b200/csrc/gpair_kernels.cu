@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
 // One CTA per sensor j.  Warp w sums regions w, w+nw, ... into its private
 // shared-memory copy of the sensor's live range; copies are then summed in
 // warp order (deterministic).  Optionally fuses the residual and loss.
-constexpr int RED_BATCH = 4;
+constexpr int RED_BATCH = 8;  // regions in flight per warp (x Lf/32 loads each); Lf <= 128
 
 __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int32_t* __restrict__ wloT,
                                                 const int32_t* __restrict__ jlo_a, const int32_t* __restrict__ jlen_a,
@@ -154,25 +154,36 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
     double* mine = s_copy + (size_t)warp * jlen;
     for (int t = lane; t < jlen; t += 32) mine[t] = 0.0;
     __syncwarp();
+    // Warp w owns the contiguous region block [r_beg, r_end): one coalesced load
+    // brings 32 window starts, then RED_BATCH regions x Lf/32 values per lane are
+    // loaded before any is accumulated (memory-level parallelism).
     const int32_t* wl = wloT + (int64_t)j * nregions;
-    for (int r0 = warp; r0 < nregions; r0 += nw * RED_BATCH) {
-        int lo[RED_BATCH];
-#pragma unroll
-        for (int u = 0; u < RED_BATCH; ++u) {
-            int r = r0 + u * nw;
-            lo[u] = r < nregions ? wl[r] : -1;
-        }
-        for (int m0 = 0; m0 < Lf; m0 += 32) {
-            float val[RED_BATCH];
+    const int per_warp = (nregions + nw - 1) / nw;
+    const int r_beg = warp * per_warp, r_end = min(r_beg + per_warp, nregions);
+    const size_t rstride = (size_t)k.Nd * Lf;
+    const float* pj = partial + (size_t)j * Lf + lane;
+    for (int r0 = r_beg; r0 < r_end; r0 += 32) {
+        const int my_lo = (r0 + lane < r_end) ? wl[r0 + lane] : -1;
+        const int nr = min(32, r_end - r0);
+        for (int q0 = 0; q0 < Lf; q0 += 128)
+        for (int u0 = 0; u0 < nr; u0 += RED_BATCH) {
+            int lo[RED_BATCH];
+            float val[RED_BATCH][4];
 #pragma unroll
             for (int u = 0; u < RED_BATCH; ++u) {
-                int r = r0 + u * nw;
-                val[u] = lo[u] >= 0 ? partial[((int64_t)r * k.Nd + j) * Lf + m0 + lane] : 0.f;
+                lo[u] = __shfl_sync(0xffffffffu, my_lo, (u0 + u) & 31);
+                if (u0 + u >= nr) lo[u] = -1;
+                const float* src = pj + (size_t)(r0 + u0 + u) * rstride + q0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) val[u][q] = (lo[u] >= 0 && q0 + q * 32 < Lf) ? src[q * 32] : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < RED_BATCH; ++u) {
-                int n = lo[u] + m0 + lane;
-                if (lo[u] >= 0 && n < k.Nt) mine[n - jlo] += val[u];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = lo[u] + q0 + q * 32 + lane;
+                    if (lo[u] >= 0 && q0 + q * 32 < Lf && n < k.Nt) mine[n - jlo] += (double)val[u][q];
+                }
             }
         }
     }
