@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
     }
     __syncwarp();
     // flush: per 32-row block, in-place XOR-swizzled transpose then coalesced stores
-    float* dst = partial + ((int64_t)region * k.Nd + jbase) * Lf;
+    // sensor-major partials [N_d][regions][Lf]: the reducer streams each
+    // sensor's partials contiguously
+    const size_t jstride = (size_t)gridDim.x * Lf;
+    float* dst = partial + (size_t)jbase * jstride + (size_t)region * Lf;
     for (int m0 = 0; m0 < Lf; m0 += 32) {
         float v[32];
 #pragma unroll
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
         for (int t = 0; t < 32; ++t) s_acc[(m0 + t) * 32 + (lane ^ t)] = v[t];
         __syncwarp();
         for (int jj = 0; jj < 32; ++jj) {
-            if (jbase + jj < k.Nd) dst[(int64_t)jj * Lf + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
+            if (jbase + jj < k.Nd) dst[(size_t)jj * jstride + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
         }
     }
 }
@@ -160,8 +163,8 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
     const int32_t* wl = wloT + (int64_t)j * nregions;
     const int per_warp = (nregions + nw - 1) / nw;
     const int r_beg = warp * per_warp, r_end = min(r_beg + per_warp, nregions);
-    const size_t rstride = (size_t)k.Nd * Lf;
-    const float* pj = partial + (size_t)j * Lf + lane;
+    const size_t rstride = (size_t)Lf;
+    const float* pj = partial + (size_t)j * nregions * Lf + lane;
     for (int r0 = r_beg; r0 < r_end; r0 += 32) {
         const int my_lo = (r0 + lane < r_end) ? wl[r0 + lane] : -1;
         const int nr = min(32, r_end - r0);

@@ -15,3 +15,8 @@ for K in k_forward k_adjoint; do
       -o gpurun_out/prof_${CFG}_${K}_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${K}.log 2>&1
   echo "full $K rc=$?"
 done
+if [ -n "$PROFILE_REDUCE" ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_reduce" -c 1 \
+      -o gpurun_out/prof_${CFG}_k_reduce_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_k_reduce.log 2>&1
+  echo "full k_reduce rc=$?"
+fi
