@@ -13,6 +13,7 @@ FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-li
 
 
 def build(force=False, verbose=False):
+    extra = os.environ.get("GPAIR_NVCC_FLAGS", "").split()
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(HERE, "..", "include", "gpair.h"))
@@ -23,7 +24,7 @@ def build(force=False, verbose=False):
     for s in srcs:
         o = os.path.join(CSRC, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        procs.append((s, subprocess.Popen([NVCC, *FLAGS, "-c", s, "-o", o], stdout=subprocess.PIPE,
+        procs.append((s, subprocess.Popen([NVCC, *FLAGS, *extra, "-c", s, "-o", o], stdout=subprocess.PIPE,
                                           stderr=subprocess.STDOUT, text=True)))
     logs = []
     for s, p in procs:

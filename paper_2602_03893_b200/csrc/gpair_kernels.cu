@@ -41,8 +41,15 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 }
 
 // ------------------------------------------------------------------ forward
+#ifndef GPAIR_FWD_MINB
+#define GPAIR_FWD_MINB 3
+#endif
+#ifndef GPAIR_FWD_UNROLL
+#define GPAIR_FWD_UNROLL 1
+#endif
+constexpr int kFwdUnroll = GPAIR_FWD_UNROLL;  // unroll of the 8-kernel group loop
 template <int WMAX, int SER>
-__global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
+__global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  float* __restrict__ partial, int32_t cpr, int32_t ncells,
@@ -79,14 +86,17 @@ __global__ void __launch_bounds__(256) k_forward(const float4* __restrict__ kd, 
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             const bool gexact = SER == 0 && __any_sync(__activemask(), a.na == NA_EXACT);
+            const float4* kdg = s_kd + gq * GROUP;
+            const float* ampg = s_amp + gq * GROUP;
+#pragma unroll kFwdUnroll
             for (int t = 0; t < GROUP; ++t) {
                 const int li = gq * GROUP + t;
                 const int64_t gi = (int64_t)cb * CELL + li;
                 PairWin p;
                 if (SER == 0 && !gexact)
-                    p = pair_fast(a, s_kd[li], s_amp[li], orig, gi, Mpad, sx, sy, sz, k);
+                    p = pair_fast(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
                 else
-                    p = pair_setup<SER == 0 ? 2 : SER>(a, s_kd[li], s_amp[li], orig, gi, Mpad, sx, sy, sz, k);
+                    p = pair_setup<SER == 0 ? 2 : SER>(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
                 if (p.cnt <= 0) continue;
                 float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
                 if (p.cnt == WMAX && (WMAX & 1) == 0) {  // common case: packed pairs, no predicates
@@ -294,11 +304,15 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
         }
         __syncthreads();
         if (MODE != MODE_COUNT) {
-            for (int t = threadIdx.x; t < 32 * La; t += blockDim.x) {
-                const int jj = t / La, m = t - jj * La;
+            // warp per sensor row, lane per sample: coalesced row segments, no division
+            for (int jj = warp; jj < 32; jj += nw) {
                 const int lo = s_wlo[jj];
-                const int n = lo + m;
-                s_res[t] = (lo >= 0 && n < k.Nt) ? resid[(int64_t)(jb + jj) * k.Nt + n] : 0.f;
+                const float* src = resid + (int64_t)(jb + jj) * k.Nt;
+                float* dstr = s_res + jj * La;
+                for (int m = lane; m < La; m += 32) {
+                    const int n = lo + m;
+                    dstr[m] = (lo >= 0 && n < k.Nt) ? src[n] : 0.f;
+                }
             }
             __syncthreads();
         }
