@@ -136,15 +136,18 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     const size_t jstride = (size_t)gridDim.x * Lf;
     float* dst = partial + (size_t)jbase * jstride + (size_t)region * Lf;
     for (int m0 = 0; m0 < Lf; m0 += 32) {
+        const int rows = min(32, Lf - m0);  // 32, or a 16-row tail (Lf is a multiple of 16)
         float v[32];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = s_acc[(m0 + t) * 32 + lane];
+        for (int t = 0; t < 32; ++t) v[t] = (t < rows) ? s_acc[(m0 + t) * 32 + lane] : 0.f;
         __syncwarp();
 #pragma unroll
-        for (int t = 0; t < 32; ++t) s_acc[(m0 + t) * 32 + (lane ^ t)] = v[t];
+        for (int t = 0; t < 32; ++t)
+            if (t < rows) s_acc[(m0 + t) * 32 + (lane ^ t)] = v[t];
         __syncwarp();
         for (int jj = 0; jj < 32; ++jj) {
-            if (jbase + jj < k.Nd) dst[(size_t)jj * jstride + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
+            if (jbase + jj < k.Nd && lane < rows)
+                dst[(size_t)jj * jstride + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
         }
     }
 }
@@ -188,14 +191,14 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
                 if (u0 + u >= nr) lo[u] = -1;
                 const float* src = pj + (size_t)(r0 + u0 + u) * rstride + q0;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) val[u][q] = (lo[u] >= 0 && q0 + q * 32 < Lf) ? src[q * 32] : 0.f;
+                for (int q = 0; q < 4; ++q) val[u][q] = (lo[u] >= 0 && q0 + q * 32 + lane < Lf) ? src[q * 32] : 0.f;
             }
 #pragma unroll
             for (int u = 0; u < RED_BATCH; ++u) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int n = lo[u] + q0 + q * 32 + lane;
-                    if (lo[u] >= 0 && q0 + q * 32 < Lf && n < k.Nt) mine[n - jlo] += (double)val[u][q];
+                    if (lo[u] >= 0 && q0 + q * 32 + lane < Lf && n < k.Nt) mine[n - jlo] += (double)val[u][q];
                 }
             }
         }

@@ -159,9 +159,17 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
         float4 C = cell[cc];
         int a, b;
         double R;
-        if (cell_window(C, sx, sy, sz, k, a, b, R)) {
-            lo = min(lo, a);
-            hi = max(hi, b);
+        // union of the four 8-kernel group windows (tighter than the cell sphere)
+        for (int gq = 0; gq < GPC; ++gq) {
+            double Rg;
+            if (cell_window(grp[(int64_t)cc * GPC + gq], sx, sy, sz, k, a, b, Rg)) {
+                lo = min(lo, a);
+                hi = max(hi, b);
+            }
+        }
+        {
+            const double dx = (double)C.x - sx, dy = (double)C.y - sy, dz = (double)C.z - sz;
+            R = sqrt(dx * dx + dy * dy + dz * dz);
         }
         if (check) {
             if (!(R - (double)C.w > k.ks)) bad = 1;
@@ -352,7 +360,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->series_small = me <= EPS_SMALL ? 1 : 0;
         c->ser = c->series_small ? ((c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int) ? 0 : 2) : 5;
         int L = std::max(h_flags[2], 1);
-        int Lf = (L + 31) / 32 * 32;
+        int Lf = (L + 15) / 16 * 16;  // the flush transposes 32-row blocks plus a 16-row tail
         size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
         if (smem > smem_limit && cpr > 1) {
             cudaFree(wlo);
