@@ -23,6 +23,7 @@ brute force, finite differences).  Nothing is "parity unpinned".
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -62,6 +63,12 @@ def lib():
         L.oracle_adjoint.argtypes = [i64, vp, d, vp, i32, vp, d, d, d, i32, d, vp, vp, i64, vp]
         L.oracle_count_pair_samples.restype = i64
         L.oracle_count_pair_samples.argtypes = [i64, vp, d, i32, vp, d, d, d, i32, d, vp, i64]
+        L.oracle_assa_taps.restype = None
+        L.oracle_assa_taps.argtypes = [d, d, d, i32, d, vp]
+        L.oracle_assa_forward.restype = ctypes.c_int
+        L.oracle_assa_forward.argtypes = [i64, vp, vp, i32, vp, d, d, d, i32, d, d, i32, i32, vp, i32, vp]
+        L.oracle_assa_adjoint.restype = ctypes.c_int
+        L.oracle_assa_adjoint.argtypes = [i64, vp, i32, vp, d, d, d, i32, d, d, i32, i32, vp, vp, i64, vp]
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         L.oracle_get_threads.restype = ctypes.c_int
         _lib = L
@@ -168,3 +175,69 @@ def count_pair_samples(centers, sensors, *, sigma, v, fs, n_samples, t0=0.0, k=3
     return int(lib().oracle_count_pair_samples(M, _ptr(c), float(sigma), Nd, _ptr(s), float(v),
                                                float(fs), float(t0), int(n_samples), float(k),
                                                _ptr(cols), n_cols))
+
+
+# ---------------------------------------------------------------- ASSA (row f1)
+def assa_params(sigma, v, fs, k=3.0, n_min=25):
+    """Eq. 8.  N_half = ceil(k sigma / (v dt)) -- the ratio is
+    rounded to 12 significant digits before the ceiling so that an exact
+    integer ratio (8.0 at sigma = 0.1 mm, f_s = 40 MHz) is not pushed up by
+    its binary representation (reading A2); alpha = max(1, ceil(((N_min-1)/2)
+    / N_half)) in exact integer arithmetic; K = alpha N_half."""
+    ratio = float(f"{k * sigma * fs / v:.12g}")
+    n_half = max(1, int(math.ceil(ratio)))
+    num, den = n_min - 1, 2 * n_half  # ceil((N_min - 1) / (2 N_half))
+    alpha = max(1, -(-num // den))
+    return {"n_half": n_half, "alpha": alpha, "K": alpha * n_half, "fs_up": alpha * fs, "n_min": n_min}
+
+
+def assa_taps(sigma, v, fs_up, K, C=0.5):
+    """Eq. 11 (P:339-343), h[k + K] for k = -K..K."""
+    h = np.zeros(2 * K + 1)
+    lib().oracle_assa_taps(float(v), float(fs_up), float(sigma), int(K), float(C), _ptr(h))
+    return h
+
+
+def assa_forward(centers, amp, sensors, *, sigma, v, fs, n_samples, alpha, K, t0=0.0, k=3.0, rows=None):
+    """ASSA forward y = S_down(h * P_up x) (Eq. 13), Algorithm 1 ForwardOp."""
+    amp = np.ascontiguousarray(amp, dtype=np.float64)
+    M = amp.shape[0]
+    c = _f32_soa(centers, M)
+    Nd = np.asarray(sensors).shape[1]
+    s = _f32_soa(sensors, Nd)
+    if rows is not None:
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        n_rows = rows.shape[0]
+    else:
+        n_rows = Nd
+    y = np.zeros((n_rows, int(n_samples)), dtype=np.float64)
+    rc = lib().oracle_assa_forward(M, _ptr(c), _ptr(amp), Nd, _ptr(s), float(v), float(fs), float(t0),
+                                   int(n_samples), float(sigma), float(k), int(alpha), int(K), _ptr(rows), n_rows,
+                                   _ptr(y))
+    if rc == 2:
+        raise OracleGeometryError("a kernel-sensor distance r_ij <= k*sigma")
+    if rc != 0:
+        raise ValueError(f"oracle_assa_forward: invalid argument (rc={rc})")
+    return y
+
+
+def assa_adjoint(centers, delta, sensors, *, sigma, v, fs, alpha, K, t0=0.0, k=3.0, cols=None, n_kernels=None):
+    """ASSA adjoint g = P_up^T (h-bar * S_down^T delta) (Eq. 14), Algorithm 1 AdjointOp."""
+    delta = np.ascontiguousarray(delta, dtype=np.float64)
+    Nd, Nt = delta.shape
+    M = int(n_kernels) if n_kernels is not None else np.asarray(centers).shape[1]
+    c = _f32_soa(centers, M)
+    s = _f32_soa(sensors, Nd)
+    if cols is not None:
+        cols = np.ascontiguousarray(cols, dtype=np.int64)
+        n_cols = cols.shape[0]
+    else:
+        n_cols = M
+    g = np.zeros(n_cols, dtype=np.float64)
+    rc = lib().oracle_assa_adjoint(M, _ptr(c), Nd, _ptr(s), float(v), float(fs), float(t0), Nt, float(sigma),
+                                   float(k), int(alpha), int(K), _ptr(delta), _ptr(cols), n_cols, _ptr(g))
+    if rc == 2:
+        raise OracleGeometryError("a kernel-sensor distance r_ij <= k*sigma")
+    if rc != 0:
+        raise ValueError(f"oracle_assa_adjoint: invalid argument (rc={rc})")
+    return g

@@ -40,6 +40,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -218,4 +219,132 @@ int64_t oracle_count_pair_samples(int64_t M, const float* centers, double sigma,
         }
     }
     return total;
+}
+
+/* ------------------------------------------------------------------------
+ * ASSA operator: the paper's discrete operator,
+ * Eqs. 8-17 and Algorithm 1, stage by stage:
+ *   Eq. 9 projection P_up:  k_ij = floor((r_ij/v - t0) f_s^up + 0.5)
+ *          z_j[k] = sum_i x_i / r_ij 1(k = k_ij),  k = 0 .. N_t^up - 1
+ *   Eq. 11 taps h[k] = C d[k] exp(-d[k]^2 / (2 sigma^2)),
+ *          d[k] = -v k dt_up, k = -K .. K  (C = 1/2: reading A1)
+ *   Eq. 10 transposed convolution zt_j[k] = sum_m z_j[m] h[k - m]
+ *   Eq. 12 decimation y_j[n] = zt_j[alpha n]
+ *   Eqs. 15-17 adjoint: zero-fill, correlation with the
+ *          time-reversed taps, back-projection g_i = sum_j dconv_j[k_ij] / r_ij
+ * t0 (reading R3) shifts the upsampled grid: t_k = t0 + k dt_up.  Impulses
+ * with k_ij outside [0, N_t^up) do not exist (the indicator of Eq. 9 never
+ * fires); convolution sums run over the record only (reading A3).
+ * ---------------------------------------------------------------------- */
+
+/* Eq. 11 taps, fp64, h[k + K] for k = -K..K. */
+void oracle_assa_taps(double v, double fs_up, double sigma, int32_t K, double C, double* h) {
+    double dt_up = 1.0 / fs_up;
+    for (int32_t k = -K; k <= K; ++k) {
+        double d = -v * (double)k * dt_up;
+        h[k + K] = C * d * exp(-(d * d) / (2.0 * sigma * sigma));
+    }
+}
+
+/* Eq. 9 aligned index. */
+static int64_t assa_index(double r, double v, double t0, double fs_up) {
+    return (int64_t)floor((r / v - t0) * fs_up + 0.5);
+}
+
+int oracle_assa_forward(int64_t M, const float* centers, const double* amp, int32_t Nd, const float* sensors,
+                        double v, double fs, double t0, int32_t Nt, double sigma, double k, int32_t alpha,
+                        int32_t K, const int32_t* rows, int32_t n_rows, double* y) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc || alpha < 1 || K < 0) return rc ? rc : ORACLE_ERR_INVALID;
+    if (rows == NULL) n_rows = Nd;
+    const double fs_up = (double)alpha * fs;
+    const int64_t Nt_up = (int64_t)alpha * Nt;
+    const double ks = k * sigma;
+    double* h = (double*)malloc(sizeof(double) * (2 * K + 1));
+    oracle_assa_taps(v, fs_up, sigma, K, 0.5, h);
+    int err = ORACLE_OK;
+    int nth = oracle_get_threads();
+#pragma omp parallel num_threads(nth)
+    {
+        double* z = (double*)malloc(sizeof(double) * Nt_up);
+#pragma omp for schedule(dynamic, 1)
+        for (int32_t jo = 0; jo < n_rows; ++jo) {
+            int32_t j = rows ? rows[jo] : jo;
+            for (int64_t q = 0; q < Nt_up; ++q) z[q] = 0.0;
+            /* 1. P_up (Eq. 9) */
+            for (int64_t i = 0; i < M; ++i) {
+                double r = pair_distance(centers, M, i, sensors, Nd, j);
+                if (!(r > ks)) {
+#pragma omp atomic write
+                    err = ORACLE_ERR_GEOMETRY;
+                    continue;
+                }
+                int64_t kij = assa_index(r, v, t0, fs_up);
+                if (kij >= 0 && kij < Nt_up) z[kij] += amp[i] / r;
+            }
+            /* 2. transposed convolution (Eq. 10) at the decimated points (Eq. 12) */
+            double* yj = y + (int64_t)jo * Nt;
+            for (int32_t n = 0; n < Nt; ++n) {
+                int64_t kk = (int64_t)alpha * n;
+                double acc = 0.0;
+                for (int64_t m = kk - K; m <= kk + K; ++m) {
+                    if (m < 0 || m >= Nt_up) continue;
+                    acc += z[m] * h[(kk - m) + K];
+                }
+                yj[n] = acc;
+            }
+        }
+        free(z);
+    }
+    free(h);
+    return err;
+}
+
+int oracle_assa_adjoint(int64_t M, const float* centers, int32_t Nd, const float* sensors, double v, double fs,
+                        double t0, int32_t Nt, double sigma, double k, int32_t alpha, int32_t K,
+                        const double* delta, const int64_t* cols, int64_t n_cols, double* g) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc || alpha < 1 || K < 0) return rc ? rc : ORACLE_ERR_INVALID;
+    if (cols == NULL) n_cols = M;
+    const double fs_up = (double)alpha * fs;
+    const int64_t Nt_up = (int64_t)alpha * Nt;
+    const double ks = k * sigma;
+    double* h = (double*)malloc(sizeof(double) * (2 * K + 1));
+    oracle_assa_taps(v, fs_up, sigma, K, 0.5, h);
+    double* dconv = (double*)malloc(sizeof(double) * (size_t)Nd * Nt_up);
+    int nth = oracle_get_threads();
+    /* 1. zero-fill (Eq. 15) and 2. correlation with h-bar[k] = h[-k] (Eq. 16) */
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nth)
+    for (int32_t j = 0; j < Nd; ++j) {
+        double* dc = dconv + (int64_t)j * Nt_up;
+        for (int64_t q = 0; q < Nt_up; ++q) {
+            double acc = 0.0;
+            for (int64_t m = q - K; m <= q + K; ++m) {
+                if (m < 0 || m >= Nt_up || (m % alpha) != 0) continue;  /* delta_up[m] = 0 off-grid */
+                acc += h[(m - q) + K] * delta[(int64_t)j * Nt + m / alpha];
+            }
+            dc[q] = acc;
+        }
+    }
+    /* 3. back-projection (Eq. 17) */
+    int err = ORACLE_OK;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nth)
+    for (int64_t io = 0; io < n_cols; ++io) {
+        int64_t i = cols ? cols[io] : io;
+        double acc = 0.0;
+        for (int32_t j = 0; j < Nd; ++j) {
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            if (!(r > ks)) {
+#pragma omp atomic write
+                err = ORACLE_ERR_GEOMETRY;
+                continue;
+            }
+            int64_t kij = assa_index(r, v, t0, fs_up);
+            if (kij >= 0 && kij < Nt_up) acc += dconv[(int64_t)j * Nt_up + kij] / r;
+        }
+        g[io] = acc;
+    }
+    free(dconv);
+    free(h);
+    return err;
 }
