@@ -35,6 +35,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="cfg4")
+    p.add_argument("--op", default="exact", choices=["exact", "assa"],
+                   help="exact: Eq. 7 windows (north_star); assa: the paper's ASSA operator (row f1)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
@@ -203,7 +205,7 @@ def main():
     Ml = hi - lo
     ctx = gpair.Context(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), sigma=cfg.sig, v=cfg.v,
                         fs=cfg.fs, n_samples=cfg.n_samples, t0=cfg.t0, k=cfg.k, rank=rank, world=world,
-                        nccl_comm=comm)
+                        nccl_comm=comm, assa=(args.op == "assa"))
     info = ctx.info()
     pair_samples_local = ctx.count_pair_samples()
     # measured data b: forward of the vessel phantom (a workload input only)
@@ -290,9 +292,10 @@ def main():
         except Exception:
             traffic = None
     f_meas = (clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965) * 1e6
-    roof = {"bound": "alu", "kernel": f"k_{dom}", "achieved": achieved / 1e9, "peak": peak / 1e9,
-            "unit": "Gpair-samples/s", "frac": achieved / peak, "traffic": traffic,
-            "frac_at_measured_clock": achieved / (n_sm * SFU_PER_CLK_SM * f_meas),
+    roof = {"bound": "alu", "kernel": f"k_{'assa_' if args.op == 'assa' else ''}{dom}", "achieved": achieved / 1e9,
+            "peak": peak / 1e9 if args.op == "exact" else None,
+            "unit": "Gpair-samples/s", "frac": achieved / peak if args.op == "exact" else None, "traffic": traffic,
+            "frac_at_measured_clock": (achieved / (n_sm * SFU_PER_CLK_SM * f_meas)) if args.op == "exact" else None,
             "peak_def": f"{n_sm} SMs x {SFU_PER_CLK_SM} SFU ex2/clk x {f_max / 1e6:.0f} MHz (one exp per pair-sample; "
                         "DESIGN.md 'Roofline')",
             "pair_samples_per_launch": pair_samples_local,
@@ -303,7 +306,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "kernels": M, "sensors": cfg.n_sensors, "samples": cfg.n_samples,
+        "config": {"workload": args.config, "operator": args.op, "kernels": M, "sensors": cfg.n_sensors, "samples": cfg.n_samples,
                    "array": cfg.array, "fs_hz": cfg.fs, "sigma_m": cfg.sig, "k": cfg.k,
                    "step": "gpair_iterate (NPC + forward + residual/loss + adjoint + Adam)",
                    "parallelism": f"kernel-sharded x{world}" if world > 1 else "single GPU",

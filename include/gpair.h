@@ -62,7 +62,14 @@ typedef enum {
 /* gpair_desc.flags */
 enum {
     GPAIR_TOF_EXACT = 0,        /* Eq. 7 evaluated at the exact time of flight (this build) */
-    GPAIR_TOF_ASSA = 1,         /* reserved: ASSA-snapped ToF, not implemented */
+    GPAIR_TOF_ASSA = 1,         /* the paper's ASSA operator (Eqs. 8-17, Alg. 1):
+                                   ToF snapped to the alpha-upsampled grid, k_ij =
+                                   floor((r/v - t0) f_s^up + 0.5); taps h[k] = (1/2) d[k]
+                                   exp(-d[k]^2/2 sigma^2), d[k] = -v k dt_up, |k| <= K;
+                                   y_j[n] = sum_i (A_i / r_ij) h[alpha n - k_ij]; the adjoint
+                                   is its exact transpose (zero-fill, correlation,
+                                   back-projection).  Impulses with k_ij outside
+                                   [0, alpha N_t) do not exist (reading A3). */
     GPAIR_CHECK_FINITE = 1 << 9 /* gpair_iterate syncs and checks the loss is finite */
 };
 
@@ -81,7 +88,8 @@ typedef struct {
     const float* sensors;  /* DEVICE [3][N_d] SoA point-detector positions [m]   */
     int32_t rank, world;   /* kernel-shard index / count; world >= 1                      */
     void* nccl_comm;       /* ncclComm_t over `world` ranks (borrowed) or NULL if world=1 */
-    int32_t flags;         /* GPAIR_TOF_EXACT | GPAIR_CHECK_FINITE                        */
+    int32_t flags;         /* GPAIR_TOF_EXACT or GPAIR_TOF_ASSA, | GPAIR_CHECK_FINITE      */
+    int32_t assa_nmin;     /* ASSA N_min ("set to 25"); <= 0 -> 25; ignored unless ASSA */
 } gpair_desc;
 
 /* One IR iteration's hyper-parameters (Algorithm 2). */
@@ -129,6 +137,10 @@ typedef struct {
     int32_t grid_detected;      /* 1 if centres were recognised as a regular grid        */
     double max_eps;             /* max |q|/R^2 of the anchor expansion       */
     int64_t workspace_bytes;    /* device bytes owned by the context                    */
+    int32_t assa;               /* 1 if the context implements the ASSA operator        */
+    int32_t assa_alpha;         /* ASSA upsampling ratio alpha (Eq. 8)                  */
+    int32_t assa_n_half;        /* ASSA N_half (Eq. 8)                                  */
+    int32_t assa_K;             /* ASSA taps half-width K = alpha N_half (Eq. 11)       */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial
@@ -164,7 +176,8 @@ gpair_status gpair_iterate(gpair_ctx* ctx, float* z, float* m, float* v, const f
                            float* loss_out, void* stream);
 
 /* Exact number of in-window pair-samples (|d| < k sigma, n in [0, N_t)) of
- * this rank's operator; synchronous.  Host output. */
+ * this rank's operator; for an ASSA context, the number of existing impulses
+ * (pairs with k_ij in [0, alpha N_t)).  Synchronous.  Host output. */
 gpair_status gpair_count_pair_samples(gpair_ctx* ctx, int64_t* out_host, void* stream);
 
 /* Fill *out (host struct) with the context's build parameters. */

@@ -26,6 +26,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import adjoint as _adjoint
+from . import assa_adjoint as _assa_adjoint
+from . import assa_forward as _assa_forward
 from . import forward as _forward
 
 EPS_NPC = 1e-8
@@ -97,12 +99,19 @@ def data_loss(y, b):
 def loss_and_grad(z, b, geom, hp: Hyper):
     """L(z) and dL/dz for lambda = 0 (Alg. 2)."""
     x = npc(z, hp.eps_npc) if hp.mode == "npc" else z
-    y = _forward(geom["centers"], x, geom["sensors"], **geom["op"])
+    assa = geom.get("assa")  # {"alpha", "K"}: the ASSA operator (row f1) instead of Eq. 7
+    if assa:
+        y = _assa_forward(geom["centers"], x, geom["sensors"], **geom["op"], **assa)
+    else:
+        y = _forward(geom["centers"], x, geom["sensors"], **geom["op"])
     r = y - b
     N = r.size
     L = float(np.sum(r * r) / N)
     scale = (2.0 / N) if hp.grad_scale is None else hp.grad_scale
-    gx = _adjoint(geom["centers"], scale * r, geom["sensors"], **_adj_kw(geom["op"]))
+    if assa:
+        gx = _assa_adjoint(geom["centers"], scale * r, geom["sensors"], **_adj_kw(geom["op"]), **assa)
+    else:
+        gx = _adjoint(geom["centers"], scale * r, geom["sensors"], **_adj_kw(geom["op"]))
     gz = npc_chain(gx, z, hp.eps_npc) if hp.mode == "npc" else gx
     return L, gz, y
 

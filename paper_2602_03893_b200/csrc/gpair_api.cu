@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "gpair_ctx.h"
 
@@ -134,6 +135,8 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_loss_part);
     cudaFree(c->d_count);
     cudaFree(c->d_flags);
+    cudaFree(c->d_taps);
+    cudaFree(c->d_dconv);
     prof_drain(c);
     for (auto e : c->prof_free) cudaEventDestroy(e);
     delete c;
@@ -210,7 +213,6 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     if (d->n_kernels < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_kernels must be >= 1");
     if (!d->centers || !d->sensors) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "centers/sensors NULL");
     if (d->sigmas) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "per-kernel sigmas are not supported (must be NULL)");
-    if (d->flags & GPAIR_TOF_ASSA) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "GPAIR_TOF_ASSA not implemented");
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
         return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "rank/world invalid");
     if (d->world > 1 && !d->nccl_comm) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "world > 1 needs nccl_comm");
@@ -250,6 +252,35 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
         k.c_u = k.ku - 0.5f;
     }
     k.K1u = (float)(-log2e * h * h / (2.0 * s * s));
+    k.win_half = k.ks;
+    k.two_over_h = (float)(2.0 / h);
+    const bool assa = (d->flags & GPAIR_TOF_ASSA) != 0;
+    std::vector<float> taps;
+    if (assa) {
+        // Eq. 8, integer arithmetic as in oracle.assa_params (reading A2)
+        const int nmin = d->assa_nmin > 0 ? d->assa_nmin : 25;
+        if (nmin < 3) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "assa_nmin must be >= 3");
+        char buf[64];
+        snprintf(buf, sizeof(buf), "%.12g", kk * s * fs / v);
+        const double ratio = std::strtod(buf, nullptr);
+        const int n_half = std::max(1, (int)std::ceil(ratio));
+        const int num = nmin - 1, den = 2 * n_half;
+        const int alpha = std::max(1, (num + den - 1) / den);
+        k.alpha = alpha;
+        k.n_half = n_half;
+        k.K = alpha * n_half;
+        k.fs_up = (double)alpha * fs;
+        if (2 * k.K + 1 > 1024) return fail(nullptr, GPAIR_ERR_RESOURCE, "ASSA taps table > 1024 entries");
+        if ((int64_t)alpha * d->n_samples >= (1LL << 30)) return fail(nullptr, GPAIR_ERR_RESOURCE, "alpha N_t too large");
+        // Eq. 11 taps in fp64, C = 1/2 (reading A1)
+        const double dt_up = 1.0 / k.fs_up;
+        taps.resize(2 * k.K + 1);
+        for (int q = -k.K; q <= k.K; ++q) {
+            const double dq = -v * (double)q * dt_up;
+            taps[q + k.K] = (float)(0.5 * dq * std::exp(-(dq * dq) / (2.0 * s * s)));
+        }
+        k.win_half = std::max(k.ks, (n_half + 1) * h);
+    }
 
     gpair_ctx* c = new (std::nothrow) gpair_ctx();
     if (!c) return fail(nullptr, GPAIR_ERR_RESOURCE, "host allocation failed");
@@ -266,6 +297,7 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     c->world = d->world;
     c->nccl = d->nccl_comm;
     c->flags = d->flags;
+    c->assa = assa ? 1 : 0;
     cudaStream_t st = (cudaStream_t)stream;
     std::string why;
     int geom_err = 0;
@@ -278,6 +310,19 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     if (geom_err) {
         free_ctx(c);
         return fail(nullptr, (gpair_status)geom_err, why);
+    }
+    if (assa) {
+        e = cudaMalloc(&c->d_taps, sizeof(float) * taps.size());
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(c->d_taps, taps.data(), sizeof(float) * taps.size(), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMalloc(&c->d_dconv, sizeof(float) * (size_t)c->Nd * k.alpha * c->Nt);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            std::string m = std::string("gpair_create (ASSA buffers): ") + cudaGetErrorString(e);
+            free_ctx(c);
+            return fail(nullptr, GPAIR_ERR_RESOURCE, m);
+        }
+        c->workspace_bytes += (int64_t)(sizeof(float) * (taps.size() + (size_t)c->Nd * k.alpha * c->Nt));
     }
     *out = c;
     return GPAIR_OK;
@@ -306,6 +351,10 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->grid_detected = c->grid_detected;
     o->max_eps = c->max_eps;
     o->workspace_bytes = c->workspace_bytes;
+    o->assa = c->assa;
+    o->assa_alpha = c->k.alpha;
+    o->assa_n_half = c->k.n_half;
+    o->assa_K = c->k.K;
     return GPAIR_OK;
 }
 
@@ -317,7 +366,7 @@ static gpair_status do_forward_core(gpair_ctx* c, const float* src, int npc, flo
     }
     {
         ProfScope ps(c, GPAIR_PROF_FORWARD, st);
-        API_CUDA(c, gpair::launch_forward(c, st), "forward");
+        API_CUDA(c, c->assa ? gpair::launch_assa_forward(c, st) : gpair::launch_forward(c, st), "forward");
     }
     if (c->world == 1) {
         ProfScope ps(c, GPAIR_PROF_REDUCE, st);
@@ -355,7 +404,10 @@ gpair_status gpair_adjoint(gpair_ctx* c, const float* residual, float* grad, voi
     ep.scale = 1.f;
     ep.g_out = grad;
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
-    API_CUDA(c, gpair::launch_adjoint(c, residual, gpair::EPI_GRAD, ep, st), "adjoint");
+    API_CUDA(c,
+             c->assa ? gpair::launch_assa_adjoint(c, residual, gpair::EPI_GRAD, ep, st)
+                     : gpair::launch_adjoint(c, residual, gpair::EPI_GRAD, ep, st),
+             "adjoint");
     return GPAIR_OK;
 }
 
@@ -402,7 +454,10 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     ep.v = v;
     ep.x_out = x_out;
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
-    API_CUDA(c, gpair::launch_adjoint(c, c->d_delta, npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP, ep, st),
+    const int emode = npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP;
+    API_CUDA(c,
+             c->assa ? gpair::launch_assa_adjoint(c, c->d_delta, emode, ep, st)
+                     : gpair::launch_adjoint(c, c->d_delta, emode, ep, st),
              "adjoint+update");
     return GPAIR_OK;
 }
@@ -410,7 +465,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
 gpair_status gpair_count_pair_samples(gpair_ctx* c, int64_t* out, void* stream) {
     if (!c || !out) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "NULL argument");
     cudaStream_t st = (cudaStream_t)stream;
-    API_CUDA(c, gpair::launch_count(c, st), "count");
+    API_CUDA(c, c->assa ? gpair::launch_assa_count(c, st) : gpair::launch_count(c, st), "count");
     unsigned long long h = 0;
     API_CUDA(c, cudaMemcpyAsync(&h, c->d_count, sizeof(h), cudaMemcpyDeviceToHost, st), "count readback");
     API_CUDA(c, cudaStreamSynchronize(st), "count sync");

@@ -1,0 +1,293 @@
+// gpair_assa.cu -- the paper's ASSA operator (PAPER.md
+// Eqs. 8-17 and Algorithm 1), B200-native.
+//
+// Forward (Eq. 13, y = S_down(h * P_up x)) in the paper's own structure, with
+// the intermediate buffer kept on chip:
+//   k_assa_forward  lane = sensor, warp = 32 sensors, CTA = region of cells.
+//                   P_up (Eq. 9): every pair adds A_i / r_ij into its sensor's
+//                   upsampled histogram z_j[k_ij] held in a private shared-
+//                   memory column (one RMW per pair, no atomics); then each
+//                   lane evaluates the transposed convolution (Eq. 10) only at
+//                   the decimated points alpha n (Eq. 12) and the region trace
+//                   is flushed like k_forward (same partial layout, reduced by
+//                   k_reduce in a fixed order).
+// Adjoint (Eq. 14, g = P_up^T (h-bar * S_down^T delta)):
+//   k_assa_dconv    zero-fill (Eq. 15) + correlation with h-bar (Eq. 16), one
+//                   thread per upsampled sample: dconv_j[q] = sum_n h[alpha n - q] delta_j[n].
+//   k_assa_adjoint  lane = kernel: back-projection (Eq. 17) g_i = sum_j
+//                   dconv_j[k_ij] / r_ij from dconv windows staged in shared
+//                   memory, fused with the same update epilogue as k_adjoint.
+// k_ij and the weight 1/r_ij come from assa_setup() (gpair_internal.cuh): the
+// fp64 group anchors of the exact operator, with an fp64 re-decision of the
+// rounding (bit-identical to the oracle) when alpha eu + 1/2 is near an integer.
+#include <algorithm>
+
+#include "gpair_ctx.h"
+
+namespace gpair {
+
+namespace {
+
+constexpr int A_STAGE = 8;     // cells staged per step
+constexpr int A_WARPS = 4;     // sensor warps per forward CTA
+constexpr int MAX_TAPS = 1024; // 2K+1 limit of the shared-memory taps table
+
+// The convolution writes its outputs in place (rows [0, Lf)) when every later
+// output chunk only reads rows past the ones already overwritten:
+// alpha (32 c + 32) - K >= 32 c + 32 for all c >= 0  <=>  K <= 32 (alpha - 1).
+__host__ __device__ inline bool conv_inplace(int alpha, int K) { return alpha >= 2 && K <= 32 * (alpha - 1); }
+int zrows_of(int alpha, int K, int Lf) { return conv_inplace(alpha, K) ? alpha * Lf : (alpha + 1) * Lf; }
+
+template <int SER>
+__global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
+    const float4* __restrict__ kd, const float* __restrict__ amp, const float4* __restrict__ grp,
+    const float* __restrict__ orig, const float* __restrict__ sens, const int32_t* __restrict__ wlo,
+    const float* __restrict__ taps, float* __restrict__ partial, int32_t cpr, int32_t ncells, int32_t Lf,
+    int32_t zrows, int64_t Mpad, OpConst k) {
+    extern __shared__ float4 smem4[];
+    float4* s_kd = smem4;                                // [A_STAGE*32]
+    float4* s_grp = s_kd + A_STAGE * CELL;               // [A_STAGE*GPC]
+    float* s_amp = (float*)(s_grp + A_STAGE * GPC);      // [A_STAGE*32]
+    float* s_taps = s_amp + A_STAGE * CELL;              // [2K+1] (padded to 4)
+    const int ntaps = 2 * k.K + 1;
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_z = s_taps + ((ntaps + 3) & ~3) + (size_t)warp * zrows * 32;
+
+    for (int t = threadIdx.x; t < ntaps; t += blockDim.x) s_taps[t] = taps[t];
+    const int region = blockIdx.x;
+    const int jbase = (blockIdx.y * nw + warp) * 32;
+    const int j = jbase + lane;
+    const bool jok = j < k.Nd;
+    for (int t = lane; t < zrows * 32; t += 32) s_z[t] = 0.f;
+    const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
+    const int klo = k.alpha * lo_j;  // upsampled index of the column's first row
+    const int kmax = k.alpha * k.Nt;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    if (jok) {
+        sx = sens[j];
+        sy = sens[k.Nd + j];
+        sz = sens[2 * k.Nd + j];
+    }
+    float* zc = s_z + lane;
+    // ---- 1. projection P_up (Eq. 9): one shared-memory RMW per pair
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    for (int cb = c0; cb < c1; cb += A_STAGE) {
+        const int nc = min(A_STAGE, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            s_kd[t] = kd[(int64_t)cb * CELL + t];
+            s_amp[t] = amp[(int64_t)cb * CELL + t];
+        }
+        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        __syncthreads();
+        for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+#pragma unroll 2
+            for (int t = 0; t < GROUP; ++t) {
+                const int li = gq * GROUP + t;
+                const AssaPair p =
+                    assa_setup<SER>(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy, sz, k);
+                if (p.k >= 0 && p.k < kmax) zc[(p.k - klo) * 32] += p.w;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- 2. transposed convolution (Eq. 10) at the decimated points (Eq. 12),
+    // per lane on its own column, in chunks of 32 outputs (conv_inplace():
+    // later chunks never read rows already overwritten; otherwise the outputs
+    // go to rows [alpha Lf, (alpha+1) Lf)).
+    const int zlim = k.alpha * Lf;
+    const int yoff = conv_inplace(k.alpha, k.K) ? 0 : zlim;
+    for (int cc = 0; cc < Lf; cc += 32) {
+        float yv[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+            const int pc = k.alpha * (cc + t);
+            float acc = 0.f;
+            const int qlo = max(-k.K, pc - zlim + 1), qhi = min(k.K, pc);
+            for (int q = qlo; q <= qhi; ++q) acc = fmaf(zc[(pc - q) * 32], s_taps[q + k.K], acc);
+            yv[t] = acc;
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+            if (cc + t < Lf) zc[(yoff + cc + t) * 32] = yv[t];
+    }
+    __syncwarp();
+    // ---- 3. flush the region trace (same layout and transpose as k_forward)
+    float* s_acc = s_z + (size_t)yoff * 32;
+    const size_t jstride = (size_t)gridDim.x * Lf;
+    float* dst = partial + (size_t)jbase * jstride + (size_t)region * Lf;
+    for (int m0 = 0; m0 < Lf; m0 += 32) {
+        const int rows = min(32, Lf - m0);
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = (t < rows) ? s_acc[(m0 + t) * 32 + lane] : 0.f;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+            if (t < rows) s_acc[(m0 + t) * 32 + (lane ^ t)] = v[t];
+        __syncwarp();
+        for (int jj = 0; jj < 32; ++jj)
+            if (jbase + jj < k.Nd && lane < rows)
+                dst[(size_t)jj * jstride + m0 + lane] = s_acc[(m0 + lane) * 32 + (jj ^ lane)];
+    }
+}
+
+// zero-fill + correlation (Eqs. 15-16): dconv_j[q] = sum_{n: |alpha n - q| <= K} h[alpha n - q] delta_j[n]
+__global__ void k_assa_dconv(const float* __restrict__ resid, const float* __restrict__ taps, OpConst k,
+                             float* __restrict__ dconv) {
+    const int j = blockIdx.y;
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Nup = k.alpha * k.Nt;
+    if (q >= Nup) return;
+    const float* dj = resid + (int64_t)j * k.Nt;
+    const int num = q - k.K;  // n_lo = ceil((q - K) / alpha), clipped at 0
+    const int nlo = max(0, num >= 0 ? (num + k.alpha - 1) / k.alpha : -((-num) / k.alpha));
+    const int nhi = min(k.Nt - 1, (q + k.K) / k.alpha);
+    float acc = 0.f;
+    for (int n = nlo; n <= nhi; ++n) acc = fmaf(taps[k.alpha * n - q + k.K], dj[n], acc);
+    dconv[(int64_t)j * Nup + q] = acc;
+}
+
+constexpr int MODE_COUNT = 3;
+
+template <int SER, int MODE>
+__global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__ kd, const float4* __restrict__ grp,
+                                                      const float* __restrict__ orig, const int32_t* __restrict__ perm,
+                                                      const float* __restrict__ sens, const int32_t* __restrict__ wlo,
+                                                      const float* __restrict__ dconv, int32_t cpr, int32_t ncells,
+                                                      int32_t Lz, int64_t Mpad, OpConst k, EpiParams ep,
+                                                      unsigned long long* count) {
+    extern __shared__ float4 smem4[];
+    Anchor* s_anc = (Anchor*)smem4;                          // [nw][GPC][33]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t* s_wlo = (int32_t*)(s_anc + nw * GPC * 33);     // [32]
+    float* s_dc = (float*)(s_wlo + 32);                      // [32][Lz]
+
+    const int cid = blockIdx.x * cpr + warp;
+    const bool cok = (warp < cpr) && (cid < ncells);
+    const int64_t gi = (int64_t)cid * CELL + lane;
+    float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cok) d4 = kd[gi];
+    const Anchor* my_anc = s_anc + (warp * GPC + lane / GROUP) * 33;
+    const int Nup = k.alpha * k.Nt;
+    float acc = 0.f;
+    unsigned long long nimp = 0;
+    const bool real = cok && perm[gi] >= 0;
+    for (int jb = 0; jb < k.Nd; jb += 32) {
+        const int nj = min(32, k.Nd - jb);
+        __syncthreads();
+        if (threadIdx.x < 32)
+            s_wlo[threadIdx.x] = threadIdx.x < nj ? wlo[(int64_t)blockIdx.x * k.Nd + jb + threadIdx.x] : -1;
+        if (cok && lane < nj) {
+            const int j = jb + lane;
+            const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
+#pragma unroll
+            for (int gq = 0; gq < GPC; ++gq)
+                s_anc[(warp * GPC + gq) * 33 + lane] = make_anchor(grp[(int64_t)cid * GPC + gq], sx, sy, sz, k);
+        }
+        __syncthreads();
+        if (MODE != MODE_COUNT) {
+            for (int jj = warp; jj < 32; jj += nw) {
+                const int lo = s_wlo[jj];
+                const int qlo = k.alpha * lo;
+                const float* src = dconv + (int64_t)(jb + jj) * Nup;
+                float* dstr = s_dc + jj * Lz;
+                for (int m = lane; m < Lz; m += 32) {
+                    const int q = qlo + m;
+                    dstr[m] = (lo >= 0 && q < Nup) ? src[q] : 0.f;
+                }
+            }
+            __syncthreads();
+        }
+        if (!cok) continue;
+        float accb = 0.f;
+        for (int jj = 0; jj < nj; ++jj) {
+            const int lo = s_wlo[jj];
+            if (lo < 0) continue;
+            const int j = jb + jj;
+            const AssaPair p = assa_setup<SER>(my_anc[jj], d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j],
+                                               sens[2 * k.Nd + j], k);
+            if (p.k < 0 || p.k >= Nup) continue;
+            if (MODE == MODE_COUNT) {
+                nimp += real ? 1ull : 0ull;
+                continue;
+            }
+            accb = fmaf(p.w, s_dc[jj * Lz + (p.k - k.alpha * lo)], accb);  // Eq. 17
+        }
+        acc += accb;
+    }
+    if (!cok) return;
+    if (MODE == MODE_COUNT) {
+        for (int o = 16; o > 0; o >>= 1) nimp += __shfl_xor_sync(0xffffffffu, nimp, o);
+        if (lane == 0) atomicAdd(count, nimp);
+        return;
+    }
+    const int32_t ic = perm[gi];
+    if (ic < 0) return;
+    adjoint_epilogue<MODE>(acc, ic, ep);
+}
+
+template <int SER>
+cudaError_t assa_fwd_launch(gpair_ctx* c, cudaStream_t st) {
+    const size_t smem = assa_forward_smem(c, c->Lf);
+    cudaError_t e = cudaFuncSetAttribute(k_assa_forward<SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(c->f_regions, c->f_sgroups);
+    k_assa_forward<SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
+                                                             c->d_wlo_f, c->d_taps, c->d_partial, c->f_cpr, c->ncells,
+                                                             c->Lf, zrows_of(c->k.alpha, c->k.K, c->Lf), c->Mpad, c->k);
+    return cudaGetLastError();
+}
+
+template <int SER, int MODE>
+cudaError_t assa_adj_launch(gpair_ctx* c, const EpiParams& ep, cudaStream_t st) {
+    const int Lz = c->k.alpha * c->La + 2 * c->k.alpha;
+    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 + (MODE == MODE_COUNT ? 0 : (size_t)32 * Lz * 4);
+    cudaError_t e =
+        cudaFuncSetAttribute(k_assa_adjoint<SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int threads = 32 * std::max(c->a_cpr, 1);
+    k_assa_adjoint<SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm,
+                                                                   c->d_sens, c->d_wlo_a, c->d_dconv, c->a_cpr,
+                                                                   c->ncells, Lz, c->Mpad, c->k, ep, c->d_count);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t assa_adj_dispatch(gpair_ctx* c, const EpiParams& ep, cudaStream_t st) {
+    return c->series_small ? assa_adj_launch<2, MODE>(c, ep, st) : assa_adj_launch<5, MODE>(c, ep, st);
+}
+
+}  // namespace
+
+size_t assa_forward_smem(const gpair_ctx* c, int Lf) {
+    const int ntaps = 2 * c->k.K + 1;
+    return (size_t)A_STAGE * CELL * 20 + A_STAGE * GPC * 16 + (size_t)((ntaps + 3) & ~3) * 4 +
+           (size_t)c->f_warps * zrows_of(c->k.alpha, c->k.K, Lf) * 32 * 4;
+}
+
+cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st) {
+    if (2 * c->k.K + 1 > MAX_TAPS) return cudaErrorInvalidValue;
+    return c->series_small ? assa_fwd_launch<2>(c, st) : assa_fwd_launch<5>(c, st);
+}
+
+cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
+    const int Nup = c->k.alpha * c->Nt;
+    dim3 g((Nup + 255) / 256, c->Nd);
+    k_assa_dconv<<<g, 256, 0, st>>>(resid, c->d_taps, c->k, c->d_dconv);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (mode == EPI_GRAD) return assa_adj_dispatch<EPI_GRAD>(c, ep, st);
+    if (mode == EPI_NPC_ADAM) return assa_adj_dispatch<EPI_NPC_ADAM>(c, ep, st);
+    return assa_adj_dispatch<EPI_CLAMP>(c, ep, st);
+}
+
+cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    EpiParams ep{};
+    return assa_adj_dispatch<MODE_COUNT>(c, ep, st);
+}
+
+}  // namespace gpair

@@ -25,6 +25,9 @@ struct gpair_ctx_s {
     double max_eps = 0.0;
     int series_small = 0;  // 1: every group's |eps| <= EPS_SMALL -> degree-2 series
     int ser = 5;           // kernel path: 0 = pair_fast, 2 / 5 = pair_setup<SER> (gpair_kernels.cu)
+    int assa = 0;          // 1: ASSA operator (row f1, gpair_assa.cu)
+    float* d_taps = nullptr;   // [2K+1] ASSA taps h[k + K] (fp64-computed, fp32)
+    float* d_dconv = nullptr;  // [Nd][alpha Nt] ASSA adjoint correlation buffer
 
     // geometry in the internal (spatially sorted) order
     float* d_sens = nullptr;   // [3][Nd]
@@ -88,8 +91,41 @@ struct EpiParams {
     float* x_out;
 };
 enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
+
+// Adjoint epilogue: g = scale * acc, then either write g,
+// or the NPC chain rule (Eq. 19) + bias-corrected Adam,
+// or the projected clamp step x <- max(x - lr g, 0); ic = caller index.
+template <int MODE>
+__device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const EpiParams& ep) {
+    const float g = acc * ep.scale;
+    if (MODE == EPI_GRAD) {
+        ep.g_out[ic] = g;
+    } else if (MODE == EPI_NPC_ADAM) {
+        float z = ep.z[ic];
+        const float gz = g * (2.f * (z + ep.eps_npc));
+        const float mm = ep.beta1 * ep.m[ic] + (1.f - ep.beta1) * gz;
+        const float vv = ep.beta2 * ep.v[ic] + (1.f - ep.beta2) * gz * gz;
+        const float mh = mm * ep.bc1, vh = vv * ep.bc2;
+        z = z - ep.lr * mh / (sqrtf(vh) + ep.adam_eps);
+        ep.z[ic] = z;
+        ep.m[ic] = mm;
+        ep.v[ic] = vv;
+        if (ep.x_out) ep.x_out[ic] = (z + ep.eps_npc) * (z + ep.eps_npc);
+    } else {
+        const float x = fmaxf(ep.z[ic] - ep.lr * g, 0.f);
+        ep.z[ic] = x;
+        if (ep.x_out) ep.x_out[ic] = x;
+    }
+}
+
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 int pick_wmax(int w);
+
+// ASSA operator (gpair_assa.cu)
+size_t assa_forward_smem(const gpair_ctx* c, int Lf);
+cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st);
+cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
+cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st);
 
 }  // namespace gpair

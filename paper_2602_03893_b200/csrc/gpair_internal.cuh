@@ -50,6 +50,13 @@ struct OpConst {
     float c_u;             // ku - 1/2    (pair_fast)
     float ku;              // k sigma / h  [samples]
     float K1u;             // -log2(e) h^2 / (2 sigma^2)
+    // ASSA operator (row f1, Eqs. 8-12); alpha = 0 for the exact operator
+    int32_t alpha;         // upsampling ratio
+    int32_t K;             // taps half-width alpha N_half
+    int32_t n_half;        // N_half
+    double fs_up;          // alpha f_s (computed as (double)alpha * fs, like the oracle)
+    float two_over_h;      // 2 / h: (A h / 2r) * (2/h) = A / r
+    double win_half;       // half-width [m] of the conservative sample windows (setup)
 };
 
 // fp64 anchor of a (group, sensor) pair, reduced to what the per-pair fp32
@@ -261,6 +268,69 @@ __device__ __forceinline__ PairWin pair_fast(const Anchor& a, float4 kd, float A
     const bool amb = fabsf(d) > 0.5f - GAMMA;
     if (amb || (unsigned)p.n_lo > (unsigned)(k.Nt - k.cnt_int))
         p = pair_fix(p, eu, a.na, amb, orig, gi, Mpad, sx, sy, sz, k.cnt_int, k);
+    return p;
+}
+
+// ---- ASSA (row f1): aligned upsampled index k_ij and weight A / r_ij.
+// k_ij = floor((r/v - t0) f_s^up + 0.5) = alpha n_a + floor(alpha eu + 1/2)
+// (alpha n_a is an exact integer).  When alpha eu + 1/2 is within
+// GAMMA * alpha of an integer the index is re-decided in fp64 with the
+// oracle's exact operations (gpair_oracle.c assa_index()).
+struct AssaPair {
+    int32_t k;   // aligned index on the upsampled grid (may be outside [0, alpha N_t))
+    float w;     // A / r
+};
+
+__device__ __forceinline__ int64_t assa_exact_k(double r, const OpConst& k) {
+    double q = __ddiv_rn(r, k.v);
+    q = __dsub_rn(q, k.t0);
+    q = __dmul_rn(q, k.fs_up);
+    q = __dadd_rn(q, 0.5);
+    return (int64_t)floor(q);
+}
+
+template <int SER>
+__device__ __forceinline__ AssaPair assa_setup(const Anchor& a, float4 kd, float A, const float* __restrict__ orig,
+                                               int64_t gi, int64_t Mpad, float sx, float sy, float sz,
+                                               const OpConst& k) {
+    AssaPair p;
+    float eu, w;
+    int na;
+    if (a.na != NA_EXACT) {
+        const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+        const float eps = q * a.invR2;
+        float S, Tw;
+        if (SER <= 2) {
+            S = fmaf(eps, fmaf(eps, 1.f / 8.f, -0.25f), 1.f);
+            Tw = fmaf(eps, fmaf(eps, 3.f / 8.f, -0.5f), 1.f);
+        } else {
+            S = fmaf(eps, -21.f / 512.f, 7.f / 128.f);
+            S = fmaf(eps, S, -5.f / 64.f);
+            S = fmaf(eps, S, 1.f / 8.f);
+            S = fmaf(eps, S, -0.25f);
+            S = fmaf(eps, S, 1.f);
+            Tw = fmaf(eps, 35.f / 128.f, -5.f / 16.f);
+            Tw = fmaf(eps, Tw, 3.f / 8.f);
+            Tw = fmaf(eps, Tw, -0.5f);
+            Tw = fmaf(eps, Tw, 1.f);
+        }
+        eu = fmaf(q * a.inv2Rh, S, a.Eu);
+        w = A * (a.h2R * Tw);
+        na = a.na;
+    } else {
+        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, w, na);
+    }
+    p.w = w * k.two_over_h;
+    const float xa = fmaf((float)k.alpha, eu, 0.5f);
+    const float t = (xa - 0.5f) + RND_MAGIC;  // rint(xa - 1/2) = floor(xa) unless ambiguous
+    const float fl = t - RND_MAGIC;
+    const bool amb = fabsf((xa - fl) - 0.5f) > 0.5f - GAMMA * (float)k.alpha;
+    if (amb) {
+        const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
+        p.k = (int32_t)assa_exact_k(r, k);
+    } else {
+        p.k = k.alpha * na + (__float_as_int(t) - RND_MAGIC_BITS);
+    }
     return p;
 }
 

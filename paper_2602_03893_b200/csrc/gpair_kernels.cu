@@ -377,25 +377,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     }
     const int32_t ic = perm[gi];
     if (ic < 0) return;
-    const float g = acc * ep.scale;
-    if (MODE == EPI_GRAD) {
-        ep.g_out[ic] = g;
-    } else if (MODE == EPI_NPC_ADAM) {
-        float z = ep.z[ic];
-        const float gz = g * (2.f * (z + ep.eps_npc));              // Eq. 19
-        const float mm = ep.beta1 * ep.m[ic] + (1.f - ep.beta1) * gz;
-        const float vv = ep.beta2 * ep.v[ic] + (1.f - ep.beta2) * gz * gz;
-        const float mh = mm * ep.bc1, vh = vv * ep.bc2;
-        z = z - ep.lr * mh / (sqrtf(vh) + ep.adam_eps);
-        ep.z[ic] = z;
-        ep.m[ic] = mm;
-        ep.v[ic] = vv;
-        if (ep.x_out) ep.x_out[ic] = (z + ep.eps_npc) * (z + ep.eps_npc);
-    } else {  // clamp
-        float x = fmaxf(ep.z[ic] - ep.lr * g, 0.f);
-        ep.z[ic] = x;
-        if (ep.x_out) ep.x_out[ic] = x;
-    }
+    adjoint_epilogue<MODE>(acc, ic, ep);
 }
 
 }  // namespace

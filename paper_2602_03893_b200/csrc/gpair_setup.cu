@@ -130,8 +130,8 @@ __device__ __forceinline__ bool cell_window(float4 C, float sx, float sy, float 
     double dx = (double)C.x - sx, dy = (double)C.y - sy, dz = (double)C.z - sz;
     R = sqrt(dx * dx + dy * dy + dz * dz);
     double rad = C.w;
-    double a = floor(((R - rad - k.ks) / k.v - k.t0) * k.fs) - 1.0;
-    double b = ceil(((R + rad + k.ks) / k.v - k.t0) * k.fs) + 1.0;
+    double a = floor(((R - rad - k.win_half) / k.v - k.t0) * k.fs) - 1.0;
+    double b = ceil(((R + rad + k.win_half) / k.v - k.t0) * k.fs) + 1.0;
     a = fmax(a, 0.0);
     b = fmin(b, (double)(k.Nt - 1));
     if (a > b) return false;
@@ -329,7 +329,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     // ---- forward regions: sized for >= ~4 CTAs per SM of work and smem fit
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->f_warps = std::min(8, (Nd + 31) / 32);
+    c->f_warps = std::min(c->assa ? 4 : 8, (Nd + 31) / 32);
     c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
     int cpr = 16;  // 512 kernels (8x8x8 on a grid): bounds fp32 accumulation chains
     while (cpr > 1 && (int64_t)((c->ncells + cpr - 1) / cpr) * c->f_sgroups < 4LL * dev_sms) cpr /= 2;
@@ -361,7 +361,8 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->ser = c->series_small ? ((c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int) ? 0 : 2) : 5;
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 15) / 16 * 16;  // the flush transposes 32-row blocks plus a 16-row tail
-        size_t smem = (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
+        size_t smem = c->assa ? assa_forward_smem(c, Lf)
+                              : (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
         if (smem > smem_limit && cpr > 1) {
             cudaFree(wlo);
             cpr /= 2;

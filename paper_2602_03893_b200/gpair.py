@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(_HERE, "libgpair.so")
 
 OK, ERR_INVALID_ARGUMENT, ERR_GEOMETRY, ERR_RESOURCE, ERR_NUMERICAL, ERR_CUDA, ERR_NCCL = range(7)
 CHECK_FINITE = 1 << 9
+TOF_ASSA = 1
 PROF_NAMES = ["gather", "forward", "reduce", "allreduce", "residual", "adjoint", "loss"]
 
 
@@ -41,6 +42,7 @@ class Desc(ctypes.Structure):
         ("world", ctypes.c_int32),
         ("nccl_comm", ctypes.c_void_p),
         ("flags", ctypes.c_int32),
+        ("assa_nmin", ctypes.c_int32),
     ]
 
 
@@ -77,6 +79,10 @@ class Info(ctypes.Structure):
         ("grid_detected", ctypes.c_int32),
         ("max_eps", ctypes.c_double),
         ("workspace_bytes", ctypes.c_int64),
+        ("assa", ctypes.c_int32),
+        ("assa_alpha", ctypes.c_int32),
+        ("assa_n_half", ctypes.c_int32),
+        ("assa_K", ctypes.c_int32),
     ]
 
     def as_dict(self):
@@ -182,7 +188,7 @@ class Context:
     """One gpair_ctx (one rank / device).  Mirrors include/gpair.h."""
 
     def __init__(self, centers, sensors, *, sigma, v, fs, n_samples, t0=0.0, k=3.0, rank=0, world=1,
-                 nccl_comm=None, flags=0, stream=None):
+                 nccl_comm=None, flags=0, assa=False, assa_nmin=25, stream=None):
         self.M = int(centers.shape[1])
         self.Nd = int(sensors.shape[1])
         self.Nt = int(n_samples)
@@ -190,7 +196,7 @@ class Context:
                  n_kernels=self.M, centers=_ptr(centers, numel=3 * self.M, name="centers"), sigma=float(sigma),
                  sigmas=None, window_k=float(k), n_sensors=self.Nd,
                  sensors=_ptr(sensors, numel=3 * self.Nd, name="sensors"), rank=int(rank), world=int(world),
-                 nccl_comm=nccl_comm, flags=int(flags))
+                 nccl_comm=nccl_comm, flags=int(flags) | (TOF_ASSA if assa else 0), assa_nmin=int(assa_nmin))
         h = ctypes.c_void_p()
         st = lib().gpair_create(ctypes.byref(h), ctypes.byref(d), _stream(stream))
         _check(st, None)
