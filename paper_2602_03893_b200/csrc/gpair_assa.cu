@@ -32,11 +32,18 @@ constexpr int A_STAGE = 8;     // cells staged per step
 constexpr int A_WARPS = 4;     // sensor warps per forward CTA
 constexpr int MAX_TAPS = 1024; // 2K+1 limit of the shared-memory taps table
 
-// The convolution writes its outputs in place (rows [0, Lf)) when every later
-// output chunk only reads rows past the ones already overwritten:
-// alpha (32 c + 32) - K >= 32 c + 32 for all c >= 0  <=>  K <= 32 (alpha - 1).
-__host__ __device__ inline bool conv_inplace(int alpha, int K) { return alpha >= 2 && K <= 32 * (alpha - 1); }
-int zrows_of(int alpha, int K, int Lf) { return conv_inplace(alpha, K) ? alpha * Lf : (alpha + 1) * Lf; }
+// Histogram column layout (per lane): ZG zero guard rows, the alpha*Lf rows of
+// z, ZG zero guard rows (so the convolution needs no bounds checks), and, when
+// the convolution cannot run in place, Lf output rows.  In place: output chunk
+// c (CONV_CHUNK rows) is written over z rows [c C, c C + C) after it is
+// computed; later chunks only read z rows >= alpha (c+1) C - K, which is past
+// them iff K <= C (alpha - 1).
+constexpr int CONV_CHUNK = 16;
+__host__ __device__ inline int zguard(int K) { return K > 16 ? K : 16; }
+__host__ __device__ inline bool conv_inplace(int alpha, int K) { return alpha >= 2 && K <= CONV_CHUNK * (alpha - 1); }
+int zrows_of(int alpha, int K, int Lf) {
+    return alpha * Lf + 2 * zguard(K) + (conv_inplace(alpha, K) ? 0 : Lf);
+}
 
 template <int SER>
 __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
@@ -69,6 +76,8 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
         sz = sens[2 * k.Nd + j];
     }
     float* zc = s_z + lane;
+    const int ZG = zguard(k.K);
+    float* zs = zc + ZG * 32;  // z row p of this lane's column at zs[p * 32]
     // ---- 1. projection P_up (Eq. 9): one shared-memory RMW per pair
     const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
     for (int cb = c0; cb < c1; cb += A_STAGE) {
@@ -82,12 +91,15 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
         __syncthreads();
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            const bool fast = SER <= 2 && !__any_sync(__activemask(), a.na == NA_EXACT);
+            const float4* kdg = s_kd + gq * GROUP;
+            const float* ampg = s_amp + gq * GROUP;
+            const int64_t gi0 = (int64_t)cb * CELL + gq * GROUP;
 #pragma unroll 2
             for (int t = 0; t < GROUP; ++t) {
-                const int li = gq * GROUP + t;
-                const AssaPair p =
-                    assa_setup<SER>(a, s_kd[li], s_amp[li], orig, (int64_t)cb * CELL + li, Mpad, sx, sy, sz, k);
-                if (p.k >= 0 && p.k < kmax) zc[(p.k - klo) * 32] += p.w;
+                const AssaPair p = fast ? assa_fast(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k)
+                                        : assa_setup<SER>(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k);
+                if ((unsigned)p.k < (unsigned)kmax) zs[(p.k - klo) * 32] += p.w;  // impulse exists (Eq. 9)
             }
         }
     }
@@ -96,25 +108,40 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     // per lane on its own column, in chunks of 32 outputs (conv_inplace():
     // later chunks never read rows already overwritten; otherwise the outputs
     // go to rows [alpha Lf, (alpha+1) Lf)).
+    // The taps are odd (h[-q] = -h[q], h[0] = 0):
+    //   y[n] = sum_{q=1..K} h[q] (z[alpha n - q] - z[alpha n + q]).
     const int zlim = k.alpha * Lf;
-    const int yoff = conv_inplace(k.alpha, k.K) ? 0 : zlim;
-    for (int cc = 0; cc < Lf; cc += 32) {
-        float yv[32];
+    const bool inplace = conv_inplace(k.alpha, k.K);
+    float* ys = inplace ? zs : zs + (zlim + ZG) * 32;
+    if (k.K <= 16) {
+        float hq[16];
 #pragma unroll
-        for (int t = 0; t < 32; ++t) {
-            const int pc = k.alpha * (cc + t);
-            float acc = 0.f;
-            const int qlo = max(-k.K, pc - zlim + 1), qhi = min(k.K, pc);
-            for (int q = qlo; q <= qhi; ++q) acc = fmaf(zc[(pc - q) * 32], s_taps[q + k.K], acc);
-            yv[t] = acc;
+        for (int q = 0; q < 16; ++q) hq[q] = (q + 1 <= k.K) ? s_taps[k.K + q + 1] : 0.f;
+        for (int cc = 0; cc < Lf; cc += CONV_CHUNK) {
+            float yv[CONV_CHUNK];
+#pragma unroll
+            for (int t = 0; t < CONV_CHUNK; ++t) {
+                const float* zp = zs + k.alpha * (cc + t) * 32;
+                float acc = 0.f;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc = fmaf(hq[q], zp[-(q + 1) * 32] - zp[(q + 1) * 32], acc);
+                yv[t] = acc;
+            }
+#pragma unroll
+            for (int t = 0; t < CONV_CHUNK; ++t)
+                if (cc + t < Lf) ys[(cc + t) * 32] = yv[t];
         }
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-            if (cc + t < Lf) zc[(yoff + cc + t) * 32] = yv[t];
+    } else {  // long kernels (N_half >= 17 with alpha = 1): guards of K rows, separate output rows
+        for (int n = 0; n < Lf; ++n) {
+            const float* zp = zs + k.alpha * n * 32;
+            float acc = 0.f;
+            for (int q = 1; q <= k.K; ++q) acc = fmaf(s_taps[k.K + q], zp[-q * 32] - zp[q * 32], acc);
+            ys[n * 32] = acc;
+        }
     }
     __syncwarp();
     // ---- 3. flush the region trace (same layout and transpose as k_forward)
-    float* s_acc = s_z + (size_t)yoff * 32;
+    float* s_acc = ys - lane;
     const size_t jstride = (size_t)gridDim.x * Lf;
     float* dst = partial + (size_t)jbase * jstride + (size_t)region * Lf;
     for (int m0 = 0; m0 < Lf; m0 += 32) {
@@ -161,7 +188,8 @@ __global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__
     extern __shared__ float4 smem4[];
     Anchor* s_anc = (Anchor*)smem4;                          // [nw][GPC][33]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t* s_wlo = (int32_t*)(s_anc + nw * GPC * 33);     // [32]
+    float4* s_sen = (float4*)(s_anc + nw * GPC * 33);       // [32] batch sensor positions
+    int32_t* s_wlo = (int32_t*)(s_sen + 32);                 // [32]
     float* s_dc = (float*)(s_wlo + 32);                      // [32][Lz]
 
     const int cid = blockIdx.x * cpr + warp;
@@ -179,6 +207,10 @@ __global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__
         __syncthreads();
         if (threadIdx.x < 32)
             s_wlo[threadIdx.x] = threadIdx.x < nj ? wlo[(int64_t)blockIdx.x * k.Nd + jb + threadIdx.x] : -1;
+        if (threadIdx.x < nj) {
+            const int js = jb + threadIdx.x;
+            s_sen[threadIdx.x] = make_float4(sens[js], sens[k.Nd + js], sens[2 * k.Nd + js], 0.f);
+        }
         if (cok && lane < nj) {
             const int j = jb + lane;
             const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
@@ -205,15 +237,18 @@ __global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__
         for (int jj = 0; jj < nj; ++jj) {
             const int lo = s_wlo[jj];
             if (lo < 0) continue;
-            const int j = jb + jj;
-            const AssaPair p = assa_setup<SER>(my_anc[jj], d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j],
-                                               sens[2 * k.Nd + j], k);
-            if (p.k < 0 || p.k >= Nup) continue;
+            const float4 sp = s_sen[jj];
+            const Anchor a = my_anc[jj];
+            const AssaPair p = (SER <= 2 && a.na != NA_EXACT)
+                                   ? assa_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k)
+                                   : assa_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+            const bool in = (unsigned)p.k < (unsigned)Nup;  // the impulse exists (Eq. 9)
             if (MODE == MODE_COUNT) {
-                nimp += real ? 1ull : 0ull;
+                nimp += (real && in) ? 1ull : 0ull;
                 continue;
             }
-            accb = fmaf(p.w, s_dc[jj * Lz + (p.k - k.alpha * lo)], accb);  // Eq. 17
+            const int row = min(max(p.k - k.alpha * lo, 0), Lz - 1);
+            accb = fmaf(in ? p.w : 0.f, s_dc[jj * Lz + row], accb);  // Eq. 17
         }
         acc += accb;
     }
@@ -243,7 +278,7 @@ cudaError_t assa_fwd_launch(gpair_ctx* c, cudaStream_t st) {
 template <int SER, int MODE>
 cudaError_t assa_adj_launch(gpair_ctx* c, const EpiParams& ep, cudaStream_t st) {
     const int Lz = c->k.alpha * c->La + 2 * c->k.alpha;
-    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 + (MODE == MODE_COUNT ? 0 : (size_t)32 * Lz * 4);
+    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 + 32 * 16 + (MODE == MODE_COUNT ? 0 : (size_t)32 * Lz * 4);
     cudaError_t e =
         cudaFuncSetAttribute(k_assa_adjoint<SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

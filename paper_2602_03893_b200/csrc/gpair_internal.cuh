@@ -334,6 +334,32 @@ __device__ __forceinline__ AssaPair assa_setup(const Anchor& a, float4 kd, float
     return p;
 }
 
+// Rare path of assa_fast(): exact fp64 re-decision of k_ij.
+static __device__ __noinline__ int assa_fix(const float* __restrict__ orig, int64_t gi, int64_t Mpad, float sx,
+                                            float sy, float sz, const OpConst k) {
+    const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
+    return (int)assa_exact_k(r, k);
+}
+
+// Fast ASSA setup (degree-2 series, non-exact anchor): one rare branch.
+__device__ __forceinline__ AssaPair assa_fast(const Anchor& a, float4 kd, float A, const float* __restrict__ orig,
+                                              int64_t gi, int64_t Mpad, float sx, float sy, float sz,
+                                              const OpConst& k) {
+    AssaPair p;
+    const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+    const float eps = q * a.invR2;
+    const float S = fmaf(eps, fmaf(eps, 1.f / 8.f, -0.25f), 1.f);
+    const float Tw = fmaf(eps, fmaf(eps, 3.f / 8.f, -0.5f), 1.f);
+    const float eu = fmaf(q * a.inv2Rh, S, a.Eu);
+    p.w = (A * (a.h2R * Tw)) * k.two_over_h;
+    const float xa = fmaf((float)k.alpha, eu, 0.5f);
+    const float t = (xa - 0.5f) + RND_MAGIC;
+    const float fl = t - RND_MAGIC;
+    p.k = k.alpha * a.na + (__float_as_int(t) - RND_MAGIC_BITS);
+    if (fabsf((xa - fl) - 0.5f) > 0.5f - GAMMA * (float)k.alpha) p.k = assa_fix(orig, gi, Mpad, sx, sy, sz, k);
+    return p;
+}
+
 // ---- packed fp32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2)
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t pk2(float lo, float hi) {

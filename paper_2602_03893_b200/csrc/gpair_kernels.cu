@@ -282,7 +282,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     extern __shared__ float4 smem4[];
     Anchor* s_anc = (Anchor*)smem4;                          // [nw][GPC][33]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t* s_wlo = (int32_t*)(s_anc + nw * GPC * 33);     // [32]
+    float4* s_sen = (float4*)(s_anc + nw * GPC * 33);       // [32] batch sensor positions
+    int32_t* s_wlo = (int32_t*)(s_sen + 32);                 // [32]
     float* s_res = (float*)(s_wlo + 32);                     // [32][La]
 
     const int cid = blockIdx.x * cpr + warp;
@@ -298,6 +299,10 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
         const int nj = min(32, k.Nd - jb);
         __syncthreads();
         if (threadIdx.x < 32) s_wlo[threadIdx.x] = threadIdx.x < nj ? wlo[(int64_t)blockIdx.x * k.Nd + jb + threadIdx.x] : -1;
+        if (threadIdx.x < nj) {
+            const int js = jb + threadIdx.x;
+            s_sen[threadIdx.x] = make_float4(sens[js], sens[k.Nd + js], sens[2 * k.Nd + js], 0.f);
+        }
         if (cok && lane < nj) {
             const int j = jb + lane;
             const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
@@ -324,14 +329,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
         for (int jj = 0; jj < nj; ++jj) {
             const int lo = s_wlo[jj];
             if (lo < 0) continue;
-            const int j = jb + jj;
+            const float4 sp = s_sen[jj];
             const Anchor a = my_anc[jj];
             PairWin p;
             if (SER == 0 && a.na != NA_EXACT)
-                p = pair_fast(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j], sens[2 * k.Nd + j], k);
+                p = pair_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             else
-                p = pair_setup<SER == 0 ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sens[j], sens[k.Nd + j],
-                                                   sens[2 * k.Nd + j], k);
+                p = pair_setup<SER == 0 ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             if (p.cnt <= 0) continue;
             if (MODE == MODE_COUNT) {
                 npairs += real ? (unsigned long long)p.cnt : 0ull;
@@ -403,7 +407,7 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
 
 template <int W, int SER, int MODE>
 cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
-    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 +
+    size_t smem = (size_t)c->a_cpr * GPC * 33 * sizeof(Anchor) + 32 * 4 + 32 * 16 +
                   (MODE == MODE_COUNT ? 0 : (size_t)32 * c->La * 4);
     cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

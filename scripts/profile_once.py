@@ -7,10 +7,11 @@ import torch
 from paper_2602_03893_b200 import gpair, inputs
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+assa = len(sys.argv) > 2 and sys.argv[2] == "assa"
 cfg = inputs.CONFIGS[name]
 dev = torch.device("cuda:0")
 ctx = gpair.Context(torch.from_numpy(cfg.centers()).to(dev), torch.from_numpy(cfg.sensors()).to(dev),
-                    sigma=cfg.sig, v=cfg.v, fs=cfg.fs, n_samples=cfg.n_samples, t0=cfg.t0, k=cfg.k)
+                    sigma=cfg.sig, v=cfg.v, fs=cfg.fs, n_samples=cfg.n_samples, t0=cfg.t0, k=cfg.k, assa=assa)
 x = torch.from_numpy(inputs.dense_amplitudes(cfg.M)).to(dev)
 d = torch.from_numpy(inputs.residual(cfg.n_sensors, cfg.n_samples)).to(dev)
 y = ctx.forward(x)
