@@ -29,7 +29,10 @@ namespace gpair {
 namespace {
 
 constexpr int A_STAGE = 8;     // cells staged per step
-constexpr int A_WARPS = 4;     // sensor warps per forward CTA
+#ifndef GPAIR_ASSA_WARPS
+#define GPAIR_ASSA_WARPS 4
+#endif
+constexpr int A_WARPS = GPAIR_ASSA_WARPS;  // sensor warps per forward CTA
 constexpr int MAX_TAPS = 1024; // 2K+1 limit of the shared-memory taps table
 
 // Histogram column layout (per lane): ZG zero guard rows, the alpha*Lf rows of
@@ -95,11 +98,27 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
             const float4* kdg = s_kd + gq * GROUP;
             const float* ampg = s_amp + gq * GROUP;
             const int64_t gi0 = (int64_t)cb * CELL + gq * GROUP;
-#pragma unroll 2
-            for (int t = 0; t < GROUP; ++t) {
-                const AssaPair p = fast ? assa_fast(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k)
-                                        : assa_setup<SER>(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k);
-                if ((unsigned)p.k < (unsigned)kmax) zs[(p.k - klo) * 32] += p.w;  // impulse exists (Eq. 9)
+            if (fast) {
+                // 4 independent setups, one rare branch, then the RMWs (ILP)
+#pragma unroll
+                for (int t0 = 0; t0 < GROUP; t0 += 4) {
+                    AssaPre q[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) q[u] = assa_pre(a, kdg[t0 + u], ampg[t0 + u], k);
+                    if (q[0].amb | q[1].amb | q[2].amb | q[3].amb) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (q[u].amb) q[u].k = assa_fix(orig, gi0 + t0 + u, Mpad, sx, sy, sz, k);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if ((unsigned)q[u].k < (unsigned)kmax) zs[(q[u].k - klo) * 32] += q[u].w;  // Eq. 9
+                }
+            } else {
+                for (int t = 0; t < GROUP; ++t) {
+                    const AssaPair p = assa_setup<SER>(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k);
+                    if ((unsigned)p.k < (unsigned)kmax) zs[(p.k - klo) * 32] += p.w;  // impulse exists (Eq. 9)
+                }
             }
         }
     }
@@ -124,7 +143,10 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
                 const float* zp = zs + k.alpha * (cc + t) * 32;
                 float acc = 0.f;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) acc = fmaf(hq[q], zp[-(q + 1) * 32] - zp[(q + 1) * 32], acc);
+                for (int q = 0; q < 16; ++q) {
+                    acc = fmaf(hq[q], zp[-(q + 1) * 32], acc);
+                    acc = fmaf(-hq[q], zp[(q + 1) * 32], acc);
+                }
                 yv[t] = acc;
             }
 #pragma unroll
@@ -135,7 +157,10 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
         for (int n = 0; n < Lf; ++n) {
             const float* zp = zs + k.alpha * n * 32;
             float acc = 0.f;
-            for (int q = 1; q <= k.K; ++q) acc = fmaf(s_taps[k.K + q], zp[-q * 32] - zp[q * 32], acc);
+            for (int q = 1; q <= k.K; ++q) {
+                acc = fmaf(s_taps[k.K + q], zp[-q * 32], acc);
+                acc = fmaf(-s_taps[k.K + q], zp[q * 32], acc);
+            }
             ys[n * 32] = acc;
         }
     }
@@ -234,21 +259,44 @@ __global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__
         }
         if (!cok) continue;
         float accb = 0.f;
-        for (int jj = 0; jj < nj; ++jj) {
-            const int lo = s_wlo[jj];
-            if (lo < 0) continue;
-            const float4 sp = s_sen[jj];
-            const Anchor a = my_anc[jj];
-            const AssaPair p = (SER <= 2 && a.na != NA_EXACT)
-                                   ? assa_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k)
-                                   : assa_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
-            const bool in = (unsigned)p.k < (unsigned)Nup;  // the impulse exists (Eq. 9)
-            if (MODE == MODE_COUNT) {
-                nimp += (real && in) ? 1ull : 0ull;
-                continue;
+        // 4 sensors at a time: independent setups, one rare branch, 4 gathers (ILP)
+        for (int jj0 = 0; jj0 < nj; jj0 += 4) {
+            AssaPre q[4];
+            int lo4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int jj = min(jj0 + u, nj - 1);
+                lo4[u] = (jj0 + u < nj) ? s_wlo[jj] : -1;
+                const Anchor a = my_anc[jj];
+                if (SER <= 2 && a.na != NA_EXACT) {
+                    q[u] = assa_pre(a, d4, 1.f, k);
+                } else {
+                    const float4 sp = s_sen[jj];
+                    const AssaPair p = assa_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+                    q[u].k = p.k;
+                    q[u].w = p.w;
+                    q[u].amb = false;
+                }
             }
-            const int row = min(max(p.k - k.alpha * lo, 0), Lz - 1);
-            accb = fmaf(in ? p.w : 0.f, s_dc[jj * Lz + row], accb);  // Eq. 17
+            if (q[0].amb | q[1].amb | q[2].amb | q[3].amb) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q[u].amb) {
+                        const float4 sp = s_sen[min(jj0 + u, nj - 1)];
+                        q[u].k = assa_fix(orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = lo4[u] >= 0 && (unsigned)q[u].k < (unsigned)Nup;  // the impulse exists (Eq. 9)
+                if (MODE == MODE_COUNT) {
+                    nimp += (real && in) ? 1ull : 0ull;
+                } else {
+                    const int jj = min(jj0 + u, nj - 1);
+                    const int row = min(max(q[u].k - k.alpha * lo4[u], 0), Lz - 1);
+                    accb = fmaf(in ? q[u].w : 0.f, s_dc[jj * Lz + row], accb);  // Eq. 17
+                }
+            }
         }
         acc += accb;
     }
@@ -325,4 +373,8 @@ cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st) {
     return assa_adj_dispatch<MODE_COUNT>(c, ep, st);
 }
 
+}  // namespace gpair
+
+namespace gpair {
+int assa_forward_warps() { return A_WARPS; }
 }  // namespace gpair

@@ -124,6 +124,7 @@ int pick_wmax(int w);
 
 // ASSA operator (gpair_assa.cu)
 size_t assa_forward_smem(const gpair_ctx* c, int Lf);
+int assa_forward_warps();
 cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st);

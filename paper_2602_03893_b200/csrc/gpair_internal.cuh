@@ -341,6 +341,30 @@ static __device__ __noinline__ int assa_fix(const float* __restrict__ orig, int6
     return (int)assa_exact_k(r, k);
 }
 
+// Branch-free part of assa_fast(): k guess, weight and the ambiguity flag, so
+// that several pairs can be set up back to back (instruction-level parallelism)
+// before one shared rare-path branch.
+struct AssaPre {
+    int32_t k;
+    float w;
+    bool amb;
+};
+__device__ __forceinline__ AssaPre assa_pre(const Anchor& a, float4 kd, float A, const OpConst& k) {
+    AssaPre p;
+    const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+    const float eps = q * a.invR2;
+    const float S = fmaf(eps, fmaf(eps, 1.f / 8.f, -0.25f), 1.f);
+    const float Tw = fmaf(eps, fmaf(eps, 3.f / 8.f, -0.5f), 1.f);
+    const float eu = fmaf(q * a.inv2Rh, S, a.Eu);
+    p.w = (A * (a.h2R * Tw)) * k.two_over_h;
+    const float xa = fmaf((float)k.alpha, eu, 0.5f);
+    const float t = (xa - 0.5f) + RND_MAGIC;
+    const float fl = t - RND_MAGIC;
+    p.k = k.alpha * a.na + (__float_as_int(t) - RND_MAGIC_BITS);
+    p.amb = fabsf((xa - fl) - 0.5f) > 0.5f - GAMMA * (float)k.alpha;
+    return p;
+}
+
 // Fast ASSA setup (degree-2 series, non-exact anchor): one rare branch.
 __device__ __forceinline__ AssaPair assa_fast(const Anchor& a, float4 kd, float A, const float* __restrict__ orig,
                                               int64_t gi, int64_t Mpad, float sx, float sy, float sz,

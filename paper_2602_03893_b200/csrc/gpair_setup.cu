@@ -329,7 +329,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     // ---- forward regions: sized for >= ~4 CTAs per SM of work and smem fit
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->f_warps = std::min(c->assa ? 4 : 8, (Nd + 31) / 32);
+    c->f_warps = std::min(c->assa ? assa_forward_warps() : 8, (Nd + 31) / 32);
     c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
     int cpr = 16;  // 512 kernels (8x8x8 on a grid): bounds fp32 accumulation chains
     while (cpr > 1 && (int64_t)((c->ncells + cpr - 1) / cpr) * c->f_sgroups < 4LL * dev_sms) cpr /= 2;
