@@ -132,22 +132,21 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     const int zlim = k.alpha * Lf;
     const bool inplace = conv_inplace(k.alpha, k.K);
     float* ys = inplace ? zs : zs + (zlim + ZG) * 32;
+    // fp64 accumulation of the 2K products: the taps alternate in sign around
+    // each arrival, so the output is a cancelling sum.
     if (k.K <= 16) {
-        float hq[16];
+        double hq[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) hq[q] = (q + 1 <= k.K) ? s_taps[k.K + q + 1] : 0.f;
+        for (int q = 0; q < 16; ++q) hq[q] = (q + 1 <= k.K) ? (double)s_taps[k.K + q + 1] : 0.0;
         for (int cc = 0; cc < Lf; cc += CONV_CHUNK) {
             float yv[CONV_CHUNK];
 #pragma unroll
             for (int t = 0; t < CONV_CHUNK; ++t) {
                 const float* zp = zs + k.alpha * (cc + t) * 32;
-                float acc = 0.f;
+                double acc = 0.0;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    acc = fmaf(hq[q], zp[-(q + 1) * 32], acc);
-                    acc = fmaf(-hq[q], zp[(q + 1) * 32], acc);
-                }
-                yv[t] = acc;
+                for (int q = 0; q < 16; ++q) acc = fma(hq[q], (double)zp[-(q + 1) * 32] - (double)zp[(q + 1) * 32], acc);
+                yv[t] = (float)acc;
             }
 #pragma unroll
             for (int t = 0; t < CONV_CHUNK; ++t)
@@ -156,12 +155,9 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     } else {  // long kernels (N_half >= 17 with alpha = 1): guards of K rows, separate output rows
         for (int n = 0; n < Lf; ++n) {
             const float* zp = zs + k.alpha * n * 32;
-            float acc = 0.f;
-            for (int q = 1; q <= k.K; ++q) {
-                acc = fmaf(s_taps[k.K + q], zp[-q * 32], acc);
-                acc = fmaf(-s_taps[k.K + q], zp[q * 32], acc);
-            }
-            ys[n * 32] = acc;
+            double acc = 0.0;
+            for (int q = 1; q <= k.K; ++q) acc = fma((double)s_taps[k.K + q], (double)zp[-q * 32] - (double)zp[q * 32], acc);
+            ys[n * 32] = (float)acc;
         }
     }
     __syncwarp();
@@ -259,44 +255,21 @@ __global__ void __launch_bounds__(256) k_assa_adjoint(const float4* __restrict__
         }
         if (!cok) continue;
         float accb = 0.f;
-        // 4 sensors at a time: independent setups, one rare branch, 4 gathers (ILP)
-        for (int jj0 = 0; jj0 < nj; jj0 += 4) {
-            AssaPre q[4];
-            int lo4[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int jj = min(jj0 + u, nj - 1);
-                lo4[u] = (jj0 + u < nj) ? s_wlo[jj] : -1;
-                const Anchor a = my_anc[jj];
-                if (SER <= 2 && a.na != NA_EXACT) {
-                    q[u] = assa_pre(a, d4, 1.f, k);
-                } else {
-                    const float4 sp = s_sen[jj];
-                    const AssaPair p = assa_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
-                    q[u].k = p.k;
-                    q[u].w = p.w;
-                    q[u].amb = false;
-                }
+        for (int jj = 0; jj < nj; ++jj) {
+            const int lo = s_wlo[jj];
+            if (lo < 0) continue;
+            const float4 sp = s_sen[jj];
+            const Anchor a = my_anc[jj];
+            const AssaPair p = (SER <= 2 && a.na != NA_EXACT)
+                                   ? assa_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k)
+                                   : assa_setup<SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+            const bool in = (unsigned)p.k < (unsigned)Nup;  // the impulse exists (Eq. 9)
+            if (MODE == MODE_COUNT) {
+                nimp += (real && in) ? 1ull : 0ull;
+                continue;
             }
-            if (q[0].amb | q[1].amb | q[2].amb | q[3].amb) {
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (q[u].amb) {
-                        const float4 sp = s_sen[min(jj0 + u, nj - 1)];
-                        q[u].k = assa_fix(orig, gi, Mpad, sp.x, sp.y, sp.z, k);
-                    }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const bool in = lo4[u] >= 0 && (unsigned)q[u].k < (unsigned)Nup;  // the impulse exists (Eq. 9)
-                if (MODE == MODE_COUNT) {
-                    nimp += (real && in) ? 1ull : 0ull;
-                } else {
-                    const int jj = min(jj0 + u, nj - 1);
-                    const int row = min(max(q[u].k - k.alpha * lo4[u], 0), Lz - 1);
-                    accb = fmaf(in ? q[u].w : 0.f, s_dc[jj * Lz + row], accb);  // Eq. 17
-                }
-            }
+            const int row = min(max(p.k - k.alpha * lo, 0), Lz - 1);
+            accb = fmaf(in ? p.w : 0.f, s_dc[jj * Lz + row], accb);  // Eq. 17
         }
         acc += accb;
     }
