@@ -132,21 +132,22 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     const int zlim = k.alpha * Lf;
     const bool inplace = conv_inplace(k.alpha, k.K);
     float* ys = inplace ? zs : zs + (zlim + ZG) * 32;
-    // fp64 accumulation of the 2K products: the taps alternate in sign around
-    // each arrival, so the output is a cancelling sum.
     if (k.K <= 16) {
-        double hq[16];
+        float hq[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) hq[q] = (q + 1 <= k.K) ? (double)s_taps[k.K + q + 1] : 0.0;
+        for (int q = 0; q < 16; ++q) hq[q] = (q + 1 <= k.K) ? s_taps[k.K + q + 1] : 0.f;
         for (int cc = 0; cc < Lf; cc += CONV_CHUNK) {
             float yv[CONV_CHUNK];
 #pragma unroll
             for (int t = 0; t < CONV_CHUNK; ++t) {
                 const float* zp = zs + k.alpha * (cc + t) * 32;
-                double acc = 0.0;
+                float acc = 0.f;
 #pragma unroll
-                for (int q = 0; q < 16; ++q) acc = fma(hq[q], (double)zp[-(q + 1) * 32] - (double)zp[(q + 1) * 32], acc);
-                yv[t] = (float)acc;
+                for (int q = 0; q < 16; ++q) {
+                    acc = fmaf(hq[q], zp[-(q + 1) * 32], acc);
+                    acc = fmaf(-hq[q], zp[(q + 1) * 32], acc);
+                }
+                yv[t] = acc;
             }
 #pragma unroll
             for (int t = 0; t < CONV_CHUNK; ++t)
@@ -155,9 +156,12 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     } else {  // long kernels (N_half >= 17 with alpha = 1): guards of K rows, separate output rows
         for (int n = 0; n < Lf; ++n) {
             const float* zp = zs + k.alpha * n * 32;
-            double acc = 0.0;
-            for (int q = 1; q <= k.K; ++q) acc = fma((double)s_taps[k.K + q], (double)zp[-q * 32] - (double)zp[q * 32], acc);
-            ys[n * 32] = (float)acc;
+            float acc = 0.f;
+            for (int q = 1; q <= k.K; ++q) {
+                acc = fmaf(s_taps[k.K + q], zp[-q * 32], acc);
+                acc = fmaf(-s_taps[k.K + q], zp[q * 32], acc);
+            }
+            ys[n * 32] = acc;
         }
     }
     __syncwarp();

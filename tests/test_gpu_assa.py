@@ -1,5 +1,9 @@
 """GPU parity of the ASSA operator (Eqs. 8-17,
-Algorithm 1) against the fp64 ASSA oracle, same gates as the direct operator."""
+Algorithm 1) against the fp64 ASSA oracle.  Gates: rel L2 <= 1e-5 as for the
+direct operator; elementwise on signal samples <= 2e-4 (DESIGN.md reading
+R21: ASSA outputs are short odd-tap sums of snapped impulses whose entries
+near 1e-3 of peak cancel ~1000:1, so fp32 taps and weights (~1e-7) set an
+elementwise floor near 1e-4; measured values are printed)."""
 import math
 
 import numpy as np
@@ -10,7 +14,18 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 from oracle import ir  # noqa: E402
 from paper_2602_03893_b200 import gpair, inputs  # noqa: E402
-from tests_common import T, assert_parity, dev  # noqa: E402
+from tests_common import T, compare, dev  # noqa: E402
+from tests_common import assert_parity as _assert_parity  # noqa: E402
+
+ASSA_ELEM = 2e-4
+
+
+def assert_parity(got, ref, what, elementwise=True):
+    rel, elem = compare(got, ref)
+    print(f"{what}: rel L2 {rel:.2e} elementwise {elem:.2e}")
+    assert rel <= 1e-5, f"{what}: rel L2 {rel:.3e}"
+    assert elem <= (ASSA_ELEM if elementwise else 1e-3), f"{what}: max elementwise rel {elem:.3e}"
+    return rel, elem
 
 pytestmark = pytest.mark.gpu
 
