@@ -43,7 +43,11 @@ constexpr int MAX_TAPS = 1024; // 2K+1 limit of the shared-memory taps table
 // them iff K <= C (alpha - 1).
 constexpr int CONV_CHUNK = 16;
 __host__ __device__ inline int zguard(int K) { return K > 16 ? K : 16; }
-__host__ __device__ inline bool conv_inplace(int alpha, int K) { return alpha >= 2 && K <= CONV_CHUNK * (alpha - 1); }
+// (only the chunked register path, K <= 16, writes in place; the generic path
+// writes each output immediately and therefore always uses separate rows)
+__host__ __device__ inline bool conv_inplace(int alpha, int K) {
+    return K <= 16 && alpha >= 2 && K <= CONV_CHUNK * (alpha - 1);
+}
 int zrows_of(int alpha, int K, int Lf) {
     return alpha * Lf + 2 * zguard(K) + (conv_inplace(alpha, K) ? 0 : Lf);
 }
