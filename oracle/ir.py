@@ -5,8 +5,8 @@ paper in its own order and notation:
 
 * NPC (Eq. 18, P:445-447):   x = phi(z) = (z + eps)^2,  eps = 1e-8 (P:449)
 * chain rule (Eq. 19):  dL/dz = dL/dx * 2 (z + eps)
-* loss (Eq. 23):  L = (1/N) ||A(phi(z)) - b||^2, N = N_d N_t,
-  lambda = 0 on the hot path (VCR is out of the hot-path scope).
+* loss (Eq. 23, P:487-491):  L = (1/N) ||A(phi(z)) - b||^2 + lambda R_VCR(x),
+  N = N_d N_t; R_VCR (Eqs. 20-22, row f2) in oracle/vcr.py, lambda = 0 default.
 * gradient scale (reading R10): dL/dy = (2/N)(y - b); ``grad_scale`` exposed,
   1.0 reproduces Alg. 2 line 529 literally.
 * CAWR (Eq. 24), as printed by default (reading R13).
@@ -74,6 +74,10 @@ class Hyper:
     grad_scale: float | None = None  # None -> 2/N
     mode: str = "npc"  # "npc" (paper) | "clamp"
     printed_formula: bool = True
+    lam: float = 0.0  # lambda of Eq. 23 (VCR weight, row f2)
+    beta: float = 0.0  # beta of Eq. 20
+    eps_reg: float = 1e-8  # regulariser epsilon (reading V4)
+    dims: tuple | None = None  # voxel grid (nx, ny, nz) of the kernel order, needed when lam > 0
 
 
 @dataclass
@@ -112,6 +116,12 @@ def loss_and_grad(z, b, geom, hp: Hyper):
         gx = _assa_adjoint(geom["centers"], scale * r, geom["sensors"], **_adj_kw(geom["op"]), **assa)
     else:
         gx = _adjoint(geom["centers"], scale * r, geom["sensors"], **_adj_kw(geom["op"]))
+    if hp.lam > 0.0:  # Alg. 2: L += lambda R_VCR(x), grad_x += lambda grad R_VCR(x)
+        from .vcr import r_vcr
+
+        rv, gv = r_vcr(x, hp.dims, hp.beta, hp.eps_reg)
+        L += hp.lam * rv
+        gx = gx + hp.lam * gv
     gz = npc_chain(gx, z, hp.eps_npc) if hp.mode == "npc" else gx
     return L, gz, y
 
