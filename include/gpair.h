@@ -103,6 +103,14 @@ typedef struct {
     int32_t step;      /* 1-based Adam step count t >= 1 (bias correction)               */
     int32_t mode;      /* 0 = NPC x=(z+eps)^2 + Adam (paper);
                           1 = clamp: state z holds x, x <- max(x - lr g, 0) (R15)       */
+    /* Vessel continuity regularisation (Eqs. 20-23; row f2).
+     * lam = 0 disables it (the paper's lambda = 0 runs); lam > 0 needs
+     * world == 1 and grid[0] grid[1] grid[2] == M with the kernels in grid
+     * order i = ix + nx (iy + ny iz) (the order R_VCR's differences use). */
+    float lam;         /* lambda of Eq. 23 (>= 0)                                        */
+    float beta;        /* beta of Eq. 20: R_VCR = R_H + beta R_TV                        */
+    float eps_reg;     /* smoothing epsilon inside both square roots (V4), > 0           */
+    int32_t grid[3];   /* (n_x, n_y, n_z) voxel grid of the kernel order                 */
 } gpair_step;
 
 /* Accumulated device time of the library's own kernels (gpair_profile_*). */
@@ -114,7 +122,8 @@ enum {
     GPAIR_PROF_RESIDUAL = 4, /* residual + loss (world > 1 only)                    */
     GPAIR_PROF_ADJOINT = 5,  /* adjoint gather (+ fused update) (dominant)          */
     GPAIR_PROF_LOSS = 6,     /* loss finalisation                                   */
-    GPAIR_PROF_N = 7
+    GPAIR_PROF_VCR = 7,      /* VCR terms + gradient (lam > 0 only)                 */
+    GPAIR_PROF_N = 8
 };
 typedef struct {
     double ms[GPAIR_PROF_N];       /* summed CUDA-event durations [ms]                */
@@ -161,9 +170,26 @@ gpair_status gpair_forward(gpair_ctx* ctx, const float* amplitudes, float* signa
  * grad:     DEVICE [M_local] output g_i = sum_j sum_n a_ijn delta_j[n]. */
 gpair_status gpair_adjoint(gpair_ctx* ctx, const float* residual, float* grad, void* stream);
 
-/* One iteration of Algorithm 2, lambda = 0:
+/* Vessel continuity regulariser R_VCR = R_H + beta R_TV (Eqs. 20-22,
+ * P:457-481) with the difference operators of DESIGN.md readings V1-V3:
+ *   R_TV = sum_i sqrt(sum_d (D_d x_i)^2 + eps),   D_d forward difference, 0 on
+ *          the last index;
+ *   R_H  = sum_i sqrt(sum_d (D_dd x_i)^2 + 2 sum_{p<q} (D_pq x_i)^2 + eps),
+ *          D_dd = [1,-2,1] centred at clamp(i_d, 1, n_d - 2) (0 if n_d < 3),
+ *          D_pq forward-forward cross difference, 0 on the last index of p or q.
+ * grid:  HOST int32[3] (n_x, n_y, n_z) >= 1; M = n_x n_y n_z.
+ * x:     DEVICE [M] image, index i = ix + n_x (iy + n_y iz).
+ * grad:  DEVICE [M] output dR/dx, or NULL.
+ * value: DEVICE float scalar R_VCR(x) (fp64-accumulated), or NULL.
+ * Needs only a context for its workspace (any M; reallocated on change).
+ * Errors: INVALID_ARGUMENT (NULL x, bad grid, eps <= 0, non-finite beta), CUDA. */
+gpair_status gpair_vcr(gpair_ctx* ctx, const int32_t* grid, const float* x, float beta, float eps,
+                       float* grad, float* value, void* stream);
+
+/* One iteration of Algorithm 2:
  *   x = (z + eps)^2 (mode 0) or x = z (mode 1);  y = A x  [+ allreduce];
- *   L = (1/N) |y - b|^2;  g = A^T (grad_scale (y - b));
+ *   L = (1/N) |y - b|^2 + lam R_VCR(x);
+ *   g = A^T (grad_scale (y - b)) + lam grad R_VCR(x);
  *   mode 0: dz = g 2 (z + eps); Adam step on (z, m, v) with s->lr, s->step;
  *   mode 1: z = max(z - lr g, 0).
  * z, m, v:     DEVICE [M_local] in/out state (m, v unused in mode 1, may be NULL).

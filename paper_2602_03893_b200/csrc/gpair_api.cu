@@ -137,6 +137,9 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_flags);
     cudaFree(c->d_taps);
     cudaFree(c->d_dconv);
+    cudaFree(c->d_vcr_u);
+    cudaFree(c->d_vcr_part);
+    cudaFree(c->d_vcr_g);
     prof_drain(c);
     for (auto e : c->prof_free) cudaEventDestroy(e);
     delete c;
@@ -411,6 +414,31 @@ gpair_status gpair_adjoint(gpair_ctx* c, const float* residual, float* grad, voi
     return GPAIR_OK;
 }
 
+static gpair_status check_vcr_args(gpair_ctx* c, const int32_t* grid, float beta, float eps) {
+    if (!grid) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid is NULL");
+    for (int d = 0; d < 3; ++d)
+        if (grid[d] < 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid dimensions must be >= 1");
+    if ((int64_t)grid[0] * grid[1] * grid[2] > ((int64_t)1 << 31) / 9)
+        return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid too large");
+    if (!std::isfinite(beta)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "beta not finite");
+    if (!(eps > 0.f) || !std::isfinite(eps)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "eps_reg must be > 0");
+    return GPAIR_OK;
+}
+
+gpair_status gpair_vcr(gpair_ctx* c, const int32_t* grid, const float* x, float beta, float eps, float* grad,
+                       float* value, void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!x) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "x is NULL");
+    gpair_status gs = check_vcr_args(c, grid, beta, eps);
+    if (gs) return gs;
+    gs = sticky_check(c);
+    if (gs) return gs;
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope ps(c, GPAIR_PROF_VCR, st);
+    API_CUDA(c, gpair::launch_vcr(c, grid, x, 0, 0.f, beta, eps, grad, value, st), "vcr");
+    return GPAIR_OK;
+}
+
 gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const float* b, const gpair_step* s,
                            float* signals_out, float* x_out, float* loss_out, void* stream) {
     if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
@@ -421,15 +449,33 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     if (!std::isfinite(s->lr)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lr not finite");
     gpair_status st0 = sticky_check(c);
     if (st0) return st0;
+    const bool reg = s->lam != 0.f;
+    if (reg) {
+        if (!(s->lam > 0.f) || !std::isfinite(s->lam)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam must be >= 0");
+        if (c->world != 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam > 0 needs world == 1 (whole grid per rank)");
+        gpair_status gs = check_vcr_args(c, s->grid, s->beta, s->eps_reg);
+        if (gs) return gs;
+        if ((int64_t)s->grid[0] * s->grid[1] * s->grid[2] != c->M)
+            return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid[0] grid[1] grid[2] != n_kernels");
+    }
     cudaStream_t st = (cudaStream_t)stream;
     const int npc = s->mode == 0;
     float* y = signals_out ? signals_out : c->d_y;
+    if (reg) {  // R_VCR and its gradient at the pre-update x (Alg. 2)
+        ProfScope ps(c, GPAIR_PROF_VCR, st);
+        API_CUDA(c, gpair::vcr_ensure(c, c->M), "vcr workspace");
+        API_CUDA(c, gpair::launch_vcr(c, s->grid, z, npc, s->eps_npc, s->beta, s->eps_reg, c->d_vcr_g, nullptr, st),
+                 "vcr");
+    }
     gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (c->world == 1 && !signals_out) ? nullptr : y, b, st);
     if (r) return r;
     if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
         ProfScope ps(c, GPAIR_PROF_LOSS, st);
         float* lo = loss_out ? loss_out : (float*)(c->d_count);  // scratch word when only checking
-        API_CUDA(c, gpair::launch_loss(c, lo, st), "loss");
+        API_CUDA(c,
+                 reg ? gpair::launch_loss(c, lo, st, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
+                     : gpair::launch_loss(c, lo, st),
+                 "loss");
         if (c->flags & GPAIR_CHECK_FINITE) {
             float h = 0.f;
             API_CUDA(c, cudaMemcpyAsync(&h, lo, sizeof(float), cudaMemcpyDeviceToHost, st), "loss readback");
@@ -453,6 +499,8 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     ep.m = m;
     ep.v = v;
     ep.x_out = x_out;
+    ep.g_reg = reg ? c->d_vcr_g : nullptr;
+    ep.lam = s->lam;
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
     const int emode = npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP;
     API_CUDA(c,

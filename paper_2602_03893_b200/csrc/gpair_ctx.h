@@ -58,6 +58,12 @@ struct gpair_ctx_s {
     unsigned long long* d_count = nullptr;
     int32_t* d_flags = nullptr;   // scratch flags
 
+    // VCR regulariser workspaces (row f2, gpair_vcr.cu), allocated on first use
+    int64_t vcr_M = 0;
+    float* d_vcr_u = nullptr;     // [9][M] normalised difference fields
+    double* d_vcr_part = nullptr; // [ceil(M/256)] per-block fp64 values
+    float* d_vcr_g = nullptr;     // [M] dR/dx (caller order)
+
     int64_t workspace_bytes = 0;
     std::string err;
 
@@ -80,7 +86,9 @@ cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cu
 cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st);
 cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st);
-cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st);
+// loss = (1/N) sum of the data partials + lam * sum of n_reg regulariser partials
+cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st, const double* reg_part = nullptr,
+                        int32_t n_reg = 0, double lam = 0.0);
 struct EpiParams {
     float scale;
     float lr, beta1, beta2, adam_eps, eps_npc, bc1, bc2;
@@ -89,6 +97,8 @@ struct EpiParams {
     float* m;
     float* v;
     float* x_out;
+    const float* g_reg;  // [M] dR/dx in caller order (lam > 0), else NULL
+    float lam;
 };
 enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
 
@@ -97,7 +107,7 @@ enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
 // or the projected clamp step x <- max(x - lr g, 0); ic = caller index.
 template <int MODE>
 __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const EpiParams& ep) {
-    const float g = acc * ep.scale;
+    const float g = ep.g_reg ? fmaf(ep.lam, ep.g_reg[ic], acc * ep.scale) : acc * ep.scale;
     if (MODE == EPI_GRAD) {
         ep.g_out[ic] = g;
     } else if (MODE == EPI_NPC_ADAM) {
@@ -128,5 +138,11 @@ int assa_forward_warps();
 cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st);
+
+// VCR regulariser (gpair_vcr.cu); partial values stay in c->d_vcr_part
+cudaError_t vcr_ensure(gpair_ctx* c, int64_t M);
+cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int npc, float eps_npc, float beta,
+                       float eps, float* grad, float* value, cudaStream_t st);
+inline int32_t vcr_blocks(int64_t M) { return (int32_t)((M + 255) / 256); }
 
 }  // namespace gpair

@@ -256,17 +256,23 @@ __global__ void k_residual(const float* __restrict__ y, const float* __restrict_
     }
 }
 
-__global__ void k_loss(const double* __restrict__ part, int32_t n, double inv_N, float* out) {
-    __shared__ double s[1024];
-    double a = 0.0;
+__global__ void k_loss(const double* __restrict__ part, int32_t n, double inv_N, const double* __restrict__ reg,
+                       int32_t n_reg, double lam, float* out) {
+    __shared__ double s[1024], r[1024];
+    double a = 0.0, b = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+    for (int i = threadIdx.x; i < n_reg; i += blockDim.x) b += reg[i];
     s[threadIdx.x] = a;
+    r[threadIdx.x] = b;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        if ((int)threadIdx.x < o) {
+            s[threadIdx.x] += s[threadIdx.x + o];
+            r[threadIdx.x] += r[threadIdx.x + o];
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = (float)(s[0] * inv_N);
+    if (threadIdx.x == 0) out[0] = (float)(s[0] * inv_N + lam * r[0]);  // Eq. 23: data term + lam R_VCR
 }
 
 // ------------------------------------------------------------------ adjoint
@@ -481,8 +487,10 @@ cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float*
     return cudaGetLastError();
 }
 
-cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st) {
-    k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->Nd, 1.0 / ((double)c->Nd * (double)c->Nt), loss_out);
+cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st, const double* reg_part, int32_t n_reg,
+                        double lam) {
+    k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->Nd, 1.0 / ((double)c->Nd * (double)c->Nt), reg_part,
+                               reg_part ? n_reg : 0, lam, loss_out);
     return cudaGetLastError();
 }
 

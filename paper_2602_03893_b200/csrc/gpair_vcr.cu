@@ -1,0 +1,204 @@
+// gpair_vcr.cu -- vessel continuity regularisation on the voxel grid
+// (Eqs. 20-22), readings V1-V4 of
+// DESIGN.md (the same conventions as oracle/vcr.py, written independently):
+//   R_VCR = R_H + beta R_TV,  R_H = sum_i sqrt(sum_pq (D_pq x_i)^2 + eps),
+//   R_TV = sum_i sqrt(sum_d (D_d x_i)^2 + eps),  i = ix + nx (iy + ny iz).
+//   D_d   forward difference, 0 on the last index (replicate boundary)
+//   D_pp  [1,-2,1] on the nearest interior stencil (centre clamp(i,1,n-2))
+//   D_pq  forward-forward cross difference, 0 on the last index of p or q,
+//         counted twice (ordered pairs pq and qp)
+// Two passes, both one thread per voxel, deterministic:
+//   k_vcr_terms  differences, s_H, s_TV, the 9 normalised fields
+//                u = (D_d x / s_TV, D_pp x / s_H, 2 D_pq x / s_H) and fp64
+//                per-block partial values (fixed-order reduction later)
+//   k_vcr_grad   gather of the adjoint stencils: g = sum_pq D_pq^T u_pq
+//                + beta sum_d D_d^T u_d.
+#include "gpair_ctx.h"
+
+namespace gpair {
+
+namespace {
+
+struct Grid {
+    int nx, ny, nz;
+};
+
+__device__ __forceinline__ float xval(const float* __restrict__ src, int npc, float eps_npc, int64_t i) {
+    const float v = src[i];
+    return npc ? (v + eps_npc) * (v + eps_npc) : v;  // x = (z + eps)^2 (Eq. 18) when the state is z
+}
+
+__global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_npc, Grid G, float beta, float eps,
+                            float* __restrict__ u, int64_t M, double* __restrict__ part) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double val = 0.0;
+    if (i < M) {
+        const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = (int)(i / ((int64_t)G.nx * G.ny));
+        const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
+        const float x0 = xval(src, npc, eps_npc, i);
+        auto at = [&](int a, int b, int c) { return xval(src, npc, eps_npc, a * sx + b * sy + c * sz); };
+        // forward differences (V1)
+        const int xp = min(ix + 1, G.nx - 1), yp = min(iy + 1, G.ny - 1), zp = min(iz + 1, G.nz - 1);
+        const float dx = at(xp, iy, iz) - x0, dy = at(ix, yp, iz) - x0, dz = at(ix, iy, zp) - x0;
+        // pure second differences on the nearest interior stencil (V2)
+        float dxx = 0.f, dyy = 0.f, dzz = 0.f;
+        if (G.nx >= 3) {
+            const int c = min(max(ix, 1), G.nx - 2);
+            dxx = at(c + 1, iy, iz) - 2.f * at(c, iy, iz) + at(c - 1, iy, iz);
+        }
+        if (G.ny >= 3) {
+            const int c = min(max(iy, 1), G.ny - 2);
+            dyy = at(ix, c + 1, iz) - 2.f * at(ix, c, iz) + at(ix, c - 1, iz);
+        }
+        if (G.nz >= 3) {
+            const int c = min(max(iz, 1), G.nz - 2);
+            dzz = at(ix, iy, c + 1) - 2.f * at(ix, iy, c) + at(ix, iy, c - 1);
+        }
+        // mixed forward-forward differences (V3), 0 on the last index of either axis
+        const float dxy = (ix < G.nx - 1 && iy < G.ny - 1) ? at(ix + 1, iy + 1, iz) - at(ix + 1, iy, iz) - at(ix, iy + 1, iz) + x0 : 0.f;
+        const float dxz = (ix < G.nx - 1 && iz < G.nz - 1) ? at(ix + 1, iy, iz + 1) - at(ix + 1, iy, iz) - at(ix, iy, iz + 1) + x0 : 0.f;
+        const float dyz = (iy < G.ny - 1 && iz < G.nz - 1) ? at(ix, iy + 1, iz + 1) - at(ix, iy + 1, iz) - at(ix, iy, iz + 1) + x0 : 0.f;
+        const float stv = sqrtf(dx * dx + dy * dy + dz * dz + eps);
+        const float sh =
+            sqrtf(dxx * dxx + dyy * dyy + dzz * dzz + 2.f * (dxy * dxy + dxz * dxz + dyz * dyz) + eps);
+        const float itv = 1.f / stv, ih = 1.f / sh;
+        u[0 * M + i] = dx * itv;
+        u[1 * M + i] = dy * itv;
+        u[2 * M + i] = dz * itv;
+        u[3 * M + i] = dxx * ih;
+        u[4 * M + i] = dyy * ih;
+        u[5 * M + i] = dzz * ih;
+        u[6 * M + i] = 2.f * dxy * ih;
+        u[7 * M + i] = 2.f * dxz * ih;
+        u[8 * M + i] = 2.f * dyz * ih;
+        val = (double)sh + (double)beta * (double)stv;
+    }
+    __shared__ double s_red[32];
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) s_red[warp] = val;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += s_red[w];
+        part[blockIdx.x] = s;
+    }
+}
+
+// U(m) of a pure second difference along one axis: the sum of u over the
+// voxels whose clamped centre is m (m in [1, n-2]).
+__device__ __forceinline__ float fold_pp(const float* __restrict__ up, int64_t i, int64_t stride, int c, int n) {
+    if (c < 1 || c > n - 2) return 0.f;
+    float s = up[i + (int64_t)(c)*stride];
+    if (c == 1) s += up[i];                                 // voxel 0 uses centre 1
+    if (c == n - 2) s += up[i + (int64_t)(n - 1) * stride];  // voxel n-1 uses centre n-2
+    return s;
+}
+
+__global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int64_t M, float* __restrict__ g) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = (int)(i / ((int64_t)G.nx * G.ny));
+    const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
+    const float* ux = u;
+    const float* uy = u + M;
+    const float* uz = u + 2 * M;
+    // TV: (D_d^T u)(k) = u(k - e_d) [k_d >= 1] - u(k)   (u = 0 on the last index)
+    float gtv = -(ux[i] + uy[i] + uz[i]);
+    if (ix >= 1) gtv += ux[i - sx];
+    if (iy >= 1) gtv += uy[i - sy];
+    if (iz >= 1) gtv += uz[i - sz];
+    // pure second differences: g(k) = U(k-1) - 2 U(k) + U(k+1) along each axis
+    float gh = 0.f;
+    {
+        const int64_t r0 = i - (int64_t)ix * sx;  // start of the x line
+        const float* up = u + 3 * M;
+        if (G.nx >= 3) gh += fold_pp(up, r0, sx, ix - 1, G.nx) - 2.f * fold_pp(up, r0, sx, ix, G.nx) + fold_pp(up, r0, sx, ix + 1, G.nx);
+    }
+    {
+        const int64_t r0 = i - (int64_t)iy * sy;
+        const float* up = u + 4 * M;
+        if (G.ny >= 3) gh += fold_pp(up, r0, sy, iy - 1, G.ny) - 2.f * fold_pp(up, r0, sy, iy, G.ny) + fold_pp(up, r0, sy, iy + 1, G.ny);
+    }
+    {
+        const int64_t r0 = i - (int64_t)iz * sz;
+        const float* up = u + 5 * M;
+        if (G.nz >= 3) gh += fold_pp(up, r0, sz, iz - 1, G.nz) - 2.f * fold_pp(up, r0, sz, iz, G.nz) + fold_pp(up, r0, sz, iz + 1, G.nz);
+    }
+    // mixed: taps (+1 at (a+1,b+1), -1 at (a+1,b), -1 at (a,b+1), +1 at (a,b)),
+    // u = 0 where the forward operator is 0, so only existence checks remain
+    auto mixed_T = [&](const float* um, int a, int na, int64_t sa, int b, int nb, int64_t sb) {
+        float s = um[i];
+        if (a >= 1 && b >= 1) s += um[i - sa - sb];
+        if (a >= 1) s -= um[i - sa];
+        if (b >= 1) s -= um[i - sb];
+        (void)na;
+        (void)nb;
+        return s;
+    };
+    gh += mixed_T(u + 6 * M, ix, G.nx, sx, iy, G.ny, sy);
+    gh += mixed_T(u + 7 * M, ix, G.nx, sx, iz, G.nz, sz);
+    gh += mixed_T(u + 8 * M, iy, G.ny, sy, iz, G.nz, sz);
+    g[i] = gh + beta * gtv;
+}
+
+__global__ void k_vcr_sum(const double* __restrict__ part, int n, float* __restrict__ value) {
+    __shared__ double s[1024];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
+    s[threadIdx.x] = a;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) value[0] = (float)s[0];
+}
+
+}  // namespace
+
+cudaError_t vcr_ensure(gpair_ctx* c, int64_t M) {
+    if (c->vcr_M == M && c->d_vcr_u) return cudaSuccess;
+    cudaFree(c->d_vcr_u);
+    cudaFree(c->d_vcr_part);
+    cudaFree(c->d_vcr_g);
+    c->d_vcr_u = nullptr;
+    c->d_vcr_part = nullptr;
+    c->d_vcr_g = nullptr;
+    const int nb = (int)((M + 255) / 256);
+    cudaError_t e = cudaMalloc(&c->d_vcr_u, sizeof(float) * 9 * (size_t)M);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_part, sizeof(double) * nb);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_g, sizeof(float) * (size_t)M);
+    if (e == cudaSuccess) {
+        c->vcr_M = M;
+        c->workspace_bytes += (int64_t)(sizeof(float) * 10 * M + sizeof(double) * nb);
+    }
+    return e;
+}
+
+// value (device float, nullable) and gradient (device [M], nullable) of
+// R_VCR at x (npc: x = (src + eps_npc)^2).  Returns the per-block partials in
+// c->d_vcr_part (count = blocks) for fusion into the IR loss.
+cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int npc, float eps_npc, float beta,
+                       float eps, float* grad, float* value, cudaStream_t st) {
+    const int64_t M = (int64_t)dims[0] * dims[1] * dims[2];
+    cudaError_t e = vcr_ensure(c, M);
+    if (e != cudaSuccess) return e;
+    const Grid G{dims[0], dims[1], dims[2]};
+    const int nb = (int)((M + 255) / 256);
+    k_vcr_terms<<<nb, 256, 0, st>>>(src, npc, eps_npc, G, beta, eps, c->d_vcr_u, M, c->d_vcr_part);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (grad) {
+        k_vcr_grad<<<nb, 256, 0, st>>>(c->d_vcr_u, G, beta, M, grad);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (value) {
+        k_vcr_sum<<<1, 1024, 0, st>>>(c->d_vcr_part, nb, value);
+        e = cudaGetLastError();
+    }
+    return e;
+}
+
+}  // namespace gpair

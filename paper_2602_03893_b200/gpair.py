@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libgpair.so")
 OK, ERR_INVALID_ARGUMENT, ERR_GEOMETRY, ERR_RESOURCE, ERR_NUMERICAL, ERR_CUDA, ERR_NCCL = range(7)
 CHECK_FINITE = 1 << 9
 TOF_ASSA = 1
-PROF_NAMES = ["gather", "forward", "reduce", "allreduce", "residual", "adjoint", "loss"]
+PROF_NAMES = ["gather", "forward", "reduce", "allreduce", "residual", "adjoint", "loss", "vcr"]
 
 
 class GpairError(RuntimeError):
@@ -56,11 +56,15 @@ class Step(ctypes.Structure):
         ("grad_scale", ctypes.c_float),
         ("step", ctypes.c_int32),
         ("mode", ctypes.c_int32),
+        ("lam", ctypes.c_float),
+        ("beta", ctypes.c_float),
+        ("eps_reg", ctypes.c_float),
+        ("grid", ctypes.c_int32 * 3),
     ]
 
 
 class Profile(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * 7), ("launches", ctypes.c_int64 * 7)]
+    _fields_ = [("ms", ctypes.c_double * len(PROF_NAMES)), ("launches", ctypes.c_int64 * len(PROF_NAMES))]
 
 
 class Info(ctypes.Structure):
@@ -107,6 +111,7 @@ def lib():
             "gpair_adjoint": (st, [vp, vp, vp, vp]),
             "gpair_iterate": (st, [vp, vp, vp, vp, vp, ctypes.POINTER(Step), vp, vp, vp, vp]),
             "gpair_count_pair_samples": (st, [vp, ctypes.POINTER(i64), vp]),
+            "gpair_vcr": (st, [vp, ctypes.POINTER(i32), vp, ctypes.c_float, ctypes.c_float, vp, vp, vp]),
             "gpair_get_info": (st, [vp, ctypes.POINTER(Info)]),
             "gpair_destroy": (st, [vp]),
             "gpair_profile_enable": (st, [vp, ctypes.c_int]),
@@ -236,15 +241,29 @@ class Context:
         return out
 
     def iterate(self, z, m, v, b, *, lr, step, mode=0, beta1=0.9, beta2=0.999, adam_eps=1e-8, eps_npc=1e-8,
-                grad_scale=0.0, signals_out=None, x_out=None, loss_out=None, stream=None):
+                grad_scale=0.0, lam=0.0, beta=0.0, eps_reg=1e-8, grid=None, signals_out=None, x_out=None,
+                loss_out=None, stream=None):
+        """One Alg. 2 iteration; lam > 0 adds lam R_VCR (Eqs. 20-23) over the
+        voxel grid `grid` = (nx, ny, nz) of the kernel order."""
+        g3 = (ctypes.c_int32 * 3)(*(grid if grid is not None else (0, 0, 0)))
         s = Step(lr=lr, beta1=beta1, beta2=beta2, adam_eps=adam_eps, eps_npc=eps_npc, grad_scale=grad_scale,
-                 step=int(step), mode=int(mode))
+                 step=int(step), mode=int(mode), lam=lam, beta=beta, eps_reg=eps_reg, grid=g3)
         n = self.M
         _check(lib().gpair_iterate(self._h, _ptr(z, numel=n, name="z"), _ptr(m, numel=n, name="m"),
                                    _ptr(v, numel=n, name="v"), _ptr(b, numel=self.Nd * self.Nt, name="b"),
                                    ctypes.byref(s), _ptr(signals_out, numel=self.Nd * self.Nt, name="signals_out"),
                                    _ptr(x_out, numel=n, name="x_out"), _ptr(loss_out, numel=1, name="loss_out"),
                                    _stream(stream)), self._h)
+
+    def vcr(self, x, grid, *, beta, eps=1e-8, grad=None, value=None, stream=None):
+        """R_VCR(x) = R_H + beta R_TV (Eqs. 20-22) into device `value` [1]
+        and/or its gradient into device `grad` [prod(grid)]."""
+        n = int(grid[0]) * int(grid[1]) * int(grid[2])
+        g3 = (ctypes.c_int32 * 3)(*(int(d) for d in grid))
+        n = n if n > 0 else None  # bad grids are rejected by the library (INVALID_ARGUMENT)
+        _check(lib().gpair_vcr(self._h, g3, _ptr(x, numel=n, name="x"), float(beta), float(eps),
+                               _ptr(grad, numel=n, name="grad"), _ptr(value, numel=1, name="value"),
+                               _stream(stream)), self._h)
 
     def count_pair_samples(self, stream=None):
         out = ctypes.c_int64()
