@@ -124,6 +124,33 @@ def vessel_phantom(nx, ny, nz, seed=2, n_tubes=None):
     return amp.ravel().astype(np.float32)
 
 
+def blobs_phantom(nx, ny, nz, count=5, seed=5):
+    """Desk-scale phantom ("blobs"): `count`
+    isotropic Gaussian blobs, centres U[0.25, 0.75] of each axis, std-dev
+    U[1.5, 3] voxels, peak U[0.5, 1]; max over blobs, zeroed below 1e-3.
+    Units: voxel indices; returns float32 [M] in grid order."""
+    rng = np.random.default_rng(seed)
+    zz, yy, xx = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    amp = np.zeros((nz, ny, nx), dtype=np.float64)
+    dims = np.array([nx, ny, nz], dtype=np.float64)
+    for _ in range(count):
+        c = rng.uniform(0.25, 0.75, 3) * (dims - 1)
+        rad = rng.uniform(1.5, 3.0)
+        peak = rng.uniform(0.5, 1.0)
+        d2 = (xx - c[0]) ** 2 + (yy - c[1]) ** 2 + (zz - c[2]) ** 2
+        np.maximum(amp, peak * np.exp(-d2 / (2.0 * rad * rad)), out=amp)
+    amp[amp < 1e-3] = 0.0
+    return amp.ravel().astype(np.float32)
+
+
+def add_noise(b, snr, seed=9):
+    """Additive zero-mean Gaussian noise with max|b| / std = snr (SPEC S:708,
+    the amplitude reading of the paper's "SNR ~ 5:1")."""
+    rng = np.random.default_rng(seed)
+    std = float(np.abs(b).max()) / snr
+    return (b + rng.standard_normal(b.shape) * std).astype(b.dtype)
+
+
 @dataclass(frozen=True)
 class Config:
     """One workload of SURVEY.md section 8(d) (BASELINE.json configs)."""
@@ -168,6 +195,9 @@ CONFIGS = {
     "cfg3": Config("cfg3", (128, 128, 128), 0.1 * MM, "hemisphere", 1024, 60 * MM, 4096),
     "cfg4": Config("cfg4", (256, 256, 128), 0.1 * MM, "hemisphere", 1024, 60 * MM, 4096),
     "cfg5": Config("cfg5", (256, 256, 128), 0.1 * MM, "planar", 512, 0.0, 4096),
+    # desk-scale reconstruction workload (row f3): 32^3 at 0.4 mm,
+    # 64-element hemisphere of radius 25 mm, W = 64 samples per pair
+    "desk": Config("desk", (32, 32, 32), 0.4 * MM, "hemisphere", 64, 25 * MM, 1024),
     # secondary regime of the paper's Fig. 1f (f_s = 20 MHz, sigma = 62.5 um): W = 5
     "cfg4p": Config("cfg4p", (256, 256, 128), 0.1 * MM, "hemisphere", 1024, 60 * MM, 4096,
                     fs=20e6, sigma=62.5e-6),

@@ -36,3 +36,14 @@ def assert_parity(got, ref, what, elementwise=True):
     return rel, elem
 
 
+
+
+def psnr(a, ref):
+    """Desk-scale quality metric: both max-normalised,
+    psnr = 10 log10(1 / mse), capped at 200 dB."""
+    a = np.asarray(a, np.float64)
+    ref = np.asarray(ref, np.float64)
+    a = a / np.abs(a).max()
+    ref = ref / np.abs(ref).max()
+    mse = float(np.mean((a - ref) ** 2))
+    return 200.0 if mse < 1e-20 else 10.0 * np.log10(1.0 / mse)
