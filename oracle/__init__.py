@@ -61,6 +61,10 @@ def lib():
         L.oracle_forward.argtypes = [i64, vp, vp, d, vp, i32, vp, d, d, d, i32, d, vp, i32, vp]
         L.oracle_adjoint.restype = ctypes.c_int
         L.oracle_adjoint.argtypes = [i64, vp, d, vp, i32, vp, d, d, d, i32, d, vp, vp, i64, vp]
+        L.oracle_forward_nf.restype = ctypes.c_int
+        L.oracle_forward_nf.argtypes = L.oracle_forward.argtypes
+        L.oracle_adjoint_nf.restype = ctypes.c_int
+        L.oracle_adjoint_nf.argtypes = L.oracle_adjoint.argtypes
         L.oracle_count_pair_samples.restype = i64
         L.oracle_count_pair_samples.argtypes = [i64, vp, d, i32, vp, d, d, d, i32, d, vp, i64]
         L.oracle_assa_taps.restype = None
@@ -109,11 +113,13 @@ def pressure_outgoing(A, r, t, v, sigma, k=3.0):
 
 
 def forward(centers, amp, sensors, *, sigma, v, fs, n_samples, t0=0.0, k=3.0,
-            sigmas=None, rows=None):
+            sigmas=None, rows=None, near_field=False):
     """y = A x by direct enumeration. Returns fp64 [n_rows][N_t].
 
     centers: [3][M] float32 SoA (metres); amp: [M] (promoted to fp64);
-    sensors: [3][N_d] float32 SoA; rows: optional sensor subset (exact rows).
+    sensors: [3][N_d] float32 SoA; rows: optional sensor subset (exact rows);
+    sigmas: optional per-kernel sigma_i [M] (row f4, reading N2);
+    near_field: Eq. 6 with both terms (row f4, reading N1), pairs need r > 0.
     """
     amp = np.ascontiguousarray(amp, dtype=np.float64)
     M = amp.shape[0]
@@ -127,18 +133,19 @@ def forward(centers, amp, sensors, *, sigma, v, fs, n_samples, t0=0.0, k=3.0,
     else:
         n_rows = Nd
     y = np.zeros((n_rows, int(n_samples)), dtype=np.float64)
-    rc = lib().oracle_forward(M, _ptr(c), _ptr(amp), float(sigma), _ptr(sg), Nd, _ptr(s),
-                              float(v), float(fs), float(t0), int(n_samples), float(k),
-                              _ptr(rows), n_rows, _ptr(y))
+    fn = lib().oracle_forward_nf if near_field else lib().oracle_forward
+    rc = fn(M, _ptr(c), _ptr(amp), float(sigma), _ptr(sg), Nd, _ptr(s),
+            float(v), float(fs), float(t0), int(n_samples), float(k), _ptr(rows), n_rows, _ptr(y))
     if rc == 2:
-        raise OracleGeometryError("a kernel-sensor distance r_ij <= k*sigma (far-field model invalid)")
+        raise OracleGeometryError("r_ij = 0" if near_field else
+                                  "a kernel-sensor distance r_ij <= k*sigma (far-field model invalid)")
     if rc != 0:
         raise ValueError(f"oracle_forward: invalid argument (rc={rc})")
     return y
 
 
 def adjoint(centers, delta, sensors, *, sigma, v, fs, t0=0.0, k=3.0, sigmas=None, cols=None,
-            n_kernels=None):
+            n_kernels=None, near_field=False):
     """g = A^T delta (exact transpose of ``forward``). Returns fp64 [n_cols]."""
     delta = np.ascontiguousarray(delta, dtype=np.float64)
     Nd, Nt = delta.shape
@@ -152,10 +159,12 @@ def adjoint(centers, delta, sensors, *, sigma, v, fs, t0=0.0, k=3.0, sigmas=None
     else:
         n_cols = M
     g = np.zeros(n_cols, dtype=np.float64)
-    rc = lib().oracle_adjoint(M, _ptr(c), float(sigma), _ptr(sg), Nd, _ptr(s), float(v), float(fs),
-                              float(t0), Nt, float(k), _ptr(delta), _ptr(cols), n_cols, _ptr(g))
+    fn = lib().oracle_adjoint_nf if near_field else lib().oracle_adjoint
+    rc = fn(M, _ptr(c), float(sigma), _ptr(sg), Nd, _ptr(s), float(v), float(fs),
+            float(t0), Nt, float(k), _ptr(delta), _ptr(cols), n_cols, _ptr(g))
     if rc == 2:
-        raise OracleGeometryError("a kernel-sensor distance r_ij <= k*sigma (far-field model invalid)")
+        raise OracleGeometryError("r_ij = 0" if near_field else
+                                  "a kernel-sensor distance r_ij <= k*sigma (far-field model invalid)")
     if rc != 0:
         raise ValueError(f"oracle_adjoint: invalid argument (rc={rc})")
     return g

@@ -222,6 +222,112 @@ int64_t oracle_count_pair_samples(int64_t M, const float* centers, double sigma,
 }
 
 /* ------------------------------------------------------------------------
+ * Near-field operator: Eq. 6 with BOTH terms,
+ * the outgoing (r - v t) and the incoming (r + v t) wave, each truncated to
+ * |.| < k sigma like P:291 (reading N1), with an optional
+ * per-kernel sigma_i (reading N2):
+ *   a_ijn = [dm exp(-dm^2/(2 s^2)) 1(|dm| < k s) + dp exp(-dp^2/(2 s^2)) 1(|dp| < k s)] / (2 r)
+ *   dm = r - v t_n,  dp = r + v t_n,  s = sigma_i,  t_n = t0 + n / f_s.
+ * Eq. 6 holds for every r > 0 (its 1/r is the only singularity), so pairs
+ * need r > 0 instead of r > k sigma; r = 0 returns ORACLE_ERR_GEOMETRY
+ * (reading N3).  When the incoming window of a pair is empty the entry is
+ * bit-identical to oracle_forward's (an added +0.0 changes nothing).
+ * Candidates: the union of the outgoing range and the incoming range
+ * n in [floor(((-k s - r)/v - t0) f_s) - 2, ceil(((k s - r)/v - t0) f_s) + 2].
+ * ---------------------------------------------------------------------- */
+static double nf_entry(double r, double s, double ks, double v, double t) {
+    double dm = r - v * t, dp = r + v * t;
+    double tm = 0.0, tp = 0.0;
+    if (fabs(dm) < ks) tm = dm * exp(-(dm * dm) / (2.0 * s * s));
+    if (fabs(dp) < ks) tp = dp * exp(-(dp * dp) / (2.0 * s * s));
+    return (tm + tp) / (2.0 * r);
+}
+
+static void nf_range(double r, double ks, double v, double fs, double t0, int32_t Nt, int64_t* n0, int64_t* n1) {
+    candidate_range(r, ks, v, fs, t0, Nt, n0, n1);
+    double lo = floor(((-ks - r) / v - t0) * fs) - 2.0;
+    double hi = ceil(((ks - r) / v - t0) * fs) + 2.0;
+    if (lo < 0.0) lo = 0.0;
+    if (hi > (double)(Nt - 1)) hi = (double)(Nt - 1);
+    if (lo <= hi) {  /* non-empty incoming range: take the union */
+        if ((int64_t)lo < *n0) *n0 = (int64_t)lo;
+        if ((int64_t)hi > *n1) *n1 = (int64_t)hi;
+    }
+}
+
+int oracle_forward_nf(int64_t M, const float* centers, const double* amp,
+                      double sigma, const double* sigmas,
+                      int32_t Nd, const float* sensors,
+                      double v, double fs, double t0, int32_t Nt, double k,
+                      const int32_t* rows, int32_t n_rows, double* y) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc) return rc;
+    if (rows == NULL) n_rows = Nd;
+    int err = ORACLE_OK;
+    int nth = oracle_get_threads();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nth)
+    for (int32_t jo = 0; jo < n_rows; ++jo) {
+        int32_t j = rows ? rows[jo] : jo;
+        double* yj = y + (int64_t)jo * Nt;
+        for (int32_t n = 0; n < Nt; ++n) yj[n] = 0.0;
+        for (int64_t i = 0; i < M; ++i) {
+            double s = sigmas ? sigmas[i] : sigma;
+            double ks = k * s;
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            if (!(r > 0.0)) {
+#pragma omp atomic write
+                err = ORACLE_ERR_GEOMETRY;
+                continue;
+            }
+            int64_t n0, n1;
+            nf_range(r, ks, v, fs, t0, Nt, &n0, &n1);
+            for (int64_t n = n0; n <= n1; ++n) {
+                double t = t0 + (double)n / fs;
+                yj[n] += amp[i] * nf_entry(r, s, ks, v, t);
+            }
+        }
+    }
+    return err;
+}
+
+int oracle_adjoint_nf(int64_t M, const float* centers,
+                      double sigma, const double* sigmas,
+                      int32_t Nd, const float* sensors,
+                      double v, double fs, double t0, int32_t Nt, double k,
+                      const double* delta, const int64_t* cols, int64_t n_cols,
+                      double* g) {
+    int rc = check_args(M, Nd, Nt, sigma, v, fs, k);
+    if (rc) return rc;
+    if (cols == NULL) n_cols = M;
+    int err = ORACLE_OK;
+    int nth = oracle_get_threads();
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nth)
+    for (int64_t io = 0; io < n_cols; ++io) {
+        int64_t i = cols ? cols[io] : io;
+        double s = sigmas ? sigmas[i] : sigma;
+        double ks = k * s;
+        double acc = 0.0;
+        for (int32_t j = 0; j < Nd; ++j) {
+            double r = pair_distance(centers, M, i, sensors, Nd, j);
+            if (!(r > 0.0)) {
+#pragma omp atomic write
+                err = ORACLE_ERR_GEOMETRY;
+                continue;
+            }
+            const double* dj = delta + (int64_t)j * Nt;
+            int64_t n0, n1;
+            nf_range(r, ks, v, fs, t0, Nt, &n0, &n1);
+            for (int64_t n = n0; n <= n1; ++n) {
+                double t = t0 + (double)n / fs;
+                acc += nf_entry(r, s, ks, v, t) * dj[n];
+            }
+        }
+        g[io] = acc;
+    }
+    return err;
+}
+
+/* ------------------------------------------------------------------------
  * ASSA operator: the paper's discrete operator,
  * Eqs. 8-17 and Algorithm 1, stage by stage:
  *   Eq. 9 projection P_up:  k_ij = floor((r_ij/v - t0) f_s^up + 0.5)

@@ -117,6 +117,8 @@ def test_iterate_with_vcr_teacher_forced(mode):
     v0 = (gz0 * gz0 * rng.uniform(0.5, 1.5, cfg.M)).astype(np.float32)
     t_step = 4
     lr = gpair.cawr_lr(t_step - 1, 1e-4, 0.1, 50, 1)
+    if mode == 1:  # projected step: take lr so that lr |g| is a visible fraction of z (fp32 z - lr g)
+        lr = float(0.05 * np.abs(z0).max() / np.abs(gz0).max())
     zt, mt, vt = T(z0), T(m0), T(v0)
     loss = torch.empty(1, device=dev())
     ctx.iterate(zt, mt, vt, T(b), lr=lr, step=t_step, mode=mode, lam=lam, beta=0.5, eps_reg=1e-4, grid=cfg.grid,
