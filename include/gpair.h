@@ -70,6 +70,12 @@ enum {
                                    is its exact transpose (zero-fill, correlation,
                                    back-projection).  Impulses with k_ij outside
                                    [0, alpha N_t) do not exist (reading A3). */
+    GPAIR_NEAR_FIELD = 1 << 1,  /* near-field operator (N1-N3):
+                                   Eq. 6 with BOTH terms, each truncated to
+                                   |.| < k sigma_i:  a_ijn = [dm e^{-dm^2/2s^2} 1(|dm|<ks)
+                                   + dp e^{-dp^2/2s^2} 1(|dp|<ks)] / (2 r),  dm = r - v t_n,
+                                   dp = r + v t_n.  Pairs need only r > 0 (GEOMETRY if some
+                                   r = 0).  Exact operator only (not with GPAIR_TOF_ASSA). */
     GPAIR_CHECK_FINITE = 1 << 9 /* gpair_iterate syncs and checks the loss is finite */
 };
 
@@ -82,7 +88,10 @@ typedef struct {
     int64_t n_kernels;     /* M_local >= 1: kernels owned by this rank            */
     const float* centers;  /* DEVICE [3][M_local] SoA centres c_i [m], caller order      */
     double sigma;          /* Gaussian std-dev [m] > 0, shared by all kernels    */
-    const float* sigmas;   /* must be NULL: per-kernel sigma is a NEXT row (R5)          */
+    const float* sigmas;   /* DEVICE [M_local] per-kernel sigma_i > 0 [m] (row f4, N2), read
+                              during create only; NULL -> `sigma` for every kernel.  Not
+                              with GPAIR_TOF_ASSA.  With sigmas and without
+                              GPAIR_NEAR_FIELD the r > k sigma check uses max sigma_i    */
     double window_k;       /* k in |d| < k sigma; paper: 3                        */
     int32_t n_sensors;     /* N_d >= 1                                                    */
     const float* sensors;  /* DEVICE [3][N_d] SoA point-detector positions [m]   */
@@ -150,6 +159,9 @@ typedef struct {
     int32_t assa_alpha;         /* ASSA upsampling ratio alpha (Eq. 8)                  */
     int32_t assa_n_half;        /* ASSA N_half (Eq. 8)                                  */
     int32_t assa_K;             /* ASSA taps half-width K = alpha N_half (Eq. 11)       */
+    int32_t general;            /* 1: per-kernel sigma and/or near-field path (row f4)   */
+    int32_t near_rows;          /* sensors with near-field pairs                        */
+    int64_t near_pairs;         /* pairs evaluated with both Eq. 6 terms (r < k sigma_i) */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial
@@ -203,7 +215,8 @@ gpair_status gpair_iterate(gpair_ctx* ctx, float* z, float* m, float* v, const f
 
 /* Exact number of in-window pair-samples (|d| < k sigma, n in [0, N_t)) of
  * this rank's operator; for an ASSA context, the number of existing impulses
- * (pairs with k_ij in [0, alpha N_t)).  Synchronous.  Host output. */
+ * (pairs with k_ij in [0, alpha N_t)).  Synchronous.  Host output.
+ * INVALID_ARGUMENT for per-kernel-sigma / near-field contexts. */
 gpair_status gpair_count_pair_samples(gpair_ctx* ctx, int64_t* out_host, void* stream);
 
 /* Fill *out (host struct) with the context's build parameters. */

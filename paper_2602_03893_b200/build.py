@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpair.so")
-SOURCES = ["gpair_api.cu", "gpair_setup.cu", "gpair_kernels.cu", "gpair_assa.cu", "gpair_vcr.cu"]
+SOURCES = ["gpair_api.cu", "gpair_setup.cu", "gpair_kernels.cu", "gpair_assa.cu", "gpair_vcr.cu", "gpair_near.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -137,6 +137,14 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_flags);
     cudaFree(c->d_taps);
     cudaFree(c->d_dconv);
+    cudaFree(c->d_ksig);
+    cudaFree(c->d_near_f);
+    cudaFree(c->d_near_a);
+    cudaFree(c->d_near_rseg);
+    cudaFree(c->d_near_cseg);
+    cudaFree(c->d_near_row);
+    cudaFree(c->d_ynear);
+    cudaFree(c->d_gnear);
     cudaFree(c->d_vcr_u);
     cudaFree(c->d_vcr_part);
     cudaFree(c->d_vcr_g);
@@ -215,7 +223,24 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     if (d->n_sensors < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_sensors must be >= 1");
     if (d->n_kernels < 1) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "n_kernels must be >= 1");
     if (!d->centers || !d->sensors) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "centers/sensors NULL");
-    if (d->sigmas) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "per-kernel sigmas are not supported (must be NULL)");
+    const bool nf = (d->flags & GPAIR_NEAR_FIELD) != 0;
+    const bool gen = nf || d->sigmas;
+    if (gen && (d->flags & GPAIR_TOF_ASSA))
+        return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "per-kernel sigmas / near field need the exact operator");
+    double s_max = d->sigma;
+    if (d->sigmas) {  // validate sigma_i > 0 finite; the largest sizes the windows (row f4)
+        std::vector<float> hs((size_t)d->n_kernels);
+        cudaError_t e0 = cudaMemcpyAsync(hs.data(), d->sigmas, sizeof(float) * hs.size(), cudaMemcpyDeviceToHost,
+                                         (cudaStream_t)stream);
+        if (e0 == cudaSuccess) e0 = cudaStreamSynchronize((cudaStream_t)stream);
+        if (e0 != cudaSuccess) return cuda_fail(nullptr, e0, "reading sigmas");
+        s_max = 0.0;
+        for (float x : hs) {
+            if (!(x > 0.f) || !std::isfinite(x))
+                return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "sigmas must be finite > 0");
+            s_max = std::max(s_max, (double)x);
+        }
+    }
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
         return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "rank/world invalid");
     if (d->world > 1 && !d->nccl_comm) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "world > 1 needs nccl_comm");
@@ -232,7 +257,7 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     k.v = v;
     k.fs = fs;
     k.t0 = d->t0;
-    k.ks = kk * s;  // same expression as the oracle's k * sigma
+    k.ks = kk * (d->sigmas ? s_max : s);  // same expression as the oracle's k * sigma
     k.Nt = d->n_samples;
     k.Nd = d->n_sensors;
     double Lw = 2.0 * k.ks / h;
@@ -256,6 +281,14 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     }
     k.K1u = (float)(-log2e * h * h / (2.0 * s * s));
     k.win_half = k.ks;
+    k.kwin = kk;
+    k.sigma = s;
+    k.per_sigma = d->sigmas ? 1 : 0;
+    k.gen = gen ? 1 : 0;
+    k.nf = nf ? 1 : 0;
+    k.nf_add = std::max(0.0, -v * d->t0);
+    k.nf_thr_max = nf ? (k.ks + k.nf_add) * (1.0 + 1e-6) + 1e-12 : -1.0;
+    if (gen) k.cnt_int = 0;
     k.two_over_h = (float)(2.0 / h);
     const bool assa = (d->flags & GPAIR_TOF_ASSA) != 0;
     std::vector<float> taps;
@@ -301,12 +334,16 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     c->nccl = d->nccl_comm;
     c->flags = d->flags;
     c->assa = assa ? 1 : 0;
+    c->gen = gen ? 1 : 0;
+    c->nf = nf ? 1 : 0;
+    c->create_sigmas = d->sigmas;
     cudaStream_t st = (cudaStream_t)stream;
     std::string why;
     int geom_err = 0;
     e = gpair::build_geometry(c, d->centers, d->sensors, st, why, geom_err);
     if (e != cudaSuccess) {
-        std::string m = std::string("gpair_create: ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+        std::string m = std::string("gpair_create: ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")" +
+                        (why.empty() ? "" : " at " + why);
         free_ctx(c);
         return fail(nullptr, e == cudaErrorMemoryAllocation ? GPAIR_ERR_RESOURCE : GPAIR_ERR_CUDA, m);
     }
@@ -327,6 +364,7 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
         }
         c->workspace_bytes += (int64_t)(sizeof(float) * (taps.size() + (size_t)c->Nd * k.alpha * c->Nt));
     }
+    c->create_sigmas = nullptr;
     *out = c;
     return GPAIR_OK;
 }
@@ -358,6 +396,9 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->assa_alpha = c->k.alpha;
     o->assa_n_half = c->k.n_half;
     o->assa_K = c->k.K;
+    o->general = c->gen;
+    o->near_rows = c->n_near_rows;
+    o->near_pairs = c->n_near;
     return GPAIR_OK;
 }
 
@@ -370,6 +411,7 @@ static gpair_status do_forward_core(gpair_ctx* c, const float* src, int npc, flo
     {
         ProfScope ps(c, GPAIR_PROF_FORWARD, st);
         API_CUDA(c, c->assa ? gpair::launch_assa_forward(c, st) : gpair::launch_forward(c, st), "forward");
+        if (c->n_near) API_CUDA(c, gpair::launch_near_forward(c, st), "near-field forward");
     }
     if (c->world == 1) {
         ProfScope ps(c, GPAIR_PROF_REDUCE, st);
@@ -407,6 +449,10 @@ gpair_status gpair_adjoint(gpair_ctx* c, const float* residual, float* grad, voi
     ep.scale = 1.f;
     ep.g_out = grad;
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+    if (c->n_near) {
+        API_CUDA(c, gpair::launch_near_adjoint(c, residual, st), "near-field adjoint");
+        ep.g_add = c->d_gnear;
+    }
     API_CUDA(c,
              c->assa ? gpair::launch_assa_adjoint(c, residual, gpair::EPI_GRAD, ep, st)
                      : gpair::launch_adjoint(c, residual, gpair::EPI_GRAD, ep, st),
@@ -502,6 +548,10 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     ep.g_reg = reg ? c->d_vcr_g : nullptr;
     ep.lam = s->lam;
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+    if (c->n_near) {
+        API_CUDA(c, gpair::launch_near_adjoint(c, c->d_delta, st), "near-field adjoint");
+        ep.g_add = c->d_gnear;
+    }
     const int emode = npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP;
     API_CUDA(c,
              c->assa ? gpair::launch_assa_adjoint(c, c->d_delta, emode, ep, st)
@@ -512,6 +562,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
 
 gpair_status gpair_count_pair_samples(gpair_ctx* c, int64_t* out, void* stream) {
     if (!c || !out) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (c->gen) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "count is not defined for per-kernel sigma / near field");
     cudaStream_t st = (cudaStream_t)stream;
     API_CUDA(c, c->assa ? gpair::launch_assa_count(c, st) : gpair::launch_count(c, st), "count");
     unsigned long long h = 0;

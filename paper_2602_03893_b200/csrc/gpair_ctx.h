@@ -58,6 +58,20 @@ struct gpair_ctx_s {
     unsigned long long* d_count = nullptr;
     int32_t* d_flags = nullptr;   // scratch flags
 
+    // general operator (row f4): per-kernel sigma table and near-field pairs
+    int gen = 0, nf = 0;
+    const float* create_sigmas = nullptr;  // caller's DEVICE sigmas, read during create only
+    float4* d_ksig = nullptr;     // [Mpad] (k sigma_i / h, -log2e h^2 / 2 sigma_i^2, sigma_i, 0), sorted order
+    int64_t n_near = 0;           // near pairs (r < near_threshold) of this rank
+    int32_t n_near_rows = 0, n_near_cols = 0;
+    uint64_t* d_near_f = nullptr; // [n_near] (j << 32 | i_sorted), sorted: forward order
+    uint64_t* d_near_a = nullptr; // [n_near] (i_sorted << 32 | j), sorted: adjoint order
+    int32_t* d_near_rseg = nullptr; // [n_near_rows + 1] segment offsets into d_near_f
+    int32_t* d_near_cseg = nullptr; // [n_near_cols + 1] segment offsets into d_near_a
+    int32_t* d_near_row = nullptr;  // [Nd] compact near row of sensor j, or -1
+    double* d_ynear = nullptr;      // [n_near_rows][Nt] near-field signal rows
+    float* d_gnear = nullptr;       // [M] near-field adjoint terms, caller order
+
     // VCR regulariser workspaces (row f2, gpair_vcr.cu), allocated on first use
     int64_t vcr_M = 0;
     float* d_vcr_u = nullptr;     // [9][M] normalised difference fields
@@ -99,6 +113,7 @@ struct EpiParams {
     float* x_out;
     const float* g_reg;  // [M] dR/dx in caller order (lam > 0), else NULL
     float lam;
+    const float* g_add;  // [M] near-field adjoint terms in caller order (row f4), else NULL
 };
 enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
 
@@ -107,6 +122,7 @@ enum { EPI_GRAD = 0, EPI_NPC_ADAM = 1, EPI_CLAMP = 2 };
 // or the projected clamp step x <- max(x - lr g, 0); ic = caller index.
 template <int MODE>
 __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const EpiParams& ep) {
+    if (ep.g_add) acc += ep.g_add[ic];
     const float g = ep.g_reg ? fmaf(ep.lam, ep.g_reg[ic], acc * ep.scale) : acc * ep.scale;
     if (MODE == EPI_GRAD) {
         ep.g_out[ic] = g;
@@ -138,6 +154,11 @@ int assa_forward_warps();
 cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st);
+
+// general operator (gpair_near.cu)
+cudaError_t build_general(gpair_ctx* c, cudaStream_t st, std::string& why, int& geom_err);
+cudaError_t launch_near_forward(gpair_ctx* c, cudaStream_t st);
+cudaError_t launch_near_adjoint(gpair_ctx* c, const float* resid, cudaStream_t st);
 
 // VCR regulariser (gpair_vcr.cu); partial values stay in c->d_vcr_part
 cudaError_t vcr_ensure(gpair_ctx* c, int64_t M);

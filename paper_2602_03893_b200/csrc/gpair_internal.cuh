@@ -57,7 +57,33 @@ struct OpConst {
     double fs_up;          // alpha f_s (computed as (double)alpha * fs, like the oracle)
     float two_over_h;      // 2 / h: (A h / 2r) * (2/h) = A / r
     double win_half;       // half-width [m] of the conservative sample windows (setup)
+    // general operator (row f4): per-kernel sigma_i and/or the near-field term
+    double kwin;           // window k (fp64, the oracle's k in k * sigma_i)
+    int32_t gen;           // 1: per-kernel sigma table / near-field (kernel path SER_GEN)
+    int32_t nf;            // 1: near-field operator (Eq. 6, both terms; reading N1)
+    double nf_add;         // max(0, -v t0): near pairs are r < k sigma_i + nf_add (+ margin)
+    double nf_thr_max;     // bound of every pair's near threshold; -1 when nf = 0
+    int32_t per_sigma;     // 1: sigma_i from the table (desc.sigmas); 0: the scalar sigma
+    double sigma;          // scalar sigma (fp64, as given)
 };
+
+constexpr int SER_GEN = 7;  // kernel path of the general operator (pair_gen)
+
+// Near-pair threshold of reading N1: pairs with r < thr are evaluated with
+// both terms of Eq. 6 by gpair_near.cu; the rest carry only the outgoing
+// term (their incoming window is empty; the relative margin only moves a few
+// more pairs to the exact near path).  Used identically by the near-list
+// builder and the main kernels' exact path.
+__device__ __forceinline__ double kernel_sigma(float sigma_i, const OpConst& k) {
+    return k.per_sigma ? (double)sigma_i : k.sigma;
+}
+// k sigma_i exactly as the oracle forms it (`double ks = k * s;`)
+__device__ __forceinline__ double kernel_ks(float sigma_i, const OpConst& k) {
+    return k.per_sigma ? __dmul_rn(k.kwin, (double)sigma_i) : k.ks;
+}
+__device__ __forceinline__ double near_threshold(double ks, const OpConst& k) {
+    return __dadd_rn(__dmul_rn(__dadd_rn(ks, k.nf_add), 1.0 + 1e-9), 1e-15);
+}
 
 // fp64 anchor of a (group, sensor) pair, reduced to what the per-pair fp32
 // arithmetic needs.  na == NA_EXACT: use the per-pair fp64 path.
@@ -91,7 +117,8 @@ __device__ __forceinline__ Anchor make_anchor(float4 C, float sx, float sy, floa
     a.h2R = (float)(0.5 * k.h * invR);
     // series accuracy: |eps| <= (2 R rad + rad^2) / R^2 (C.w = group radius)
     const double rad = C.w;
-    const bool series_ok = fma(2.0 * R, rad, rad * rad) <= EPS_FAST * R2 && rad <= MAX_DR_SAMPLES * k.h;
+    const bool series_ok = fma(2.0 * R, rad, rad * rad) <= EPS_FAST * R2 && rad <= MAX_DR_SAMPLES * k.h &&
+                           R - rad > k.nf_thr_max;  // near pairs (row f4) always take the exact path
     a.na = series_ok ? (int32_t)na : NA_EXACT;
     return a;
 }
@@ -117,13 +144,13 @@ __device__ __forceinline__ double exact_d(double r, int n, const OpConst& k) {
 }
 
 __device__ __forceinline__ void exact_window(double r, int g_first, int g_last, const OpConst& k,
-                                                 int& n_lo, int& cnt) {
+                                                 int& n_lo, int& cnt, double ks) {
     int f = g_first;
-    while (exact_d(r, f - 1, k) < k.ks) --f;
-    while (!(exact_d(r, f, k) < k.ks)) ++f;
+    while (exact_d(r, f - 1, k) < ks) --f;
+    while (!(exact_d(r, f, k) < ks)) ++f;
     int l = g_last;
-    while (exact_d(r, l + 1, k) > -k.ks) ++l;
-    while (!(exact_d(r, l, k) > -k.ks)) --l;
+    while (exact_d(r, l + 1, k) > -ks) ++l;
+    while (!(exact_d(r, l, k) > -ks)) --l;
     if (f < 0) f = 0;
     if (l > k.Nt - 1) l = k.Nt - 1;
     n_lo = f;
@@ -133,8 +160,9 @@ __device__ __forceinline__ void exact_window(double r, int g_first, int g_last, 
 
 // Exact per-pair fp64 time of flight for groups outside the series' range.
 __device__ __forceinline__ void exact_pair(float cx, float cy, float cz, float sx, float sy, float sz,
-                                               float A, const OpConst& k, float& eu, float& w, int& na) {
-    double r = exact_r(cx, cy, cz, sx, sy, sz);
+                                               float A, const OpConst& k, float& eu, float& w, int& na,
+                                               double& r) {
+    r = exact_r(cx, cy, cz, sx, sy, sz);
     double nad = floor((r / k.v - k.t0) * k.fs);
     eu = (float)((r - k.v * (k.t0 + nad / k.fs)) / k.h);
     w = (float)((double)A * 0.5 * k.h / r);
@@ -181,7 +209,8 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
         p.w = A * (a.h2R * Tw);
         na = a.na;
     } else {
-        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, p.w, na);
+        double r_ex;
+        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, p.w, na, r_ex);
     }
     // In-window m satisfy alpha < m < beta (alpha = eu - ku, beta = eu + ku).
     // floor() without the XU pipe: for |x| < 2^22, (x + 1.5*2^23) rounds x to
@@ -209,7 +238,7 @@ __device__ __forceinline__ PairWin pair_setup(const Anchor& a, float4 kd, float 
         if (amb) {
             const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
             int cnt;
-            exact_window(r, n_lo, n_hi, k, n_lo, cnt);
+            exact_window(r, n_lo, n_hi, k, n_lo, cnt, k.ks);
             n_hi = n_lo + cnt - 1;
         } else {
             n_lo = max(n_lo, 0);
@@ -231,7 +260,7 @@ static __device__ __noinline__ PairWin pair_fix(PairWin p, float eu, int na, boo
     if (amb) {
         const double r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
         int cnt;
-        exact_window(r, n_lo, n_hi, k, n_lo, cnt);
+        exact_window(r, n_lo, n_hi, k, n_lo, cnt, k.ks);
         n_hi = n_lo + cnt - 1;
     } else {
         n_lo = max(n_lo, 0);
@@ -268,6 +297,71 @@ __device__ __forceinline__ PairWin pair_fast(const Anchor& a, float4 kd, float A
     const bool amb = fabsf(d) > 0.5f - GAMMA;
     if (amb || (unsigned)p.n_lo > (unsigned)(k.Nt - k.cnt_int))
         p = pair_fix(p, eu, a.na, amb, orig, gi, Mpad, sx, sy, sz, k.cnt_int, k);
+    return p;
+}
+
+// General per-pair setup (row f4; kernel path SER_GEN): per-kernel sigma_i
+// from ks4 = (k sigma_i / h, -log2(e) h^2 / (2 sigma_i^2), sigma_i, 0) and,
+// when k.nf, near pairs (r < near_threshold) skipped here: gpair_near.cu
+// evaluates them with both terms of Eq. 6.  Same window logic as
+// pair_setup<5> with the per-kernel half-width; ambiguous edges are decided
+// in fp64 against k sigma_i computed like the oracle's `k * s`.
+__device__ __forceinline__ PairWin pair_gen(const Anchor& a, float4 kd, float A, float4 ks4,
+                                            const float* __restrict__ orig, int64_t gi, int64_t Mpad, float sx,
+                                            float sy, float sz, const OpConst& k) {
+    PairWin p;
+    float eu;
+    int na;
+    double r = -1.0;
+    if (a.na != NA_EXACT) {
+        const float q = fmaf(a.Ux, kd.x, fmaf(a.Uy, kd.y, fmaf(a.Uz, kd.z, kd.w)));
+        const float eps = q * a.invR2;
+        float S = fmaf(eps, -21.f / 512.f, 7.f / 128.f);
+        S = fmaf(eps, S, -5.f / 64.f);
+        S = fmaf(eps, S, 1.f / 8.f);
+        S = fmaf(eps, S, -0.25f);
+        S = fmaf(eps, S, 1.f);
+        float Tw = fmaf(eps, 35.f / 128.f, -5.f / 16.f);
+        Tw = fmaf(eps, Tw, 3.f / 8.f);
+        Tw = fmaf(eps, Tw, -0.5f);
+        Tw = fmaf(eps, Tw, 1.f);
+        eu = fmaf(q * a.inv2Rh, S, a.Eu);
+        p.w = A * (a.h2R * Tw);
+        na = a.na;
+    } else {
+        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, p.w, na, r);
+        if (k.nf && r < near_threshold(kernel_ks(ks4.z, k), k)) {
+            p.cnt = 0;
+            p.n_lo = 0;
+            p.u_lo = 0.f;
+            return p;
+        }
+    }
+    const float alpha = eu - ks4.x;
+    const float ta = (alpha - 0.5f) + RND_MAGIC;
+    const float fla = ta - RND_MAGIC;
+    bool amb = fabsf((alpha - fla) - 0.5f) > 0.5f - GAMMA;
+    int n_lo = na + (__float_as_int(ta) - RND_MAGIC_BITS) + 1;
+    const float beta = eu + ks4.x;
+    const float tb = (beta - 0.5f) + RND_MAGIC;
+    amb = amb || fabsf((beta - (tb - RND_MAGIC)) - 0.5f) > 0.5f - GAMMA;
+    int n_hi = na + (__float_as_int(tb) - RND_MAGIC_BITS);
+    float u_lo = eu - (fla + 1.f);
+    if (amb || n_lo < 0 || n_hi > k.Nt - 1) {
+        if (amb) {
+            if (r < 0.0) r = exact_r(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz);
+            int cnt;
+            exact_window(r, n_lo, n_hi, k, n_lo, cnt, kernel_ks(ks4.z, k));
+            n_hi = n_lo + cnt - 1;
+        } else {
+            n_lo = max(n_lo, 0);
+            n_hi = min(n_hi, k.Nt - 1);
+        }
+        u_lo = eu - (float)(n_lo - na);
+    }
+    p.n_lo = n_lo;
+    p.cnt = max(n_hi - n_lo + 1, 0);
+    p.u_lo = u_lo;
     return p;
 }
 
@@ -318,7 +412,8 @@ __device__ __forceinline__ AssaPair assa_setup(const Anchor& a, float4 kd, float
         w = A * (a.h2R * Tw);
         na = a.na;
     } else {
-        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, w, na);
+        double r_ex;
+        exact_pair(orig[gi], orig[Mpad + gi], orig[2 * Mpad + gi], sx, sy, sz, A, k, eu, w, na, r_ex);
     }
     p.w = w * k.two_over_h;
     const float xa = fmaf((float)k.alpha, eu, 0.5f);

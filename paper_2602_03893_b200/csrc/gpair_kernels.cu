@@ -53,13 +53,16 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  float* __restrict__ partial, int32_t cpr, int32_t ncells,
-                                                 int32_t Lf, int64_t Mpad, OpConst k) {
+                                                 int32_t Lf, int64_t Mpad, OpConst k,
+                                                 const float4* __restrict__ ksig) {
+    constexpr bool GEN = SER == SER_GEN;
     extern __shared__ float4 smem4[];
     float4* s_kd = smem4;                                   // [STAGE_CELLS*32]
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
     float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
+    float4* s_ks = (float4*)(s_amp + STAGE_CELLS * CELL);   // [STAGE_CELLS*32] (GEN only)
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_acc = s_amp + STAGE_CELLS * CELL + (size_t)warp * Lf * 32;
+    float* s_acc = (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0)) + (size_t)warp * Lf * 32;
 
     const int region = blockIdx.x;
     const int jbase = (blockIdx.y * nw + warp) * 32;
@@ -80,6 +83,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             s_kd[t] = kd[(int64_t)cb * CELL + t];
             s_amp[t] = amp[(int64_t)cb * CELL + t];
+            if (GEN) s_ks[t] = ksig[(int64_t)cb * CELL + t];
         }
         if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
         __syncthreads();
@@ -93,14 +97,20 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                 const int li = gq * GROUP + t;
                 const int64_t gi = (int64_t)cb * CELL + li;
                 PairWin p;
-                if (SER == 0 && !gexact)
+                float K1 = k.K1u;
+                if (GEN) {
+                    const float4 ks4 = s_ks[li];
+                    p = pair_gen(a, kdg[t], ampg[t], ks4, orig, gi, Mpad, sx, sy, sz, k);
+                    K1 = ks4.y;
+                } else if (SER == 0 && !gexact) {
                     p = pair_fast(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
-                else
-                    p = pair_setup<SER == 0 ? 2 : SER>(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
+                } else {
+                    p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
+                }
                 if (p.cnt <= 0) continue;
                 float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
                 if (p.cnt == WMAX && (WMAX & 1) == 0) {  // common case: packed pairs, no predicates
-                    const f2_t K2 = pk2(k.K1u, k.K1u), W2 = pk2(p.w, p.w), step = pk2(-2.f, -2.f);
+                    const f2_t K2 = pk2(K1, K1), W2 = pk2(p.w, p.w), step = pk2(-2.f, -2.f);
                     f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
 #pragma unroll
                     for (int m = 0; m < WMAX; m += 2) {
@@ -117,13 +127,13 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                     for (int m = 0; m < WMAX; ++m) {
                         if (m < p.cnt) {
                             const float um = p.u_lo - (float)m;
-                            const float g = ex2f((um * k.K1u) * um);
+                            const float g = ex2f((um * K1) * um);
                             ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
                         }
                     }
                     for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
                         const float um = p.u_lo - (float)m;
-                        ap[m * 32] = fmaf(p.w * um, ex2f((um * k.K1u) * um), ap[m * 32]);
+                        ap[m * 32] = fmaf(p.w * um, ex2f((um * K1) * um), ap[m * 32]);
                     }
                 }
             }
@@ -162,7 +172,8 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
                                                 const int32_t* __restrict__ jlo_a, const int32_t* __restrict__ jlen_a,
                                                 int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
                                                 const float* __restrict__ b, float* __restrict__ delta,
-                                                double* __restrict__ loss_part) {
+                                                double* __restrict__ loss_part, const int32_t* __restrict__ near_row,
+                                                const double* __restrict__ ynear) {
     extern __shared__ double s_copy[];
     const int j = blockIdx.x;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -206,12 +217,14 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
     __syncthreads();
     double lsum = 0.0;
     const int64_t row = (int64_t)j * k.Nt;
+    const int nrow = near_row ? near_row[j] : -1;  // near-field rows (row f4, gpair_near.cu)
     for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
         double ys = 0.0;
         int t = n - jlo;
         if (t >= 0 && t < jlen) {
             for (int w = 0; w < nw; ++w) ys += s_copy[(size_t)w * jlen + t];
         }
+        if (nrow >= 0) ys += ynear[(int64_t)nrow * k.Nt + n];
         const float yv = (float)ys;
         if (y) y[row + n] = yv;
         if (b) {
@@ -284,7 +297,8 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  const float* __restrict__ resid, int32_t cpr, int32_t ncells,
                                                  int32_t La, int64_t Mpad, OpConst k, EpiParams ep,
-                                                 unsigned long long* count) {
+                                                 unsigned long long* count, const float4* __restrict__ ksig) {
+    constexpr bool GEN = SER == SER_GEN;
     extern __shared__ float4 smem4[];
     Anchor* s_anc = (Anchor*)smem4;                          // [nw][GPC][33]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -297,6 +311,9 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     const int64_t gi = (int64_t)cid * CELL + lane;
     float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
     if (cok) d4 = kd[gi];
+    float4 ks4 = make_float4(0.f, k.K1u, 0.f, 0.f);
+    if (GEN && cok) ks4 = ksig[gi];
+    const float K1 = ks4.y;
     const Anchor* my_anc = s_anc + (warp * GPC + lane / GROUP) * 33;
     float acc = 0.f;
     unsigned long long npairs = 0;
@@ -338,10 +355,12 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             const float4 sp = s_sen[jj];
             const Anchor a = my_anc[jj];
             PairWin p;
-            if (SER == 0 && a.na != NA_EXACT)
+            if (GEN)
+                p = pair_gen(a, d4, 1.f, ks4, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+            else if (SER == 0 && a.na != NA_EXACT)
                 p = pair_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             else
-                p = pair_setup<SER == 0 ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+                p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             if (p.cnt <= 0) continue;
             if (MODE == MODE_COUNT) {
                 npairs += real ? (unsigned long long)p.cnt : 0ull;
@@ -350,7 +369,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             const float* rp = s_res + jj * La + (p.n_lo - lo);
             float part = 0.f;
             if (p.cnt == WMAX && (WMAX & 1) == 0) {  // packed pairs, no predicates
-                const f2_t K2 = pk2(k.K1u, k.K1u), step = pk2(-2.f, -2.f);
+                const f2_t K2 = pk2(K1, K1), step = pk2(-2.f, -2.f);
                 f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
                 f2_t part2 = 0ull;
 #pragma unroll
@@ -366,13 +385,13 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
                 for (int m = 0; m < WMAX; ++m) {
                     if (m < p.cnt) {
                         const float um = p.u_lo - (float)m;
-                        const float g = ex2f((um * k.K1u) * um);
+                        const float g = ex2f((um * K1) * um);
                         part = fmaf(um * g, rp[m], part);
                     }
                 }
                 for (int m = WMAX; m < p.cnt; ++m) {
                     const float um = p.u_lo - (float)m;
-                    part = fmaf(um * ex2f((um * k.K1u) * um), rp[m], part);
+                    part = fmaf(um * ex2f((um * K1) * um), rp[m], part);
                 }
             }
             accb = fmaf(p.w, part, accb);
@@ -401,13 +420,14 @@ namespace {
 
 template <int W, int SER>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
-    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 + (size_t)c->f_warps * c->Lf * 32 * 4;
+    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 + (size_t)c->f_warps * c->Lf * 32 * 4 +
+                  (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0);
     cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->f_sgroups);
     k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
-                                                      c->Mpad, c->k);
+                                                      c->Mpad, c->k, c->d_ksig);
     return cudaGetLastError();
 }
 
@@ -420,7 +440,7 @@ cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cu
     int threads = 32 * std::max(c->a_cpr, 1);
     k_adjoint<W, SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                            c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
-                                                           c->k, ep, c->d_count);
+                                                           c->k, ep, c->d_count, c->d_ksig);
     return cudaGetLastError();
 }
 
@@ -439,8 +459,26 @@ cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep,
     }
 }
 
+// general operator (row f4): windows rounded up to 8 / 16 / 32 / 64 samples
+int pick_wmax_gen(int w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+
+template <int MODE>
+cudaError_t adj_dispatch_gen(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    switch (pick_wmax_gen(c->k.wmax)) {
+        case 8: return adj_launch<8, SER_GEN, MODE>(c, resid, ep, st);
+        case 16: return adj_launch<16, SER_GEN, MODE>(c, resid, ep, st);
+        case 32: return adj_launch<32, SER_GEN, MODE>(c, resid, ep, st);
+        default: return adj_launch<64, SER_GEN, MODE>(c, resid, ep, st);
+    }
+}
+
 template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    if constexpr (MODE != MODE_COUNT) {
+        if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
+    } else {
+        if (c->ser == SER_GEN) return cudaErrorNotSupported;
+    }
     return c->ser == 0 ? adj_dispatch2<0, MODE>(c, resid, ep, st)
                        : (c->ser == 2 ? adj_dispatch2<2, MODE>(c, resid, ep, st) : adj_dispatch2<5, MODE>(c, resid, ep, st));
 }
@@ -468,6 +506,14 @@ cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cu
 }
 
 cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
+    if (c->ser == SER_GEN) {
+        switch (pick_wmax_gen(c->k.wmax)) {
+            case 8: return fwd_launch<8, SER_GEN>(c, st);
+            case 16: return fwd_launch<16, SER_GEN>(c, st);
+            case 32: return fwd_launch<32, SER_GEN>(c, st);
+            default: return fwd_launch<64, SER_GEN>(c, st);
+        }
+    }
     return c->ser == 0 ? fwd_dispatch<0>(c, st) : (c->ser == 2 ? fwd_dispatch<2>(c, st) : fwd_dispatch<5>(c, st));
 }
 
@@ -478,7 +524,8 @@ cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, 
     cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_wlo_fT, c->d_jlo, c->d_jlen, c->f_regions, c->Lf,
-                                           c->k, y, b, delta, c->d_loss_part);
+                                           c->k, y, b, delta, c->d_loss_part, c->n_near ? c->d_near_row : nullptr,
+                                           c->d_ynear);
     return cudaGetLastError();
 }
 

@@ -28,10 +28,13 @@ namespace gpair {
 
 namespace {
 
-#define SETUP_CHECK(x)                          \
-    do {                                        \
-        cudaError_t e_ = (x);                   \
-        if (e_ != cudaSuccess) return e_;       \
+#define SETUP_CHECK(x)                                                   \
+    do {                                                                 \
+        cudaError_t e_ = (x);                                            \
+        if (e_ != cudaSuccess) {                                         \
+            if (why.empty()) why = "gpair_setup.cu:" + std::to_string(__LINE__); \
+            return e_;                                                   \
+        }                                                                \
     } while (0)
 
 __global__ void k_check_finite(const float* __restrict__ c, int64_t n, int* flag) {
@@ -172,7 +175,7 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
             R = sqrt(dx * dx + dy * dy + dz * dz);
         }
         if (check) {
-            if (!(R - (double)C.w > k.ks)) bad = 1;
+            if (!k.nf && !(R - (double)C.w > k.ks)) bad = 1;  // near field: any r > 0 (row f4)
             for (int gq = 0; gq < GPC; ++gq) {  // anchor-expansion bound per 8-kernel group
                 const float4 G = grp[(int64_t)cc * GPC + gq];
                 double gx = (double)G.x - sx, gy = (double)G.y - sy, gz = (double)G.z - sz;
@@ -240,6 +243,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     auto pol = thrust::cuda::par.on(st);
 
     SETUP_CHECK(dmalloc(c, &c->d_flags, 8));
+    SETUP_CHECK(dmalloc(c, &c->d_count, 1));
     SETUP_CHECK(cudaMemsetAsync(c->d_flags, 0, 8 * sizeof(int32_t), st));
     SETUP_CHECK(dmalloc(c, &c->d_sens, (size_t)3 * Nd));
     SETUP_CHECK(cudaMemcpyAsync(c->d_sens, sensors, sizeof(float) * 3 * Nd, cudaMemcpyDeviceToDevice, st));
@@ -325,6 +329,10 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     SETUP_CHECK(cudaGetLastError());
     cudaFree(keys);
     cudaFree(vals);
+    if (c->gen) {  // per-kernel sigma table and near-field pair lists (row f4, gpair_near.cu)
+        SETUP_CHECK(build_general(c, st, why, geom_err));
+        if (geom_err) return cudaSuccess;
+    }
 
     // ---- forward regions: sized for >= ~4 CTAs per SM of work and smem fit
     int dev_sms = 148;
@@ -359,10 +367,12 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->max_eps = me;
         c->series_small = me <= EPS_SMALL ? 1 : 0;
         c->ser = c->series_small ? ((c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int) ? 0 : 2) : 5;
+        if (c->gen) c->ser = SER_GEN;
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 15) / 16 * 16;  // the flush transposes 32-row blocks plus a 16-row tail
         size_t smem = c->assa ? assa_forward_smem(c, Lf)
-                              : (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * 20 + 8 * GPC * 16;
+                              : (size_t)c->f_warps * Lf * 32 * sizeof(float) + 8 * CELL * (c->gen ? 36 : 20) +
+                                    8 * GPC * 16;
         if (smem > smem_limit && cpr > 1) {
             cudaFree(wlo);
             cpr /= 2;
@@ -432,7 +442,6 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_delta, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_loss_part, Nd));
-    SETUP_CHECK(dmalloc(c, &c->d_count, 1));
     SETUP_CHECK(cudaStreamSynchronize(st));
     return cudaSuccess;
 }

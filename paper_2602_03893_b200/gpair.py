@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libgpair.so")
 OK, ERR_INVALID_ARGUMENT, ERR_GEOMETRY, ERR_RESOURCE, ERR_NUMERICAL, ERR_CUDA, ERR_NCCL = range(7)
 CHECK_FINITE = 1 << 9
 TOF_ASSA = 1
+NEAR_FIELD = 1 << 1
 PROF_NAMES = ["gather", "forward", "reduce", "allreduce", "residual", "adjoint", "loss", "vcr"]
 
 
@@ -87,6 +88,9 @@ class Info(ctypes.Structure):
         ("assa_alpha", ctypes.c_int32),
         ("assa_n_half", ctypes.c_int32),
         ("assa_K", ctypes.c_int32),
+        ("general", ctypes.c_int32),
+        ("near_rows", ctypes.c_int32),
+        ("near_pairs", ctypes.c_int64),
     ]
 
     def as_dict(self):
@@ -193,15 +197,18 @@ class Context:
     """One gpair_ctx (one rank / device).  Mirrors include/gpair.h."""
 
     def __init__(self, centers, sensors, *, sigma, v, fs, n_samples, t0=0.0, k=3.0, rank=0, world=1,
-                 nccl_comm=None, flags=0, assa=False, assa_nmin=25, stream=None):
+                 nccl_comm=None, flags=0, assa=False, assa_nmin=25, sigmas=None, near_field=False, stream=None):
+        """sigmas: optional CUDA float32 [M] per-kernel sigma_i (row f4);
+        near_field: Eq. 6 with both terms (GPAIR_NEAR_FIELD, row f4)."""
         self.M = int(centers.shape[1])
         self.Nd = int(sensors.shape[1])
         self.Nt = int(n_samples)
+        flags = int(flags) | (TOF_ASSA if assa else 0) | (NEAR_FIELD if near_field else 0)
         d = Desc(sound_speed=float(v), sampling_rate=float(fs), n_samples=self.Nt, t0=float(t0),
                  n_kernels=self.M, centers=_ptr(centers, numel=3 * self.M, name="centers"), sigma=float(sigma),
-                 sigmas=None, window_k=float(k), n_sensors=self.Nd,
+                 sigmas=_ptr(sigmas, numel=self.M, name="sigmas"), window_k=float(k), n_sensors=self.Nd,
                  sensors=_ptr(sensors, numel=3 * self.Nd, name="sensors"), rank=int(rank), world=int(world),
-                 nccl_comm=nccl_comm, flags=int(flags) | (TOF_ASSA if assa else 0), assa_nmin=int(assa_nmin))
+                 nccl_comm=nccl_comm, flags=flags, assa_nmin=int(assa_nmin))
         h = ctypes.c_void_p()
         st = lib().gpair_create(ctypes.byref(h), ctypes.byref(d), _stream(stream))
         _check(st, None)

@@ -86,9 +86,13 @@ def test_create_validates_before_touching_the_device(lib):
     d.n_samples = 0
     assert lib.gpair_create(ctypes.byref(h), ctypes.byref(d), None) == gpair.ERR_INVALID_ARGUMENT
     d.n_samples = 64
-    d.sigmas = 1
+    d.sigmas = 1  # per-kernel sigma (row f4) needs the exact operator, not ASSA
+    d.flags = gpair.TOF_ASSA
     assert lib.gpair_create(ctypes.byref(h), ctypes.byref(d), None) == gpair.ERR_INVALID_ARGUMENT
     d.sigmas = None
+    d.flags = gpair.TOF_ASSA | gpair.NEAR_FIELD
+    assert lib.gpair_create(ctypes.byref(h), ctypes.byref(d), None) == gpair.ERR_INVALID_ARGUMENT
+    d.flags = 0
     d.world = 2
     assert lib.gpair_create(ctypes.byref(h), ctypes.byref(d), None) == gpair.ERR_INVALID_ARGUMENT
     d.world = 1
