@@ -48,6 +48,52 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 #define GPAIR_FWD_UNROLL 1
 #endif
 constexpr int kFwdUnroll = GPAIR_FWD_UNROLL;  // unroll of the 8-kernel group loop
+
+// Accumulate one pair's WMAX in-window samples into its smem column (lane
+// stride 32): packed f32x2, no predicates (the common case).
+template <int WMAX>
+__device__ __forceinline__ void acc_packed(float* ap, float u_lo, float w, float K1) {
+    const f2_t K2 = pk2(K1, K1), W2 = pk2(w, w), step = pk2(-2.f, -2.f);
+    f2_t u2 = pk2(u_lo, u_lo - 1.f);
+#pragma unroll
+    for (int m = 0; m < WMAX; m += 2) {
+        f2_t acc2 = pk2(ap[m * 32], ap[(m + 1) * 32]);
+        acc2 = fma2(mul2(W2, u2), gauss2(u2, K2), acc2);
+        float v0, v1;
+        upk2(acc2, v0, v1);
+        ap[m * 32] = v0;
+        ap[(m + 1) * 32] = v1;
+        u2 = add2(u2, step);
+    }
+}
+
+// Any window length (clipped / exact-edge / general pairs).
+template <int WMAX>
+__device__ __forceinline__ void acc_generic(float* ap, float u_lo, float w, float K1, int cnt) {
+#pragma unroll
+    for (int m = 0; m < WMAX; ++m) {
+        if (m < cnt) {
+            const float um = u_lo - (float)m;
+            const float g = ex2f((um * K1) * um);
+            ap[m * 32] = fmaf(w * um, g, ap[m * 32]);
+        }
+    }
+    for (int m = WMAX; m < cnt; ++m) {  // only if an exact window exceeds WMAX
+        const float um = u_lo - (float)m;
+        ap[m * 32] = fmaf(w * um, ex2f((um * K1) * um), ap[m * 32]);
+    }
+}
+
+template <int WMAX>
+__device__ __forceinline__ void acc_pair(float* s_acc_lane, int lo_j, const PairWin& p, float K1) {
+    if (p.cnt <= 0) return;
+    float* ap = s_acc_lane + (p.n_lo - lo_j) * 32;
+    if (p.cnt == WMAX && (WMAX & 1) == 0)
+        acc_packed<WMAX>(ap, p.u_lo, p.w, K1);
+    else
+        acc_generic<WMAX>(ap, p.u_lo, p.w, K1, p.cnt);
+}
+
 template <int WMAX, int SER>
 __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
@@ -56,13 +102,19 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                                  int32_t Lf, int64_t Mpad, OpConst k,
                                                  const float4* __restrict__ ksig) {
     constexpr bool GEN = SER == SER_GEN;
+    constexpr bool FAST = SER == 0;  // two pairs per setup in f32x2 (common configuration)
     extern __shared__ float4 smem4[];
-    float4* s_kd = smem4;                                   // [STAGE_CELLS*32]
+    float4* s_kd = smem4;                                   // [STAGE_CELLS*32] (FAST: SoA x, y, z, |d|^2)
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
     float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
     float4* s_ks = (float4*)(s_amp + STAGE_CELLS * CELL);   // [STAGE_CELLS*32] (GEN only)
+    float* s_kx = (float*)s_kd;                             // FAST SoA views
+    float* s_ky = s_kx + STAGE_CELLS * CELL;
+    float* s_kz = s_ky + STAGE_CELLS * CELL;
+    float* s_kw = s_kz + STAGE_CELLS * CELL;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_acc = (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0)) + (size_t)warp * Lf * 32;
+    float* s_acc_lane = s_acc + lane;
 
     const int region = blockIdx.x;
     const int jbase = (blockIdx.y * nw + warp) * 32;
@@ -81,7 +133,15 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         const int nc = min(STAGE_CELLS, c1 - cb);
         __syncthreads();
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            s_kd[t] = kd[(int64_t)cb * CELL + t];
+            const float4 v = kd[(int64_t)cb * CELL + t];
+            if (FAST) {
+                s_kx[t] = v.x;
+                s_ky[t] = v.y;
+                s_kz[t] = v.z;
+                s_kw[t] = v.w;
+            } else {
+                s_kd[t] = v;
+            }
             s_amp[t] = amp[(int64_t)cb * CELL + t];
             if (GEN) s_ks[t] = ksig[(int64_t)cb * CELL + t];
         }
@@ -89,7 +149,72 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         __syncthreads();
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
-            const bool gexact = SER == 0 && __any_sync(__activemask(), a.na == NA_EXACT);
+            if constexpr (FAST) {
+                if (!__any_sync(__activemask(), a.na == NA_EXACT)) {
+                    // Two pairs per step: pair_fast's arithmetic in f32x2 (bit-identical
+                    // results), the anchor's per-lane scalars broadcast to both halves.
+                    const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
+                    const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
+                    const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R), clo = pk2(k.c_lo, k.c_lo);
+                    const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
+                    const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
+                    const f2_t mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
+                    const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // n_lo - lo_j = bits(t) + nrel
+                    const unsigned span = (unsigned)(k.Nt - k.cnt_int);
+#pragma unroll 1
+                    for (int t = 0; t < GROUP; t += 2) {
+                        const int li = gq * GROUP + t;
+                        const f2_t kx = *(const f2_t*)(s_kx + li), ky = *(const f2_t*)(s_ky + li);
+                        const f2_t kz = *(const f2_t*)(s_kz + li), kw = *(const f2_t*)(s_kw + li);
+                        const f2_t A2 = *(const f2_t*)(s_amp + li);
+                        const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
+                        const f2_t eps = mul2(q, iR2);
+                        const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
+                        const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                        const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
+                        const f2_t w = mul2(A2, mul2(h2R, Tw));
+                        const f2_t x = add2(eu, clo);
+                        const f2_t tt = add2(x, mag);
+                        const f2_t fl = add2(tt, nmag);
+                        const f2_t d = sub2(x, fl);
+                        const f2_t ulo = sub2(eu, add2(fl, one));
+                        float d0, d1, t0, t1, u0, u1, w0, w1;
+                        upk2(d, d0, d1);
+                        upk2(tt, t0, t1);
+                        upk2(ulo, u0, u1);
+                        upk2(w, w0, w1);
+                        const int n0 = __float_as_int(t0) + nrel, n1 = __float_as_int(t1) + nrel;
+                        const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
+                        const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
+                        if (!(bad0 || bad1)) {
+                            acc_packed<WMAX>(s_acc_lane + n0 * 32, u0, w0, k.K1u);
+                            acc_packed<WMAX>(s_acc_lane + n1 * 32, u1, w1, k.K1u);
+                        } else {  // rare: exact window edges and/or record clipping
+                            float e0, e1;
+                            upk2(eu, e0, e1);
+                            const int64_t gi = (int64_t)cb * CELL + li;
+                            PairWin p;
+                            p.w = w0;
+                            p.n_lo = n0 + lo_j;
+                            p.u_lo = u0;
+                            p.cnt = k.cnt_int;
+                            if (bad0)
+                                p = pair_fix(p, e0, a.na, fabsf(d0) > 0.5f - GAMMA, orig, gi, Mpad, sx, sy, sz,
+                                             k.cnt_int, k);
+                            acc_pair<WMAX>(s_acc_lane, lo_j, p, k.K1u);
+                            p.w = w1;
+                            p.n_lo = n1 + lo_j;
+                            p.u_lo = u1;
+                            p.cnt = k.cnt_int;
+                            if (bad1)
+                                p = pair_fix(p, e1, a.na, fabsf(d1) > 0.5f - GAMMA, orig, gi + 1, Mpad, sx, sy, sz,
+                                             k.cnt_int, k);
+                            acc_pair<WMAX>(s_acc_lane, lo_j, p, k.K1u);
+                        }
+                    }
+                    continue;
+                }
+            }
             const float4* kdg = s_kd + gq * GROUP;
             const float* ampg = s_amp + gq * GROUP;
 #pragma unroll kFwdUnroll
@@ -98,44 +223,15 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                 const int64_t gi = (int64_t)cb * CELL + li;
                 PairWin p;
                 float K1 = k.K1u;
+                const float4 kdt = FAST ? make_float4(s_kx[li], s_ky[li], s_kz[li], s_kw[li]) : kdg[t];
                 if (GEN) {
                     const float4 ks4 = s_ks[li];
-                    p = pair_gen(a, kdg[t], ampg[t], ks4, orig, gi, Mpad, sx, sy, sz, k);
+                    p = pair_gen(a, kdt, ampg[t], ks4, orig, gi, Mpad, sx, sy, sz, k);
                     K1 = ks4.y;
-                } else if (SER == 0 && !gexact) {
-                    p = pair_fast(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
                 } else {
-                    p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, kdg[t], ampg[t], orig, gi, Mpad, sx, sy, sz, k);
+                    p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, kdt, ampg[t], orig, gi, Mpad, sx, sy, sz, k);
                 }
-                if (p.cnt <= 0) continue;
-                float* ap = s_acc + (p.n_lo - lo_j) * 32 + lane;
-                if (p.cnt == WMAX && (WMAX & 1) == 0) {  // common case: packed pairs, no predicates
-                    const f2_t K2 = pk2(K1, K1), W2 = pk2(p.w, p.w), step = pk2(-2.f, -2.f);
-                    f2_t u2 = pk2(p.u_lo, p.u_lo - 1.f);
-#pragma unroll
-                    for (int m = 0; m < WMAX; m += 2) {
-                        f2_t acc2 = pk2(ap[m * 32], ap[(m + 1) * 32]);
-                        acc2 = fma2(mul2(W2, u2), gauss2(u2, K2), acc2);
-                        float v0, v1;
-                        upk2(acc2, v0, v1);
-                        ap[m * 32] = v0;
-                        ap[(m + 1) * 32] = v1;
-                        u2 = add2(u2, step);
-                    }
-                } else {
-#pragma unroll
-                    for (int m = 0; m < WMAX; ++m) {
-                        if (m < p.cnt) {
-                            const float um = p.u_lo - (float)m;
-                            const float g = ex2f((um * K1) * um);
-                            ap[m * 32] = fmaf(p.w * um, g, ap[m * 32]);
-                        }
-                    }
-                    for (int m = WMAX; m < p.cnt; ++m) {  // only if an exact window exceeds WMAX
-                        const float um = p.u_lo - (float)m;
-                        ap[m * 32] = fmaf(p.w * um, ex2f((um * K1) * um), ap[m * 32]);
-                    }
-                }
+                acc_pair<WMAX>(s_acc_lane, lo_j, p, K1);
             }
         }
     }
