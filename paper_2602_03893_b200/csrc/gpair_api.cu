@@ -20,6 +20,42 @@ namespace {
 
 thread_local std::string g_static_err;
 
+// Table of the factorised-Gaussian fast path (gpair_internal.cuh TabConst):
+// c_i = exp2(K m^2) and d_i = -m c_i, m = i - W/2, in fp64 with
+// K = -log2(e) h^2 / (2 sigma^2), each rounded once to fp32.  A table error is
+// SYSTEMATIC (the same at window position m for every pair) and dense
+// amplitudes cancel strongly in y, so the entries are kept at full fp32
+// precision (a 20-bit table measured 1e-3 elementwise at cfg4).  Enabled for
+// full windows of W = cnt_int samples with W % 4 == 0 and TAB_MIN <= W <=
+// TAB_MAX (the per-pair chain then spans |m| <= 16);
+// GPAIR_NO_TAB=1 in the environment keeps the per-sample MUFU path (A/B runs).
+void build_tab(gpair_ctx* c) {
+    gpair::TabConst t{};
+    const gpair::OpConst& k = c->k;
+    const int W = k.cnt_int;
+    const char* off = std::getenv("GPAIR_NO_TAB");
+    t.on = (W >= gpair::TAB_MIN && W % 4 == 0 && W <= gpair::TAB_MAX && !k.gen && !(off && off[0] == '1')) ? 1 : 0;
+    t.K = k.K1u;
+    t.m2K = -2.0f * k.K1u;
+    t.kappa = (float)(-2.0 * (double)k.K1u * 0.6931471805599453);
+    if (t.on) {
+        const int C = W / 2;
+        const double Kd = -1.4426950408889634 * k.h * k.h / (2.0 * k.sigma * k.sigma);
+        float cf[gpair::TAB_MAX], df[gpair::TAB_MAX];
+        for (int i = 0; i < W; ++i) {
+            const int m = i - C;
+            const double cv = std::exp2(Kd * (double)m * (double)m);
+            cf[i] = (float)cv;                 // each entry rounded once from fp64:
+            df[i] = (float)(-(double)m * cv);  // the table's error is common to every pair
+        }
+        for (int i = 0; i < W; i += 2) {
+            t.c2[i / 2] = ((gpair::f2_t)__builtin_bit_cast(uint32_t, cf[i + 1]) << 32) | __builtin_bit_cast(uint32_t, cf[i]);
+            t.d2[i / 2] = ((gpair::f2_t)__builtin_bit_cast(uint32_t, df[i + 1]) << 32) | __builtin_bit_cast(uint32_t, df[i]);
+        }
+    }
+    c->tab = t;
+}
+
 // ---------------------------------------------------------------- NCCL (dlopen)
 typedef int nccl_res_t;
 struct nccl_uid_t {
@@ -326,6 +362,7 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
         return cuda_fail(nullptr, e, "cudaGetDevice");
     }
     c->k = k;
+    build_tab(c);
     c->M = d->n_kernels;
     c->Nd = d->n_sensors;
     c->Nt = d->n_samples;

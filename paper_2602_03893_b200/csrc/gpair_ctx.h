@@ -16,6 +16,7 @@ struct GpairEventPair {
 struct gpair_ctx_s {
     int device = 0;
     gpair::OpConst k{};
+    gpair::TabConst tab{};  // factorised-Gaussian table of the TAB fast path (on = 0: per-sample MUFU path)
     int64_t M = 0, Mpad = 0;
     int32_t ncells = 0, Nd = 0, Nt = 0;
     int32_t rank = 0, world = 1;

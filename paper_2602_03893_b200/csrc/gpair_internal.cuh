@@ -521,4 +521,84 @@ __device__ __forceinline__ f2_t gauss2(f2_t u2, f2_t K2) {
     return pk2(ex2f(a0), ex2f(a1));
 }
 
+// ---- factorised Gaussian window ("TAB" fast path).
+// For a full window of W = cnt_int samples (W % 4 == 0, W <= 32) centred at
+// i = C = W/2, u_i = u_c - m with m = i - C and u_c = u_lo - C in (-1, 0):
+//
+//   u_i exp2(K u_i^2) = exp2(K u_c^2) * exp2(-2 K u_c)^m * [exp2(K m^2) (u_c - m)]
+//                     =       E       *        r^m       *      Q_m(u_c)
+//
+// Q_m = fma(u_c, c_m, d_m) with the per-operator table c_m = exp2(K m^2),
+// d_m = -m c_m (fp64 on the host, each rounded to fp32), i.e. Q_m = c_m (u_c - m).  r^m is a
+// geometric chain from the centre (up by r, down by s = 1/r = exp2(2 K u_c)),
+// so per pair there are 3 MUFU.EX2 (E, r, s) instead of W, and per sample one
+// FFMA (Q), one FMUL (chain) and one FFMA (accumulate), all in f32x2.
+//
+// r and s multiply into every sample at |m| > 0 (r^m), so a BIASED error in
+// them becomes an even-shaped systematic error that the strongly cancelling
+// sums of y do not average away (measured: MUFU.EX2 for r, s gave 4e-4
+// elementwise at cfg4).  They are therefore evaluated as e^{+-x} =
+// C(x^2) +- x S(x^2), x = -2 K ln2 u_c in (-kappa, 0), kappa = -2 K ln2 <= 0.25
+// for W >= TAB_MIN, with the Taylor polynomials to x^7 (truncation < 4e-10),
+// i.e. to fp32 rounding.  E multiplies the whole pulse and keeps MUFU.EX2.
+constexpr int TAB_MIN = 12;
+constexpr int TAB_MAX = 32;
+struct TabConst {
+    f2_t c2[TAB_MAX / 2];  // (c_i, c_{i+1}), i even, i = 0..W-1 (sample index in the window)
+    f2_t d2[TAB_MAX / 2];  // (d_i, d_{i+1}) = -(i - C) c_i
+    float m2K;             // -2 K1u
+    float K;               // K1u
+    float kappa;           // -2 K1u ln 2
+    int32_t on;            // 1: cnt_int == W, W % 4 == 0, TAB_MIN <= W <= TAB_MAX, degree-2 series path
+};
+
+// r = exp2(-2 K u_c), s = 1 / r for two pairs (f32x2)
+__device__ __forceinline__ void tab_rs(f2_t uc, const TabConst& t, f2_t& r, f2_t& s) {
+    const f2_t x = mul2(uc, pk2(t.kappa, t.kappa));
+    const f2_t y = mul2(x, x);
+    f2_t C = fma2(y, pk2(1.f / 720.f, 1.f / 720.f), pk2(1.f / 24.f, 1.f / 24.f));
+    C = fma2(y, C, pk2(0.5f, 0.5f));
+    C = fma2(y, C, pk2(1.f, 1.f));
+    f2_t S = fma2(y, pk2(1.f / 5040.f, 1.f / 5040.f), pk2(1.f / 120.f, 1.f / 120.f));
+    S = fma2(y, S, pk2(1.f / 6.f, 1.f / 6.f));
+    S = fma2(y, S, pk2(1.f, 1.f));
+    const f2_t xS = mul2(x, S);
+    r = add2(C, xS);
+    s = sub2(C, xS);
+}
+
+// Forward accumulate of one pair's W samples into its smem column (lane stride
+// 32; ap points at sample n_lo).  P0 = w E; r, s = exp2(-/+2 K u_c).
+template <int W>
+__device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, float s, const TabConst& t) {
+    constexpr int C = W / 2;
+    const f2_t U = pk2(uc, uc);
+    f2_t P = pk2(P0, P0 * r);  // (P_0, P_1)
+    const float r2 = r * r;
+#pragma unroll
+    for (int i = C; i < W; i += 2) {
+        const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
+        f2_t acc2 = pk2(ap[i * 32], ap[(i + 1) * 32]);
+        acc2 = fma2(P, Q, acc2);
+        float v0, v1;
+        upk2(acc2, v0, v1);
+        ap[i * 32] = v0;
+        ap[(i + 1) * 32] = v1;
+        P = mul2(P, pk2(r2, r2));
+    }
+    const float s2 = s * s;
+    f2_t Pd = pk2(P0 * s2, P0 * s);  // (P_-2, P_-1)
+#pragma unroll
+    for (int i = C - 2; i >= 0; i -= 2) {
+        const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
+        f2_t acc2 = pk2(ap[i * 32], ap[(i + 1) * 32]);
+        acc2 = fma2(Pd, Q, acc2);
+        float v0, v1;
+        upk2(acc2, v0, v1);
+        ap[i * 32] = v0;
+        ap[(i + 1) * 32] = v1;
+        Pd = mul2(Pd, pk2(s2, s2));
+    }
+}
+
 }  // namespace gpair

@@ -100,9 +100,11 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  float* __restrict__ partial, int32_t cpr, int32_t ncells,
                                                  int32_t Lf, int64_t Mpad, OpConst k,
-                                                 const float4* __restrict__ ksig) {
+                                                 const float4* __restrict__ ksig, const TabConst tab) {
     constexpr bool GEN = SER == SER_GEN;
     constexpr bool FAST = SER == 0;  // two pairs per setup in f32x2 (common configuration)
+    // factorised Gaussian (TabConst): 3 MUFU per pair instead of WMAX
+    constexpr bool TABW = FAST && (WMAX % 4 == 0) && WMAX >= TAB_MIN && WMAX <= TAB_MAX;
     extern __shared__ float4 smem4[];
     float4* s_kd = smem4;                                   // [STAGE_CELLS*32] (FAST: SoA x, y, z, |d|^2)
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
@@ -187,8 +189,23 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                         const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
                         const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
                         if (!(bad0 || bad1)) {
-                            acc_packed<WMAX>(s_acc_lane + n0 * 32, u0, w0, k.K1u);
-                            acc_packed<WMAX>(s_acc_lane + n1 * 32, u1, w1, k.K1u);
+                            if (TABW && tab.on) {
+                                // u_c = u_lo - C (exact), E = exp2(K u_c^2), r = exp2(-2K u_c), s = 1/r
+                                const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
+                                f2_t r2, s2;
+                                tab_rs(uc, tab, r2, s2);
+                                float e0, e1, uc0, uc1, p0, p1, r0, r1, q0, q1;
+                                upk2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), e0, e1);
+                                upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), p0, p1);
+                                upk2(uc, uc0, uc1);
+                                upk2(r2, r0, r1);
+                                upk2(s2, q0, q1);
+                                acc_tab<TABW ? WMAX : 4>(s_acc_lane + n0 * 32, uc0, p0, r0, q0, tab);
+                                acc_tab<TABW ? WMAX : 4>(s_acc_lane + n1 * 32, uc1, p1, r1, q1, tab);
+                            } else {
+                                acc_packed<WMAX>(s_acc_lane + n0 * 32, u0, w0, k.K1u);
+                                acc_packed<WMAX>(s_acc_lane + n1 * 32, u1, w1, k.K1u);
+                            }
                         } else {  // rare: exact window edges and/or record clipping
                             float e0, e1;
                             upk2(eu, e0, e1);
@@ -523,7 +540,7 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
     dim3 grid(c->f_regions, c->f_sgroups);
     k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
-                                                      c->Mpad, c->k, c->d_ksig);
+                                                      c->Mpad, c->k, c->d_ksig, c->tab);
     return cudaGetLastError();
 }
 
