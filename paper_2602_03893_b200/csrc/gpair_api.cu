@@ -160,9 +160,8 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_orig);
     cudaFree(c->d_perm);
     cudaFree(c->d_wlo_f);
-    cudaFree(c->d_wlo_fT);
-    cudaFree(c->d_jlo);
-    cudaFree(c->d_jlen);
+    cudaFree(c->d_rent);
+    cudaFree(c->d_rchunk);
     cudaFree(c->d_partial);
     cudaFree(c->d_wlo_a);
     cudaFree(c->d_amp);

@@ -276,86 +276,64 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
 }
 
 // ------------------------------------------------------------------ reduce
-// One CTA per sensor j.  Warp w sums regions w, w+nw, ... into its private
-// shared-memory copy of the sensor's live range; copies are then summed in
-// warp order (deterministic).  Optionally fuses the residual and loss.
-constexpr int RED_BATCH = 8;  // regions in flight per warp (x Lf/32 loads each); Lf <= 128
+// Gather reducer: one warp per (sensor j, 32-sample chunk c), lane = sample
+// n = 32c + lane.  The region partials of sensor j whose windows [lo, lo + Lf)
+// meet the chunk are a contiguous range of the per-sensor list sorted by lo
+// (built at create, gpair_setup.cu); each is read once, coalesced, and summed
+// in fp64 registers in the list order (deterministic, no atomics, no smem).
+// Fuses the near-field rows, y, the residual delta = y - b and one fp64 loss
+// partial per warp.
+constexpr int RED_U = 8;  // partial loads in flight per warp
 
-__global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int32_t* __restrict__ wloT,
-                                                const int32_t* __restrict__ jlo_a, const int32_t* __restrict__ jlen_a,
-                                                int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
+__global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int2* __restrict__ ent,
+                                                const int2* __restrict__ bounds, int32_t nregions, int32_t Lf,
+                                                int32_t nchunks, OpConst k, float* __restrict__ y,
                                                 const float* __restrict__ b, float* __restrict__ delta,
                                                 double* __restrict__ loss_part, const int32_t* __restrict__ near_row,
                                                 const double* __restrict__ ynear) {
-    extern __shared__ double s_copy[];
-    const int j = blockIdx.x;
-    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jlo = jlo_a[j], jlen = jlen_a[j];
-    double* mine = s_copy + (size_t)warp * jlen;
-    for (int t = lane; t < jlen; t += 32) mine[t] = 0.0;
-    __syncwarp();
-    // Warp w owns the contiguous region block [r_beg, r_end): one coalesced load
-    // brings 32 window starts, then RED_BATCH regions x Lf/32 values per lane are
-    // loaded before any is accumulated (memory-level parallelism).
-    const int32_t* wl = wloT + (int64_t)j * nregions;
-    const int per_warp = (nregions + nw - 1) / nw;
-    const int r_beg = warp * per_warp, r_end = min(r_beg + per_warp, nregions);
-    const size_t rstride = (size_t)Lf;
-    const float* pj = partial + (size_t)j * nregions * Lf + lane;
-    for (int r0 = r_beg; r0 < r_end; r0 += 32) {
-        const int my_lo = (r0 + lane < r_end) ? wl[r0 + lane] : -1;
-        const int nr = min(32, r_end - r0);
-        for (int q0 = 0; q0 < Lf; q0 += 128)
-        for (int u0 = 0; u0 < nr; u0 += RED_BATCH) {
-            int lo[RED_BATCH];
-            float val[RED_BATCH][4];
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (wid >= (int64_t)k.Nd * nchunks) return;
+    const int j = (int)(wid / nchunks), c = (int)(wid - (int64_t)j * nchunks);
+    const int n = 32 * c + lane;
+    const int2 bd = bounds[wid];
+    const int2* e = ent + (int64_t)j * nregions;
+    const float* pj = partial + (size_t)j * nregions * Lf;
+    double acc = 0.0;
+    for (int k0 = bd.x; k0 < bd.y; k0 += 32) {
+        const int cnt = min(32, bd.y - k0);
+        const int2 my = lane < cnt ? e[k0 + lane] : make_int2(-(1 << 30), 0);
+        for (int u = 0; u < cnt; u += RED_U) {
+            float v[RED_U];
 #pragma unroll
-            for (int u = 0; u < RED_BATCH; ++u) {
-                lo[u] = __shfl_sync(0xffffffffu, my_lo, (u0 + u) & 31);
-                if (u0 + u >= nr) lo[u] = -1;
-                const float* src = pj + (size_t)(r0 + u0 + u) * rstride + q0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) val[u][q] = (lo[u] >= 0 && q0 + q * 32 + lane < Lf) ? src[q * 32] : 0.f;
+            for (int q = 0; q < RED_U; ++q) {
+                const int lo = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
+                const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
+                const int t = n - lo;
+                v[q] = (u + q < cnt && (unsigned)t < (unsigned)Lf) ? pj[(size_t)r * Lf + t] : 0.f;
             }
 #pragma unroll
-            for (int u = 0; u < RED_BATCH; ++u) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int n = lo[u] + q0 + q * 32 + lane;
-                    if (lo[u] >= 0 && q0 + q * 32 + lane < Lf && n < k.Nt) mine[n - jlo] += (double)val[u][q];
-                }
-            }
+            for (int q = 0; q < RED_U; ++q) acc += (double)v[q];
         }
     }
-    __syncthreads();
     double lsum = 0.0;
-    const int64_t row = (int64_t)j * k.Nt;
-    const int nrow = near_row ? near_row[j] : -1;  // near-field rows (row f4, gpair_near.cu)
-    for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
-        double ys = 0.0;
-        int t = n - jlo;
-        if (t >= 0 && t < jlen) {
-            for (int w = 0; w < nw; ++w) ys += s_copy[(size_t)w * jlen + t];
+    if (n < k.Nt) {
+        const int64_t idx = (int64_t)j * k.Nt + n;
+        if (near_row) {  // near-field rows (row f4, gpair_near.cu)
+            const int nrow = near_row[j];
+            if (nrow >= 0) acc += ynear[(int64_t)nrow * k.Nt + n];
         }
-        if (nrow >= 0) ys += ynear[(int64_t)nrow * k.Nt + n];
-        const float yv = (float)ys;
-        if (y) y[row + n] = yv;
+        const float yv = (float)acc;
+        if (y) y[idx] = yv;
         if (b) {
-            float dv = yv - b[row + n];
-            delta[row + n] = dv;
-            lsum += (double)dv * (double)dv;
+            const float dv = yv - b[idx];
+            delta[idx] = dv;
+            lsum = (double)dv * (double)dv;
         }
     }
     if (b) {
-        __shared__ double s_red[32];
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-        if (lane == 0) s_red[warp] = lsum;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < nw; ++w) s += s_red[w];
-            loss_part[j] = s;
-        }
+        if (lane == 0) loss_part[wid] = lsum;
     }
 }
 
@@ -894,25 +872,23 @@ cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
 }
 
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {
-    int nw = 8;
-    while (nw > 1 && (size_t)nw * c->jlen_max * 8 > 200 * 1024) nw /= 2;
-    size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_wlo_fT, c->d_jlo, c->d_jlen, c->f_regions, c->Lf,
-                                           c->k, y, b, delta, c->d_loss_part, c->n_near ? c->d_near_row : nullptr,
-                                           c->d_ynear);
+    const int64_t warps = (int64_t)c->Nd * c->nchunks;
+    k_reduce<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(c->d_partial, c->d_rent, c->d_rchunk, c->f_regions, c->Lf,
+                                                         c->nchunks, c->k, y, b, delta, c->d_loss_part,
+                                                         c->n_near ? c->d_near_row : nullptr, c->d_ynear);
+    if (b) c->n_loss_part = (int32_t)warps;
     return cudaGetLastError();
 }
 
 cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st) {
     k_residual<<<c->Nd, 256, 0, st>>>(y, b, c->Nt, delta, c->d_loss_part);
+    c->n_loss_part = c->Nd;
     return cudaGetLastError();
 }
 
 cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st, const double* reg_part, int32_t n_reg,
                         double lam) {
-    k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->Nd, 1.0 / ((double)c->Nd * (double)c->Nt), reg_part,
+    k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->n_loss_part, 1.0 / ((double)c->Nd * (double)c->Nt), reg_part,
                                reg_part ? n_reg : 0, lam, loss_out);
     return cudaGetLastError();
 }

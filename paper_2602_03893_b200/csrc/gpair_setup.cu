@@ -199,30 +199,46 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
     }
 }
 
-// Thread per sensor: live range of the forward partial windows (reducer) and
-// the transposed window table.
-__global__ void k_reducer_tables(const int32_t* __restrict__ wlo, int32_t nregions, int32_t Nd,
-                                 int32_t Nt, int32_t Lf, int32_t* wloT, int32_t* jlo, int32_t* jlen,
-                                 int* jlen_max) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= Nd) return;
-    int lo = INT_MAX, hi = INT_MIN;
-    for (int r = 0; r < nregions; ++r) {
-        int a = wlo[(int64_t)r * Nd + j];
-        wloT[(int64_t)j * nregions + r] = a;
-        if (a >= 0) {
-            lo = min(lo, a);
-            hi = max(hi, min(a + Lf - 1, Nt - 1));
-        }
+// Reducer tables (gather reducer, gpair_kernels.cu k_reduce): per sensor j
+// the forward regions sorted by window start, as (lo, region) entries, and per
+// 32-sample chunk c the range of entries whose window [lo, lo + Lf) meets
+// [32c, 32c + 32).  Regions with an empty window (lo = -1) sort first and are
+// excluded by the chunk ranges.
+__global__ void k_reducer_keys(const int32_t* __restrict__ wlo, int32_t nregions, int32_t Nd, int32_t Nt,
+                               uint32_t* keys, int32_t* vals) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nregions * Nd) return;
+    const int32_t r = (int32_t)(idx / Nd), j = (int32_t)(idx - (int64_t)r * Nd);
+    keys[idx] = (uint32_t)j * (uint32_t)(Nt + 1) + (uint32_t)(wlo[idx] + 1);
+    vals[idx] = r;
+}
+
+__global__ void k_reducer_entries(const uint32_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                                  int32_t nregions, int32_t Nd, int32_t Nt, int2* ent) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)nregions * Nd) return;
+    const uint32_t j = (uint32_t)(idx / nregions);
+    ent[idx] = make_int2((int32_t)(keys[idx] - j * (uint32_t)(Nt + 1)) - 1, vals[idx]);
+}
+
+__device__ __forceinline__ int lower_bound_lo(const int2* e, int n, int v) {
+    int a = 0, b = n;
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        if (e[m].x < v) a = m + 1; else b = m;
     }
-    if (lo > hi) {
-        jlo[j] = 0;
-        jlen[j] = 0;
-    } else {
-        jlo[j] = lo;
-        jlen[j] = hi - lo + 1;
-        atomicMax(jlen_max, hi - lo + 1);
-    }
+    return a;
+}
+
+__global__ void k_reducer_chunks(const int2* __restrict__ ent, int32_t nregions, int32_t Nd, int32_t nchunks,
+                                 int32_t Lf, int2* bounds) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)Nd * nchunks) return;
+    const int32_t j = (int32_t)(idx / nchunks), c = (int32_t)(idx - (int64_t)j * nchunks);
+    const int2* e = ent + (int64_t)j * nregions;
+    const int beg = lower_bound_lo(e, nregions, max(0, 32 * c - Lf + 1));
+    const int end = lower_bound_lo(e, nregions, 32 * c + 32);
+    bounds[idx] = make_int2(beg, max(beg, end));
 }
 
 template <class T>
@@ -391,14 +407,32 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->workspace_bytes += sizeof(int32_t) * (int64_t)nreg * Nd;
         break;
     }
-    // reducer tables
-    SETUP_CHECK(dmalloc(c, &c->d_wlo_fT, (size_t)c->f_regions * Nd));
-    SETUP_CHECK(dmalloc(c, &c->d_jlo, Nd));
-    SETUP_CHECK(dmalloc(c, &c->d_jlen, Nd));
-    SETUP_CHECK(cudaMemsetAsync(c->d_flags + 5, 0, sizeof(int32_t), st));
-    k_reducer_tables<<<(Nd + 127) / 128, 128, 0, st>>>(c->d_wlo_f, c->f_regions, Nd, c->Nt, c->Lf,
-                                                       c->d_wlo_fT, c->d_jlo, c->d_jlen, c->d_flags + 5);
-    SETUP_CHECK(cudaGetLastError());
+    // reducer tables (sorted window starts per sensor, chunk ranges)
+    {
+        const int64_t nt = (int64_t)c->f_regions * Nd;
+        uint32_t* keys = nullptr;
+        int32_t* vals = nullptr;
+        SETUP_CHECK(cudaMalloc(&keys, sizeof(uint32_t) * (size_t)nt));
+        SETUP_CHECK(cudaMalloc(&vals, sizeof(int32_t) * (size_t)nt));
+        k_reducer_keys<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(c->d_wlo_f, c->f_regions, Nd, c->Nt, keys, vals);
+        SETUP_CHECK(cudaGetLastError());
+        thrust::device_ptr<uint32_t> kp(keys);
+        thrust::device_ptr<int32_t> vp(vals);
+        thrust::stable_sort_by_key(pol, kp, kp + nt, vp);
+        SETUP_CHECK(dmalloc(c, &c->d_rent, (size_t)nt));
+        k_reducer_entries<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(keys, vals, c->f_regions, Nd, c->Nt,
+                                                                         c->d_rent);
+        SETUP_CHECK(cudaGetLastError());
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        cudaFree(keys);
+        cudaFree(vals);
+        c->nchunks = (c->Nt + 31) / 32;
+        const int64_t nb = (int64_t)Nd * c->nchunks;
+        SETUP_CHECK(dmalloc(c, &c->d_rchunk, (size_t)nb));
+        k_reducer_chunks<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(c->d_rent, c->f_regions, Nd, c->nchunks,
+                                                                        c->Lf, c->d_rchunk);
+        SETUP_CHECK(cudaGetLastError());
+    }
 
     // ---- adjoint regions
     int acpr = 8;
@@ -434,7 +468,6 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->La = La;
         c->d_wlo_a = wlo;
         c->workspace_bytes += sizeof(int32_t) * (int64_t)nreg * Nd;
-        c->jlen_max = h_flags[5];
         break;
     }
 
@@ -443,7 +476,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     SETUP_CHECK(dmalloc(c, &c->d_amp, c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_delta, (size_t)Nd * c->Nt));
-    SETUP_CHECK(dmalloc(c, &c->d_loss_part, Nd));
+    SETUP_CHECK(dmalloc(c, &c->d_loss_part, (size_t)Nd * std::max(c->nchunks, 1)));
     SETUP_CHECK(cudaStreamSynchronize(st));
     return cudaSuccess;
 }
