@@ -161,7 +161,6 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_perm);
     cudaFree(c->d_wlo_f);
     cudaFree(c->d_rent);
-    cudaFree(c->d_rchunk);
     cudaFree(c->d_partial);
     cudaFree(c->d_wlo_a);
     cudaFree(c->d_amp);

@@ -41,9 +41,8 @@ struct gpair_ctx_s {
     // forward decomposition
     int32_t f_cpr = 0, f_regions = 0, f_warps = 0, f_sgroups = 0, Lf = 0;
     int32_t* d_wlo_f = nullptr;   // [f_regions][Nd] window start (-1 = empty)
-    int2* d_rent = nullptr;       // [Nd][f_regions] (window start, region) sorted by start (gather reducer)
-    int2* d_rchunk = nullptr;     // [Nd][nchunks] entry range meeting each 32-sample chunk
-    int32_t nchunks = 0;          // ceil(N_t / 32)
+    int2* d_rent = nullptr;       // [Nd][f_regions] (window start, region) sorted by start (reducer)
+    int32_t jlen_max = 0;         // longest per-sensor live range of the partial windows
     int32_t n_loss_part = 0;      // loss partials written by the last reduce / residual launch
     float* d_partial = nullptr;   // [f_regions][Nd][Lf]
 

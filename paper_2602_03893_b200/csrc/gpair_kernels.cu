@@ -276,64 +276,111 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
 }
 
 // ------------------------------------------------------------------ reduce
-// Gather reducer: one warp per (sensor j, 32-sample chunk c), lane = sample
-// n = 32c + lane.  The region partials of sensor j whose windows [lo, lo + Lf)
-// meet the chunk are a contiguous range of the per-sensor list sorted by lo
-// (built at create, gpair_setup.cu); each is read once, coalesced, and summed
-// in fp64 registers in the list order (deterministic, no atomics, no smem).
-// Fuses the near-field rows, y, the residual delta = y - b and one fp64 loss
-// partial per warp.
-constexpr int RED_U = 8;  // partial loads in flight per warp
+// One CTA per sensor j.  The region partials of j are visited in the
+// per-sensor list sorted by window start (built at create, gpair_setup.cu);
+// warp w takes a contiguous block of the list and adds each row into its
+// private fp64 smem copy of the sensor's live range (lane = samples l and
+// l + 32 of the row: two aligned 128-B loads per row, every DRAM sector read
+// once; RED_U rows in flight per warp).  The copies are summed in warp order
+// (deterministic, no atomics).  Fuses the near-field rows, y, the residual
+// delta = y - b and one fp64 loss partial per sensor.
+constexpr int RED_U = 16;  // rows in flight per warp
+
+__device__ __forceinline__ int red_lower_bound(const int2* e, int n, int v) {
+    int a = 0, b = n;
+    while (a < b) {
+        const int m = (a + b) >> 1;
+        if (e[m].x < v) a = m + 1; else b = m;
+    }
+    return a;
+}
 
 __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int2* __restrict__ ent,
-                                                const int2* __restrict__ bounds, int32_t nregions, int32_t Lf,
-                                                int32_t nchunks, OpConst k, float* __restrict__ y,
+                                                int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
                                                 const float* __restrict__ b, float* __restrict__ delta,
                                                 double* __restrict__ loss_part, const int32_t* __restrict__ near_row,
                                                 const double* __restrict__ ynear) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (wid >= (int64_t)k.Nd * nchunks) return;
-    const int j = (int)(wid / nchunks), c = (int)(wid - (int64_t)j * nchunks);
-    const int n = 32 * c + lane;
-    const int2 bd = bounds[wid];
+    extern __shared__ double s_copy[];
+    __shared__ int s_hdr[2];
+    __shared__ double s_red[32];
+    const int j = blockIdx.x;
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int2* e = ent + (int64_t)j * nregions;
+    if (threadIdx.x == 0) {
+        const int k0 = red_lower_bound(e, nregions, 0);  // first non-empty window
+        s_hdr[0] = k0;
+        s_hdr[1] = k0 < nregions ? e[k0].x : 0;
+    }
+    __syncthreads();
+    const int k0 = s_hdr[0], jlo = s_hdr[1];
+    const int jlen = k0 < nregions ? min(e[nregions - 1].x + Lf, k.Nt) - jlo : 0;
+    double* mine = s_copy + (size_t)warp * jlen;
+    for (int t = lane; t < jlen; t += 32) mine[t] = 0.0;
+    __syncwarp();
     const float* pj = partial + (size_t)j * nregions * Lf;
-    double acc = 0.0;
-    for (int k0 = bd.x; k0 < bd.y; k0 += 32) {
-        const int cnt = min(32, bd.y - k0);
-        const int2 my = lane < cnt ? e[k0 + lane] : make_int2(-(1 << 30), 0);
+    const int per_warp = (nregions - k0 + nw - 1) / nw;
+    const int kb = k0 + warp * per_warp, ke = min(kb + per_warp, nregions);
+    for (int kk = kb; kk < ke; kk += 32) {
+        const int cnt = min(32, ke - kk);
+        const int2 my = lane < cnt ? e[kk + lane] : make_int2(0, 0);
         for (int u = 0; u < cnt; u += RED_U) {
-            float v[RED_U];
+            float v0[RED_U], v1[RED_U];
+            int lo[RED_U];
 #pragma unroll
             for (int q = 0; q < RED_U; ++q) {
-                const int lo = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
+                lo[q] = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
                 const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
-                const int t = n - lo;
-                v[q] = (u + q < cnt && (unsigned)t < (unsigned)Lf) ? pj[(size_t)r * Lf + t] : 0.f;
+                const float* row = pj + (size_t)r * Lf;
+                const bool ok = u + q < cnt;
+                v0[q] = (ok && lane < Lf) ? row[lane] : 0.f;
+                v1[q] = (ok && lane + 32 < Lf) ? row[lane + 32] : 0.f;
+                if (!ok) lo[q] = -1;
             }
 #pragma unroll
-            for (int q = 0; q < RED_U; ++q) acc += (double)v[q];
+            for (int q = 0; q < RED_U; ++q) {
+                if (lo[q] < 0) continue;
+                const int t0 = lo[q] - jlo + lane;
+                if (lane < Lf && t0 < jlen) mine[t0] += (double)v0[q];
+                if (lane + 32 < Lf && t0 + 32 < jlen) mine[t0 + 32] += (double)v1[q];
+            }
+            for (int q0 = 64; q0 < Lf; q0 += 32) {  // rows longer than 64 samples
+#pragma unroll 1
+                for (int q = 0; q < RED_U; ++q) {
+                    if (lo[q] < 0) continue;
+                    const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
+                    const int t = lo[q] - jlo + q0 + lane;
+                    if (q0 + lane < Lf && t < jlen) mine[t] += (double)pj[(size_t)r * Lf + q0 + lane];
+                }
+            }
         }
     }
+    __syncthreads();
     double lsum = 0.0;
-    if (n < k.Nt) {
-        const int64_t idx = (int64_t)j * k.Nt + n;
-        if (near_row) {  // near-field rows (row f4, gpair_near.cu)
-            const int nrow = near_row[j];
-            if (nrow >= 0) acc += ynear[(int64_t)nrow * k.Nt + n];
-        }
-        const float yv = (float)acc;
-        if (y) y[idx] = yv;
+    const int64_t row = (int64_t)j * k.Nt;
+    const int nrow = near_row ? near_row[j] : -1;  // near-field rows (row f4, gpair_near.cu)
+    for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
+        double ys = 0.0;
+        const int t = n - jlo;
+        if (t >= 0 && t < jlen)
+            for (int w = 0; w < nw; ++w) ys += s_copy[(size_t)w * jlen + t];
+        if (nrow >= 0) ys += ynear[(int64_t)nrow * k.Nt + n];
+        const float yv = (float)ys;
+        if (y) y[row + n] = yv;
         if (b) {
-            const float dv = yv - b[idx];
-            delta[idx] = dv;
-            lsum = (double)dv * (double)dv;
+            const float dv = yv - b[row + n];
+            delta[row + n] = dv;
+            lsum += (double)dv * (double)dv;
         }
     }
     if (b) {
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-        if (lane == 0) loss_part[wid] = lsum;
+        if (lane == 0) s_red[warp] = lsum;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double s = 0.0;
+            for (int w = 0; w < nw; ++w) s += s_red[w];
+            loss_part[j] = s;
+        }
     }
 }
 
@@ -872,11 +919,14 @@ cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
 }
 
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {
-    const int64_t warps = (int64_t)c->Nd * c->nchunks;
-    k_reduce<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(c->d_partial, c->d_rent, c->d_rchunk, c->f_regions, c->Lf,
-                                                         c->nchunks, c->k, y, b, delta, c->d_loss_part,
-                                                         c->n_near ? c->d_near_row : nullptr, c->d_ynear);
-    if (b) c->n_loss_part = (int32_t)warps;
+    int nw = 8;
+    while (nw > 1 && (size_t)nw * c->jlen_max * 8 > 200 * 1024) nw /= 2;
+    const size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 8;
+    cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, c->k, y, b, delta,
+                                           c->d_loss_part, c->n_near ? c->d_near_row : nullptr, c->d_ynear);
+    if (b) c->n_loss_part = c->Nd;
     return cudaGetLastError();
 }
 

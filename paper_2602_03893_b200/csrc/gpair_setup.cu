@@ -199,11 +199,9 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
     }
 }
 
-// Reducer tables (gather reducer, gpair_kernels.cu k_reduce): per sensor j
-// the forward regions sorted by window start, as (lo, region) entries, and per
-// 32-sample chunk c the range of entries whose window [lo, lo + Lf) meets
-// [32c, 32c + 32).  Regions with an empty window (lo = -1) sort first and are
-// excluded by the chunk ranges.
+// Reducer table (gpair_kernels.cu k_reduce): per sensor j the forward regions
+// sorted by window start, as (lo, region) entries.  Regions with an empty
+// window (lo = -1) sort first and are skipped.
 __global__ void k_reducer_keys(const int32_t* __restrict__ wlo, int32_t nregions, int32_t Nd, int32_t Nt,
                                uint32_t* keys, int32_t* vals) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -230,15 +228,14 @@ __device__ __forceinline__ int lower_bound_lo(const int2* e, int n, int v) {
     return a;
 }
 
-__global__ void k_reducer_chunks(const int2* __restrict__ ent, int32_t nregions, int32_t Nd, int32_t nchunks,
-                                 int32_t Lf, int2* bounds) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)Nd * nchunks) return;
-    const int32_t j = (int32_t)(idx / nchunks), c = (int32_t)(idx - (int64_t)j * nchunks);
+// thread per sensor: length of the live range [first window start, last + Lf)
+__global__ void k_reducer_len(const int2* __restrict__ ent, int32_t nregions, int32_t Nd, int32_t Nt, int32_t Lf,
+                              int* jlen_max) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Nd) return;
     const int2* e = ent + (int64_t)j * nregions;
-    const int beg = lower_bound_lo(e, nregions, max(0, 32 * c - Lf + 1));
-    const int end = lower_bound_lo(e, nregions, 32 * c + 32);
-    bounds[idx] = make_int2(beg, max(beg, end));
+    const int k0 = lower_bound_lo(e, nregions, 0);
+    if (k0 < nregions) atomicMax(jlen_max, min(e[nregions - 1].x + Lf, Nt) - e[k0].x);
 }
 
 template <class T>
@@ -426,12 +423,12 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         SETUP_CHECK(cudaStreamSynchronize(st));
         cudaFree(keys);
         cudaFree(vals);
-        c->nchunks = (c->Nt + 31) / 32;
-        const int64_t nb = (int64_t)Nd * c->nchunks;
-        SETUP_CHECK(dmalloc(c, &c->d_rchunk, (size_t)nb));
-        k_reducer_chunks<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(c->d_rent, c->f_regions, Nd, c->nchunks,
-                                                                        c->Lf, c->d_rchunk);
+        SETUP_CHECK(cudaMemsetAsync(c->d_flags + 5, 0, sizeof(int32_t), st));
+        k_reducer_len<<<(Nd + 127) / 128, 128, 0, st>>>(c->d_rent, c->f_regions, Nd, c->Nt, c->Lf, c->d_flags + 5);
         SETUP_CHECK(cudaGetLastError());
+        SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
+        SETUP_CHECK(cudaStreamSynchronize(st));
+        c->jlen_max = h_flags[5];
     }
 
     // ---- adjoint regions
@@ -476,7 +473,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     SETUP_CHECK(dmalloc(c, &c->d_amp, c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_delta, (size_t)Nd * c->Nt));
-    SETUP_CHECK(dmalloc(c, &c->d_loss_part, (size_t)Nd * std::max(c->nchunks, 1)));
+    SETUP_CHECK(dmalloc(c, &c->d_loss_part, Nd));
     SETUP_CHECK(cudaStreamSynchronize(st));
     return cudaSuccess;
 }
