@@ -49,6 +49,7 @@ struct gpair_ctx_s {
     // adjoint decomposition
     int32_t a_cpr = 0, a_regions = 0, La = 0;
     int32_t* d_wlo_a = nullptr;   // [a_regions][Nd]
+    float* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
 
     // per-call workspaces
     float* d_amp = nullptr;       // [Mpad] amplitudes in sorted order
@@ -147,6 +148,7 @@ __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const Ep
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 int pick_wmax(int w);
+bool getenv_flag(const char* name);
 
 // ASSA operator (gpair_assa.cu)
 size_t assa_forward_smem(const gpair_ctx* c, int Lf);

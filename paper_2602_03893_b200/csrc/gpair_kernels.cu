@@ -18,6 +18,7 @@
 //                   the epilogue writes g or applies the fused NPC chain rule
 //                   (Eq. 19) + Adam, or the projected clamp step.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gpair_ctx.h"
 
@@ -325,30 +326,27 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
         const int2 my = lane < cnt ? e[kk + lane] : make_int2(0, 0);
         for (int u = 0; u < cnt; u += RED_U) {
             float v0[RED_U], v1[RED_U];
-            int lo[RED_U];
 #pragma unroll
             for (int q = 0; q < RED_U; ++q) {
-                lo[q] = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
                 const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
                 const float* row = pj + (size_t)r * Lf;
                 const bool ok = u + q < cnt;
                 v0[q] = (ok && lane < Lf) ? row[lane] : 0.f;
                 v1[q] = (ok && lane + 32 < Lf) ? row[lane + 32] : 0.f;
-                if (!ok) lo[q] = -1;
             }
 #pragma unroll
             for (int q = 0; q < RED_U; ++q) {
-                if (lo[q] < 0) continue;
-                const int t0 = lo[q] - jlo + lane;
+                if (u + q >= cnt) break;
+                const int t0 = __shfl_sync(0xffffffffu, my.x, (u + q) & 31) - jlo + lane;
                 if (lane < Lf && t0 < jlen) mine[t0] += (double)v0[q];
                 if (lane + 32 < Lf && t0 + 32 < jlen) mine[t0 + 32] += (double)v1[q];
             }
             for (int q0 = 64; q0 < Lf; q0 += 32) {  // rows longer than 64 samples
 #pragma unroll 1
-                for (int q = 0; q < RED_U; ++q) {
-                    if (lo[q] < 0) continue;
+                for (int q = 0; q < RED_U && u + q < cnt; ++q) {
+                    const int lo = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
                     const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
-                    const int t = lo[q] - jlo + q0 + lane;
+                    const int t = lo - jlo + q0 + lane;
                     if (q0 + lane < Lf && t < jlen) mine[t] += (double)pj[(size_t)r * Lf + q0 + lane];
                 }
             }
@@ -565,6 +563,213 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
 __device__ __forceinline__ int s_wlo_read(const int32_t* wl, int jj) { return wl[jj]; }
 constexpr int ANC_SLOT = 16;                     // floats per (group, sensor pair) slot
 constexpr int ANC_G = 16 * ANC_SLOT + 4;         // floats per group (+16 B: groups on different banks)
+
+// ------------------------------------------------------------------ adjoint, TAB path, sensor lanes
+// The adjoint with the forward's decomposition: lane = sensor j, warp = 32
+// sensors, CTA = adjoint region of cells x 256 sensors (blockIdx.y = sensor
+// group).  Each lane stages its sensor's residual window [lo_j, lo_j + La) as
+// a private smem column [t][32] (conflict-free), keeps the fp64 anchor of the
+// current 8-kernel group in registers, sets up two kernels per step in f32x2
+// (kernel parameters broadcast from smem) and evaluates
+//   g_ij = w E sum_m r^m Q_m(u_c) delta_j[n_c + m]
+// with two Horner chains (gpair_internal.cuh TabConst).  The 8 per-lane
+// values of a group are summed over the warp's 32 sensors by a reduce-scatter
+// of shuffles (lane 4k ends with kernel k), the CTA's warps are summed in
+// smem in a fixed order, and each sensor group writes its partial gradient
+// gpart[group][i]; k_adj_gather sums the groups in order and applies the
+// epilogue (deterministic, no atomics).
+template <int W>
+__global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__ kd, const float4* __restrict__ grp,
+                                                     const float* __restrict__ orig, const float* __restrict__ sens,
+                                                     const int32_t* __restrict__ wlo, const float* __restrict__ resid,
+                                                     float* __restrict__ gpart, int32_t cpr, int32_t ncells,
+                                                     int32_t La, int64_t Mpad, OpConst k, const TabConst tab) {
+    constexpr int C = W / 2;
+    extern __shared__ float4 smem4[];
+    float* s_kx = (float*)smem4;                        // [STAGE_CELLS*32] SoA kernel offsets
+    float* s_ky = s_kx + STAGE_CELLS * CELL;
+    float* s_kz = s_ky + STAGE_CELLS * CELL;
+    float* s_kw = s_kz + STAGE_CELLS * CELL;
+    float4* s_grp = (float4*)(s_kw + STAGE_CELLS * CELL);  // [STAGE_CELLS*GPC]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    float* s_col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32;  // this warp's [La][32]
+    float* col = s_col + lane;
+
+    const int region = blockIdx.x;
+    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const bool jok = j < k.Nd;
+    const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    if (jok) {
+        sx = sens[j];
+        sy = sens[k.Nd + j];
+        sz = sens[2 * k.Nd + j];
+    }
+    {
+        const float* src = resid + (int64_t)j * k.Nt;
+        for (int t = 0; t < La; ++t) {
+            const int n = lo_j + t;
+            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] : 0.f;
+        }
+    }
+    const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
+    const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
+    const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
+    const unsigned span = (unsigned)(k.Nt - k.cnt_int);
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
+        const int nc = min(STAGE_CELLS, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            const float4 v = kd[(int64_t)cb * CELL + t];
+            s_kx[t] = v.x;
+            s_ky[t] = v.y;
+            s_kz[t] = v.z;
+            s_kw[t] = v.w;
+        }
+        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        __syncthreads();
+        for (int gq = 0; gq < nc * GPC; ++gq) {
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            float gv[GROUP];
+            const bool exact_grp = __any_sync(0xffffffffu, a.na == NA_EXACT);
+            const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
+            const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
+            const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R);
+            const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // n_lo - lo_j = bits(tt) + nrel
+#pragma unroll
+            for (int t = 0; t < GROUP; t += 2) {
+                const int li = gq * GROUP + t;
+                float g0 = 0.f, g1 = 0.f;
+                bool rare = exact_grp;
+                if (!exact_grp) {
+                    const f2_t kx = *(const f2_t*)(s_kx + li), ky = *(const f2_t*)(s_ky + li);
+                    const f2_t kz = *(const f2_t*)(s_kz + li), kw = *(const f2_t*)(s_kw + li);
+                    const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
+                    const f2_t eps = mul2(q, iR2);
+                    const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
+                    const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                    const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
+                    const f2_t w = mul2(h2R, Tw);
+                    const f2_t x = add2(eu, clo);
+                    const f2_t tt = add2(x, mag);
+                    const f2_t fl = add2(tt, nmag);
+                    const f2_t d = sub2(x, fl);
+                    const f2_t ulo = sub2(eu, add2(fl, one));
+                    float d0, d1, t0, t1;
+                    upk2(d, d0, d1);
+                    upk2(tt, t0, t1);
+                    const int n0 = __float_as_int(t0) + nrel, n1 = __float_as_int(t1) + nrel;
+                    const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
+                    const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
+                    rare = bad0 || bad1;
+                    if (!rare && lo_j >= 0) {
+                        const f2_t uc = add2(ulo, pk2(-(float)C, -(float)C));
+                        f2_t r2p, s2p;
+                        tab_rs(uc, tab, r2p, s2p);
+                        float e0, e1, P00, P01, uc0, uc1, r0, r1, s0, s1;
+                        upk2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), e0, e1);
+                        upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), P00, P01);
+                        upk2(uc, uc0, uc1);
+                        upk2(r2p, r0, r1);
+                        upk2(s2p, s0, s1);
+                        const float* rp0 = col + n0 * 32;
+                        const float* rp1 = col + n1 * 32;
+                        const f2_t U0 = pk2(uc0, uc0), U1 = pk2(uc1, uc1);
+                        const float rr0 = r0 * r0, ss0 = s0 * s0, rr1 = r1 * r1, ss1 = s1 * s1;
+                        f2_t Q0 = fma2(U0, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
+                        f2_t Q1 = fma2(U1, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
+                        f2_t Sh0 = mul2(Q0, pk2(rp0[(W - 2) * 32], rp0[(W - 1) * 32]));
+                        f2_t Sh1 = mul2(Q1, pk2(rp1[(W - 2) * 32], rp1[(W - 1) * 32]));
+#pragma unroll
+                        for (int i = W - 4; i >= C; i -= 2) {
+                            Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
+                            Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
+                            Sh0 = fma2(Sh0, pk2(rr0, rr0), mul2(Q0, pk2(rp0[i * 32], rp0[(i + 1) * 32])));
+                            Sh1 = fma2(Sh1, pk2(rr1, rr1), mul2(Q1, pk2(rp1[i * 32], rp1[(i + 1) * 32])));
+                        }
+                        Q0 = fma2(U0, tab.c2[0], tab.d2[0]);
+                        Q1 = fma2(U1, tab.c2[0], tab.d2[0]);
+                        f2_t Th0 = mul2(Q0, pk2(rp0[0], rp0[32]));
+                        f2_t Th1 = mul2(Q1, pk2(rp1[0], rp1[32]));
+#pragma unroll
+                        for (int i = 2; i < C; i += 2) {
+                            Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
+                            Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
+                            Th0 = fma2(Th0, pk2(ss0, ss0), mul2(Q0, pk2(rp0[i * 32], rp0[(i + 1) * 32])));
+                            Th1 = fma2(Th1, pk2(ss1, ss1), mul2(Q1, pk2(rp1[i * 32], rp1[(i + 1) * 32])));
+                        }
+                        float se0, so0, te0, to0, se1, so1, te1, to1;
+                        upk2(Sh0, se0, so0);
+                        upk2(Th0, te0, to0);
+                        upk2(Sh1, se1, so1);
+                        upk2(Th1, te1, to1);
+                        g0 = P00 * fmaf(s0, to0, fmaf(ss0, te0, fmaf(r0, so0, se0)));
+                        g1 = P01 * fmaf(s1, to1, fmaf(ss1, te1, fmaf(r1, so1, se1)));
+                    }
+                }
+                if (rare && lo_j >= 0) {  // exact window edges / record clipping / exact-ToF groups
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {
+                        const int64_t gi = (int64_t)cb * CELL + li + h;
+                        const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
+                        const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+                        float part = 0.f;
+                        const float* rq = col + (pw.n_lo - lo_j) * 32;
+                        for (int m = 0; m < pw.cnt; ++m) {
+                            const float um = pw.u_lo - (float)m;
+                            part = fmaf(um * ex2f((um * k.K1u) * um), rq[m * 32], part);
+                        }
+                        if (h) g1 = pw.w * part; else g0 = pw.w * part;
+                    }
+                }
+                gv[t] = g0;
+                gv[t + 1] = g1;
+            }
+            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                float h4[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+                float h2[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                // lane bits (4, 3, 2) hold the kernel index (b4 * 4 + b3 * 2 + b2)
+                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            float sum = 0.f;
+            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+        }
+    }
+}
+
+// sum of the sensor-group partial gradients (fixed order) + epilogue
+template <int MODE>
+__global__ void k_adj_gather(const float* __restrict__ gpart, int32_t ngroups, const int32_t* __restrict__ perm,
+                             int64_t Mpad, EpiParams ep) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= Mpad) return;
+    const int32_t ic = perm[i];
+    if (ic < 0) return;
+    float acc = 0.f;
+    for (int g = 0; g < ngroups; ++g) acc += gpart[(int64_t)g * Mpad + i];
+    adjoint_epilogue<MODE>(acc, ic, ep);
+}
 
 // cp.async (4 B, L1-allocating) for the residual rows of the next sensor batch
 __device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
@@ -789,6 +994,10 @@ __global__ void __launch_bounds__(256, GPAIR_ADJ_MINB) k_adjoint_tab(const float
 }
 
 }  // namespace
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && v[0] == '1';
+}
 int pick_wmax(int w) {
     static const int opts[] = {5, 8, 12, 16, 20, 24, 32, 48, 64};
     for (int o : opts)
@@ -835,6 +1044,25 @@ cudaError_t adj_tab_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
     return cudaGetLastError();
 }
 
+constexpr int ADJT_WARPS = 8;  // sensor warps per CTA of k_adjoint_t
+
+template <int W, int MODE>
+cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    const int nw = ADJT_WARPS;
+    size_t smem = (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)nw * STAGE_CELLS * CELL * 4 +
+                  (size_t)nw * c->La * 32 * 4;
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint_t<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
+    dim3 grid(c->a_regions, ngroups);
+    k_adjoint_t<W><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gpart,
+                                                c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    return cudaGetLastError();
+}
+
 template <int SER, int MODE>
 cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     switch (pick_wmax(c->k.wmax)) {
@@ -867,6 +1095,16 @@ template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
+        if (c->ser == 0 && c->tab.on && c->d_gpart && !getenv_flag("GPAIR_ADJ_TAB_OLD")) {
+            switch (c->k.cnt_int) {
+                case 12: return adj_t_launch<12, MODE>(c, resid, ep, st);
+                case 16: return adj_t_launch<16, MODE>(c, resid, ep, st);
+                case 20: return adj_t_launch<20, MODE>(c, resid, ep, st);
+                case 24: return adj_t_launch<24, MODE>(c, resid, ep, st);
+                case 32: return adj_t_launch<32, MODE>(c, resid, ep, st);
+                default: break;
+            }
+        }
         if (c->ser == 0 && c->tab.on && c->La + 1 <= RAWW) {
             switch (c->k.cnt_int) {
                 case 12: return adj_tab_launch<12, MODE>(c, resid, ep, st);

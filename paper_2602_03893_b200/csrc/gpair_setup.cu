@@ -469,6 +469,8 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     }
 
     // ---- workspaces
+    if (c->ser == 0 && c->tab.on)  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t)
+        SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 255) / 256) * c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_partial, (size_t)c->f_regions * Nd * c->Lf));
     SETUP_CHECK(dmalloc(c, &c->d_amp, c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
