@@ -242,6 +242,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     prof = ctx.profile_read()
+    n_kernels_timed = ctx.profile_kernels()  # library kernel launches inside the timed region
     ctx.profile_enable(False)
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
@@ -296,8 +297,10 @@ def main():
             "peak": peak / 1e9 if args.op == "exact" else None,
             "unit": "Gpair-samples/s", "frac": achieved / peak if args.op == "exact" else None, "traffic": traffic,
             "frac_at_measured_clock": (achieved / (n_sm * SFU_PER_CLK_SM * f_meas)) if args.op == "exact" else None,
-            "peak_def": f"{n_sm} SMs x {SFU_PER_CLK_SM} SFU ex2/clk x {f_max / 1e6:.0f} MHz (one exp per pair-sample; "
-                        "DESIGN.md 'Roofline')",
+            "peak_def": f"{n_sm} SMs x {SFU_PER_CLK_SM} pair-samples/clk x {f_max / 1e6:.0f} MHz: the SFU ex2 rate of one "
+                        "exp per pair-sample (SURVEY 8d) = the shared-memory accumulator rate of one 4-B load + 4-B "
+                        "store per pair-sample at 128 B/clk/SM (the forward's binding unit on the TAB path); "
+                        "DESIGN.md section 6",
             "pair_samples_per_launch": pair_samples_local,
             "kernel_ms": {k: (v[0] / max(v[1], 1)) for k, v in prof.items() if v[1]},
             "share_of_step": {k: (v[0] / args.steps) / ms for k, v in prof.items() if v[1]}}
@@ -315,7 +318,7 @@ def main():
         "roofline": roof,
         "e2e": {"value": pairs_iter / e2e_s, "unit": UNIT, "ms_per_step": e2e_s * 1e3,
                 "h2d_bytes_per_step": int(b.numel() * 4), "d2h_bytes_per_step": 4},
-        "gpu_launches": int(sum(v[1] for k, v in prof.items() if k != "allreduce")),
+        "gpu_launches": int(n_kernels_timed),
         "clocks": clocks,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -137,6 +137,9 @@ enum {
 typedef struct {
     double ms[GPAIR_PROF_N];       /* summed CUDA-event durations [ms]                */
     int64_t launches[GPAIR_PROF_N];/* number of timed launches                        */
+    int64_t kernels;               /* library kernels launched by the per-call entry
+                                      points since gpair_profile_enable (counted whether
+                                      or not events are recorded)                       */
 } gpair_profile;
 
 /* Static description of what gpair_create built (for benchmarks and tests). */

@@ -615,6 +615,7 @@ gpair_status gpair_profile_enable(gpair_ctx* c, int enable) {
         c->prof_ms[i] = 0.0;
         c->prof_n[i] = 0;
     }
+    c->n_launch = 0;
     c->prof_on = enable != 0;
     return GPAIR_OK;
 }
@@ -626,6 +627,7 @@ gpair_status gpair_profile_read(gpair_ctx* c, gpair_profile* out) {
         out->ms[i] = c->prof_ms[i];
         out->launches[i] = c->prof_n[i];
     }
+    out->kernels = c->n_launch;
     return GPAIR_OK;
 }
 

@@ -298,6 +298,7 @@ cudaError_t assa_fwd_launch(gpair_ctx* c, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_assa_forward<SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->f_sgroups);
+    ++c->n_launch;
     k_assa_forward<SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                              c->d_wlo_f, c->d_taps, c->d_partial, c->f_cpr, c->ncells,
                                                              c->Lf, zrows_of(c->k.alpha, c->k.K, c->Lf), c->Mpad, c->k);
@@ -312,6 +313,7 @@ cudaError_t assa_adj_launch(gpair_ctx* c, const EpiParams& ep, cudaStream_t st) 
         cudaFuncSetAttribute(k_assa_adjoint<SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int threads = 32 * std::max(c->a_cpr, 1);
+    ++c->n_launch;
     k_assa_adjoint<SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm,
                                                                    c->d_sens, c->d_wlo_a, c->d_dconv, c->a_cpr,
                                                                    c->ncells, Lz, c->Mpad, c->k, ep, c->d_count);
@@ -339,6 +341,7 @@ cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st) {
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     const int Nup = c->k.alpha * c->Nt;
     dim3 g((Nup + 255) / 256, c->Nd);
+    ++c->n_launch;
     k_assa_dconv<<<g, 256, 0, st>>>(resid, c->d_taps, c->k, c->d_dconv);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -84,6 +84,7 @@ struct gpair_ctx_s {
 
     // profiling
     bool prof_on = false;
+    int64_t n_launch = 0;  // library kernels launched by per-call entry points (gpair_profile.kernels)
     std::vector<GpairEventPair> prof_pending;
     std::vector<cudaEvent_t> prof_free;
     double prof_ms[GPAIR_PROF_N] = {0};

@@ -578,8 +578,16 @@ constexpr int ANC_G = 16 * ANC_SLOT + 4;         // floats per group (+16 B: gro
 // smem in a fixed order, and each sensor group writes its partial gradient
 // gpart[group][i]; k_adj_gather sums the groups in order and applies the
 // epilogue (deterministic, no atomics).
+#ifndef GPAIR_ADJT_DBL
+#define GPAIR_ADJT_DBL 1
+#endif
+#ifndef GPAIR_ADJT_MINB
+#define GPAIR_ADJT_MINB 2
+#endif
+constexpr int ADJT_DBL = GPAIR_ADJT_DBL;  // 1: doubled residual column (one LDS.64 per sample pair)
+
 template <int W>
-__global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__ kd, const float4* __restrict__ grp,
+__global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                      const float* __restrict__ orig, const float* __restrict__ sens,
                                                      const int32_t* __restrict__ wlo, const float* __restrict__ resid,
                                                      float* __restrict__ gpart, int32_t cpr, int32_t ncells,
@@ -593,8 +601,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__
     float4* s_grp = (float4*)(s_kw + STAGE_CELLS * CELL);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
-    float* s_col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32;  // this warp's [La][32]
+    // this warp's residual column [La][32] (ADJT_DBL: [La][32] float2 (delta_t, delta_{t+1}))
+    float* s_col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 * (1 + ADJT_DBL);
     float* col = s_col + lane;
+    f2_t* col2 = (f2_t*)s_col + lane;
 
     const int region = blockIdx.x;
     const int j = (blockIdx.y * nw + warp) * 32 + lane;
@@ -608,9 +618,16 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__
     }
     {
         const float* src = resid + (int64_t)j * k.Nt;
+        float prev = (lo_j >= 0 && lo_j < k.Nt) ? src[lo_j] : 0.f;
         for (int t = 0; t < La; ++t) {
             const int n = lo_j + t;
-            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] : 0.f;
+            if (ADJT_DBL) {
+                const float nxt = (lo_j >= 0 && n + 1 < k.Nt) ? src[n + 1] : 0.f;
+                col2[t * 32] = pk2(prev, nxt);
+                prev = nxt;
+            } else {
+                col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] : 0.f;
+            }
         }
     }
     const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
@@ -674,31 +691,33 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__
                         upk2(uc, uc0, uc1);
                         upk2(r2p, r0, r1);
                         upk2(s2p, s0, s1);
-                        const float* rp0 = col + n0 * 32;
-                        const float* rp1 = col + n1 * 32;
+                        const int rp0 = n0, rp1 = n1;  // window starts in the column
+                        auto ldp = [&](int r0, int i) -> f2_t {
+                            return ADJT_DBL ? col2[(r0 + i) * 32] : pk2(col[(r0 + i) * 32], col[(r0 + i + 1) * 32]);
+                        };
                         const f2_t U0 = pk2(uc0, uc0), U1 = pk2(uc1, uc1);
                         const float rr0 = r0 * r0, ss0 = s0 * s0, rr1 = r1 * r1, ss1 = s1 * s1;
                         f2_t Q0 = fma2(U0, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
                         f2_t Q1 = fma2(U1, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
-                        f2_t Sh0 = mul2(Q0, pk2(rp0[(W - 2) * 32], rp0[(W - 1) * 32]));
-                        f2_t Sh1 = mul2(Q1, pk2(rp1[(W - 2) * 32], rp1[(W - 1) * 32]));
+                        f2_t Sh0 = mul2(Q0, ldp(rp0, W - 2));
+                        f2_t Sh1 = mul2(Q1, ldp(rp1, W - 2));
 #pragma unroll
                         for (int i = W - 4; i >= C; i -= 2) {
                             Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
                             Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
-                            Sh0 = fma2(Sh0, pk2(rr0, rr0), mul2(Q0, pk2(rp0[i * 32], rp0[(i + 1) * 32])));
-                            Sh1 = fma2(Sh1, pk2(rr1, rr1), mul2(Q1, pk2(rp1[i * 32], rp1[(i + 1) * 32])));
+                            Sh0 = fma2(Sh0, pk2(rr0, rr0), mul2(Q0, ldp(rp0, i)));
+                            Sh1 = fma2(Sh1, pk2(rr1, rr1), mul2(Q1, ldp(rp1, i)));
                         }
                         Q0 = fma2(U0, tab.c2[0], tab.d2[0]);
                         Q1 = fma2(U1, tab.c2[0], tab.d2[0]);
-                        f2_t Th0 = mul2(Q0, pk2(rp0[0], rp0[32]));
-                        f2_t Th1 = mul2(Q1, pk2(rp1[0], rp1[32]));
+                        f2_t Th0 = mul2(Q0, ldp(rp0, 0));
+                        f2_t Th1 = mul2(Q1, ldp(rp1, 0));
 #pragma unroll
                         for (int i = 2; i < C; i += 2) {
                             Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
                             Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
-                            Th0 = fma2(Th0, pk2(ss0, ss0), mul2(Q0, pk2(rp0[i * 32], rp0[(i + 1) * 32])));
-                            Th1 = fma2(Th1, pk2(ss1, ss1), mul2(Q1, pk2(rp1[i * 32], rp1[(i + 1) * 32])));
+                            Th0 = fma2(Th0, pk2(ss0, ss0), mul2(Q0, ldp(rp0, i)));
+                            Th1 = fma2(Th1, pk2(ss1, ss1), mul2(Q1, ldp(rp1, i)));
                         }
                         float se0, so0, te0, to0, se1, so1, te1, to1;
                         upk2(Sh0, se0, so0);
@@ -716,10 +735,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_t(const float4* __restrict__
                         const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
                         const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
                         float part = 0.f;
-                        const float* rq = col + (pw.n_lo - lo_j) * 32;
+                        const float* rq = ADJT_DBL ? (const float*)(col2 + (pw.n_lo - lo_j) * 32) : col + (pw.n_lo - lo_j) * 32;
                         for (int m = 0; m < pw.cnt; ++m) {
                             const float um = pw.u_lo - (float)m;
-                            part = fmaf(um * ex2f((um * k.K1u) * um), rq[m * 32], part);
+                            part = fmaf(um * ex2f((um * k.K1u) * um), rq[m * 32 * (1 + ADJT_DBL)], part);
                         }
                         if (h) g1 = pw.w * part; else g0 = pw.w * part;
                     }
@@ -1013,6 +1032,7 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->f_sgroups);
+    ++c->n_launch;
     k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
                                                       c->Mpad, c->k, c->d_ksig, c->tab);
@@ -1026,6 +1046,7 @@ cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cu
     cudaError_t e = cudaFuncSetAttribute(k_adjoint<W, SER, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int threads = 32 * std::max(c->a_cpr, 1);
+    ++c->n_launch;
     k_adjoint<W, SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                            c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
                                                            c->k, ep, c->d_count, c->d_ksig);
@@ -1038,6 +1059,7 @@ cudaError_t adj_tab_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
     size_t smem = (size_t)nw * GPC * ANC_G * 4 + 32 * 16 + 96 * 4 + (size_t)32 * RAWW * 4 + (size_t)32 * c->La * 8;
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_tab<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    ++c->n_launch;
     k_adjoint_tab<W, MODE><<<c->a_regions, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                              c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
                                                              c->k, ep, c->tab);
@@ -1046,19 +1068,25 @@ cudaError_t adj_tab_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
 
 constexpr int ADJT_WARPS = 8;  // sensor warps per CTA of k_adjoint_t
 
+size_t adj_t_smem(const gpair_ctx* c) {
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+           (size_t)ADJT_WARPS * c->La * 32 * 4 * (1 + ADJT_DBL);
+}
+
 template <int W, int MODE>
 cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     const int nw = ADJT_WARPS;
-    size_t smem = (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)nw * STAGE_CELLS * CELL * 4 +
-                  (size_t)nw * c->La * 32 * 4;
+    const size_t smem = adj_t_smem(c);
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_t<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
     dim3 grid(c->a_regions, ngroups);
+    ++c->n_launch;
     k_adjoint_t<W><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gpart,
                                                 c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    ++c->n_launch;
     k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
     return cudaGetLastError();
 }
@@ -1095,7 +1123,7 @@ template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
-        if (c->ser == 0 && c->tab.on && c->d_gpart && !getenv_flag("GPAIR_ADJ_TAB_OLD")) {
+        if (c->ser == 0 && c->tab.on && c->d_gpart && adj_t_smem(c) <= 227 * 1024 && !getenv_flag("GPAIR_ADJ_TAB_OLD")) {
             switch (c->k.cnt_int) {
                 case 12: return adj_t_launch<12, MODE>(c, resid, ep, st);
                 case 16: return adj_t_launch<16, MODE>(c, resid, ep, st);
@@ -1140,6 +1168,7 @@ cudaError_t fwd_dispatch(gpair_ctx* c, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_gather(gpair_ctx* c, const float* src, int npc, float eps, cudaStream_t st) {
+    ++c->n_launch;
     k_gather<<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(src, c->d_perm, c->Mpad, npc, eps, c->d_amp);
     return cudaGetLastError();
 }
@@ -1162,6 +1191,7 @@ cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, 
     const size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 8;
     cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    ++c->n_launch;
     k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, c->k, y, b, delta,
                                            c->d_loss_part, c->n_near ? c->d_near_row : nullptr, c->d_ynear);
     if (b) c->n_loss_part = c->Nd;
@@ -1169,6 +1199,7 @@ cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, 
 }
 
 cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st) {
+    ++c->n_launch;
     k_residual<<<c->Nd, 256, 0, st>>>(y, b, c->Nt, delta, c->d_loss_part);
     c->n_loss_part = c->Nd;
     return cudaGetLastError();
@@ -1176,6 +1207,7 @@ cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float*
 
 cudaError_t launch_loss(gpair_ctx* c, float* loss_out, cudaStream_t st, const double* reg_part, int32_t n_reg,
                         double lam) {
+    ++c->n_launch;
     k_loss<<<1, 1024, 0, st>>>(c->d_loss_part, c->n_loss_part, 1.0 / ((double)c->Nd * (double)c->Nt), reg_part,
                                reg_part ? n_reg : 0, lam, loss_out);
     return cudaGetLastError();

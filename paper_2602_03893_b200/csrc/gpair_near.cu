@@ -269,6 +269,7 @@ cudaError_t build_general(gpair_ctx* c, cudaStream_t st, std::string& why, int& 
 
 cudaError_t launch_near_forward(gpair_ctx* c, cudaStream_t st) {
     if (!c->n_near) return cudaSuccess;
+    ++c->n_launch;
     k_near_forward<<<(c->n_near_rows + 63) / 64, 64, 0, st>>>(c->d_near_f, c->d_near_rseg, c->n_near_rows, c->d_orig,
                                                              c->d_ksig, c->d_amp, c->d_sens, c->Mpad, c->k,
                                                              c->d_ynear);
@@ -277,6 +278,7 @@ cudaError_t launch_near_forward(gpair_ctx* c, cudaStream_t st) {
 
 cudaError_t launch_near_adjoint(gpair_ctx* c, const float* resid, cudaStream_t st) {
     if (!c->n_near) return cudaSuccess;
+    ++c->n_launch;
     k_near_adjoint<<<(c->n_near_cols + 63) / 64, 64, 0, st>>>(c->d_near_a, c->d_near_cseg, c->n_near_cols, c->d_orig,
                                                              c->d_ksig, c->d_perm, c->d_sens, resid, c->Mpad, c->k,
                                                              c->d_gnear);

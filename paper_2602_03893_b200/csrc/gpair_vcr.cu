@@ -186,15 +186,18 @@ cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int 
     if (e != cudaSuccess) return e;
     const Grid G{dims[0], dims[1], dims[2]};
     const int nb = (int)((M + 255) / 256);
+    ++c->n_launch;
     k_vcr_terms<<<nb, 256, 0, st>>>(src, npc, eps_npc, G, beta, eps, c->d_vcr_u, M, c->d_vcr_part);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (grad) {
+        ++c->n_launch;
         k_vcr_grad<<<nb, 256, 0, st>>>(c->d_vcr_u, G, beta, M, grad);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     if (value) {
+        ++c->n_launch;
         k_vcr_sum<<<1, 1024, 0, st>>>(c->d_vcr_part, nb, value);
         e = cudaGetLastError();
     }

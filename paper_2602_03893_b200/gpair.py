@@ -65,7 +65,8 @@ class Step(ctypes.Structure):
 
 
 class Profile(ctypes.Structure):
-    _fields_ = [("ms", ctypes.c_double * len(PROF_NAMES)), ("launches", ctypes.c_int64 * len(PROF_NAMES))]
+    _fields_ = [("ms", ctypes.c_double * len(PROF_NAMES)), ("launches", ctypes.c_int64 * len(PROF_NAMES)),
+                ("kernels", ctypes.c_int64)]
 
 
 class Info(ctypes.Structure):
@@ -289,3 +290,9 @@ class Context:
         p = Profile()
         _check(lib().gpair_profile_read(self._h, ctypes.byref(p)), self._h)
         return {name: (p.ms[i], p.launches[i]) for i, name in enumerate(PROF_NAMES)}
+
+    def profile_kernels(self):
+        """Library kernels launched by the per-call entry points since profile_enable()."""
+        p = Profile()
+        _check(lib().gpair_profile_read(self._h, ctypes.byref(p)), self._h)
+        return int(p.kernels)

@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round evidence on one B200: GPU tests, smoke, bench (JSON line), ncu launch
+# list of a short bench, and one ncu --set full capture per hot kernel.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+TAG=${TAG:-ev}
+CFG=${CFG:-cfg4}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu_${TAG}.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_gpu_${TAG}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG}.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/smoke_${TAG}.log
+timeout 900 python bench.py --config $CFG > gpurun_out/bench_${TAG}.log 2>&1
+echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv \
+    python bench.py --config $CFG --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1
+echo "launch list rc=$?"
+for K in k_forward k_adjoint_t "k_reduce\$"; do
+  KN=$(echo "$K" | tr -d '$\\')
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -c 1 \
+      -o gpurun_out/prof_${CFG}_${KN}_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${KN}_${TAG}.log 2>&1
+  echo "full $KN rc=$?"
+  python scripts/ncu_summary.py gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep > gpurun_out/ncu_summary_${KN}_${TAG}.txt 2>&1
+  ncu -i gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_source_${KN}_${TAG}.csv 2>/dev/null
+  [ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep
+done
+tail -2 gpurun_out/pytest_gpu_${TAG}.log; tail -2 gpurun_out/smoke_${TAG}.log; tail -c 600 gpurun_out/bench_${TAG}.log

@@ -27,6 +27,16 @@ def main(rep):
         for k in KEYS:
             if k in d:
                 print(f"  {k:70s} {d[k]:>20s} {units[hdr.index(k)]}")
+        try:  # derived: shared-memory wavefronts per SM clock (the smem pipe serves 1 / clk / SM)
+            wf = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", ""))
+            t = float(d["gpu__time_duration.sum"].replace(",", "")) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(
+                units[hdr.index("gpu__time_duration.sum")].replace("second", "s").replace("msecond", "ms"), 1e-3)
+            f = float(d["sm__cycles_elapsed.avg.per_second"].replace(",", "")) * (
+                1e9 if "G" in units[hdr.index("sm__cycles_elapsed.avg.per_second")] else 1.0)
+            n_sm = 148
+            print(f"  derived: smem wavefronts / SM / clk {wf / (t * f * n_sm):.3f} (1.0 = smem pipe peak)")
+        except (KeyError, ValueError):
+            pass
         st = [(k, d[k]) for k in hdr if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
         vals = [(k.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v.replace(",", "") or 0)) for k, v in st
                 if v not in ("", "n/a")]
