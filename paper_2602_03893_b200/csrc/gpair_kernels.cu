@@ -8,15 +8,20 @@
 //                   time trace for the region in a private shared-memory
 //                   column [sample][32] (conflict-free, no atomics), then the
 //                   warp flushes it with 128-byte coalesced stores after an
-//                   in-place XOR-swizzled transpose.
+//                   in-place XOR-swizzled transpose.  Full windows use the
+//                   factorised Gaussian (TAB path, gpair_internal.cuh).
 //   k_reduce    a5+a6: sums the region partial traces of one sensor in a
 //                   fixed order (deterministic), writes y, the residual
 //                   delta = y - b and per-sensor loss partials.
+//   k_adjoint_t a7: the adjoint with the forward's decomposition (lane =
+//                   sensor) on the TAB path; per-sensor-group partial
+//                   gradients; k_adj_gather (a8) sums them in order and applies
+//                   the fused NPC chain rule (Eq. 19) + Adam, or the clamp step.
 //   k_adjoint   a7+a8: lane = kernel, warp = one 32-kernel cell, CTA = region
-//                   of cells; residual windows of 32 sensors are staged in
-//                   shared memory and read per lane (gather only, no atomics);
-//                   the epilogue writes g or applies the fused NPC chain rule
-//                   (Eq. 19) + Adam, or the projected clamp step.
+//                   of cells (every other configuration); residual windows of
+//                   32 sensors are staged in shared memory and read per lane
+//                   (gather only, no atomics); the epilogue writes g or applies
+//                   the update.
 #include <algorithm>
 #include <cstdlib>
 
