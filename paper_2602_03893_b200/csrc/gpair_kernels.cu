@@ -284,13 +284,15 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
 // ------------------------------------------------------------------ reduce
 // One CTA per sensor j.  The region partials of j are visited in the
 // per-sensor list sorted by window start (built at create, gpair_setup.cu);
-// warp w takes a contiguous block of the list and adds each row into its
-// private fp64 smem copy of the sensor's live range (lane = samples l and
-// l + 32 of the row: two aligned 128-B loads per row, every DRAM sector read
-// once; RED_U rows in flight per warp).  The copies are summed in warp order
-// (deterministic, no atomics).  Fuses the near-field rows, y, the residual
-// delta = y - b and one fp64 loss partial per sensor.
-constexpr int RED_U = 16;  // rows in flight per warp
+// warp w takes a contiguous block of the list, so its rows cover only
+// [lo(first), lo(last) + Lf): a private fp64 smem copy of just that span
+// (sum over warps ~ live range + nw Lf, not nw x live range).  Lane = samples
+// l and l + 32 of a row: two aligned 128-B loads per row, every DRAM sector
+// read once, RED_U rows in flight per warp.  The overlapping copies are summed
+// in warp order (deterministic, no atomics).  Fuses the near-field rows, y,
+// the residual delta = y - b and one fp64 loss partial per sensor.
+constexpr int RED_U = 8;      // rows in flight per warp
+constexpr int RED_WARPS = 16; // warps per CTA
 
 __device__ __forceinline__ int red_lower_bound(const int2* e, int n, int v) {
     int a = 0, b = n;
@@ -301,31 +303,44 @@ __device__ __forceinline__ int red_lower_bound(const int2* e, int n, int v) {
     return a;
 }
 
-__global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partial, const int2* __restrict__ ent,
-                                                int32_t nregions, int32_t Lf, OpConst k, float* __restrict__ y,
-                                                const float* __restrict__ b, float* __restrict__ delta,
-                                                double* __restrict__ loss_part, const int32_t* __restrict__ near_row,
-                                                const double* __restrict__ ynear) {
+__global__ void __launch_bounds__(32 * RED_WARPS, 2) k_reduce(const float* __restrict__ partial,
+                                                              const int2* __restrict__ ent, int32_t nregions,
+                                                              int32_t Lf, OpConst k, float* __restrict__ y,
+                                                              const float* __restrict__ b, float* __restrict__ delta,
+                                                              double* __restrict__ loss_part,
+                                                              const int32_t* __restrict__ near_row,
+                                                              const double* __restrict__ ynear) {
     extern __shared__ double s_copy[];
-    __shared__ int s_hdr[2];
-    __shared__ double s_red[32];
+    __shared__ int s_k0;
+    __shared__ int s_base[RED_WARPS], s_len[RED_WARPS], s_off[RED_WARPS];
+    __shared__ double s_red[RED_WARPS];
     const int j = blockIdx.x;
-    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int2* e = ent + (int64_t)j * nregions;
-    if (threadIdx.x == 0) {
-        const int k0 = red_lower_bound(e, nregions, 0);  // first non-empty window
-        s_hdr[0] = k0;
-        s_hdr[1] = k0 < nregions ? e[k0].x : 0;
+    if (threadIdx.x == 0) s_k0 = red_lower_bound(e, nregions, 0);  // first non-empty window
+    __syncthreads();
+    const int k0 = s_k0;
+    const int per_warp = (nregions - k0 + RED_WARPS - 1) / RED_WARPS;
+    const int kb = k0 + warp * per_warp, ke = min(kb + per_warp, nregions);
+    if (lane == 0) {
+        const int base = kb < ke ? e[kb].x : 0;
+        s_base[warp] = base;
+        s_len[warp] = kb < ke ? min(e[ke - 1].x + Lf, k.Nt) - base : 0;
     }
     __syncthreads();
-    const int k0 = s_hdr[0], jlo = s_hdr[1];
-    const int jlen = k0 < nregions ? min(e[nregions - 1].x + Lf, k.Nt) - jlo : 0;
-    double* mine = s_copy + (size_t)warp * jlen;
-    for (int t = lane; t < jlen; t += 32) mine[t] = 0.0;
+    if (threadIdx.x == 0) {
+        int o = 0;
+        for (int w = 0; w < RED_WARPS; ++w) {
+            s_off[w] = o;
+            o += s_len[w];
+        }
+    }
+    __syncthreads();
+    const int base = s_base[warp], len = s_len[warp];
+    double* mine = s_copy + s_off[warp];
+    for (int t = lane; t < len; t += 32) mine[t] = 0.0;
     __syncwarp();
     const float* pj = partial + (size_t)j * nregions * Lf;
-    const int per_warp = (nregions - k0 + nw - 1) / nw;
-    const int kb = k0 + warp * per_warp, ke = min(kb + per_warp, nregions);
     for (int kk = kb; kk < ke; kk += 32) {
         const int cnt = min(32, ke - kk);
         const int2 my = lane < cnt ? e[kk + lane] : make_int2(0, 0);
@@ -342,17 +357,17 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
 #pragma unroll
             for (int q = 0; q < RED_U; ++q) {
                 if (u + q >= cnt) break;
-                const int t0 = __shfl_sync(0xffffffffu, my.x, (u + q) & 31) - jlo + lane;
-                if (lane < Lf && t0 < jlen) mine[t0] += (double)v0[q];
-                if (lane + 32 < Lf && t0 + 32 < jlen) mine[t0 + 32] += (double)v1[q];
+                const int t0 = __shfl_sync(0xffffffffu, my.x, (u + q) & 31) - base + lane;
+                if (lane < Lf && t0 < len) mine[t0] += (double)v0[q];
+                if (lane + 32 < Lf && t0 + 32 < len) mine[t0 + 32] += (double)v1[q];
             }
             for (int q0 = 64; q0 < Lf; q0 += 32) {  // rows longer than 64 samples
 #pragma unroll 1
                 for (int q = 0; q < RED_U && u + q < cnt; ++q) {
                     const int lo = __shfl_sync(0xffffffffu, my.x, (u + q) & 31);
                     const int r = __shfl_sync(0xffffffffu, my.y, (u + q) & 31);
-                    const int t = lo - jlo + q0 + lane;
-                    if (q0 + lane < Lf && t < jlen) mine[t] += (double)pj[(size_t)r * Lf + q0 + lane];
+                    const int t = lo - base + q0 + lane;
+                    if (q0 + lane < Lf && t < len) mine[t] += (double)pj[(size_t)r * Lf + q0 + lane];
                 }
             }
         }
@@ -363,9 +378,10 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
     const int nrow = near_row ? near_row[j] : -1;  // near-field rows (row f4, gpair_near.cu)
     for (int n = threadIdx.x; n < k.Nt; n += blockDim.x) {
         double ys = 0.0;
-        const int t = n - jlo;
-        if (t >= 0 && t < jlen)
-            for (int w = 0; w < nw; ++w) ys += s_copy[(size_t)w * jlen + t];
+        for (int w = 0; w < RED_WARPS; ++w) {
+            const int t = n - s_base[w];
+            if (t >= 0 && t < s_len[w]) ys += s_copy[s_off[w] + t];
+        }
         if (nrow >= 0) ys += ynear[(int64_t)nrow * k.Nt + n];
         const float yv = (float)ys;
         if (y) y[row + n] = yv;
@@ -380,9 +396,9 @@ __global__ void __launch_bounds__(256) k_reduce(const float* __restrict__ partia
         if (lane == 0) s_red[warp] = lsum;
         __syncthreads();
         if (threadIdx.x == 0) {
-            double s = 0.0;
-            for (int w = 0; w < nw; ++w) s += s_red[w];
-            loss_part[j] = s;
+            double sacc = 0.0;
+            for (int w = 0; w < RED_WARPS; ++w) sacc += s_red[w];
+            loss_part[j] = sacc;
         }
     }
 }
@@ -1191,14 +1207,13 @@ cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
 }
 
 cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, cudaStream_t st) {
-    int nw = 8;
-    while (nw > 1 && (size_t)nw * c->jlen_max * 8 > 200 * 1024) nw /= 2;
-    const size_t smem = (size_t)nw * std::max(c->jlen_max, 1) * 8;
+    // per-warp spans: sum <= live range + RED_WARPS (Lf - 1) + RED_WARPS
+    const size_t smem = (size_t)(std::max(c->jlen_max, 1) + RED_WARPS * (c->Lf + 1)) * 8;
     cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     ++c->n_launch;
-    k_reduce<<<c->Nd, 32 * nw, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, c->k, y, b, delta,
-                                           c->d_loss_part, c->n_near ? c->d_near_row : nullptr, c->d_ynear);
+    k_reduce<<<c->Nd, 32 * RED_WARPS, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, c->k, y, b, delta,
+                                                  c->d_loss_part, c->n_near ? c->d_near_row : nullptr, c->d_ynear);
     if (b) c->n_loss_part = c->Nd;
     return cudaGetLastError();
 }
