@@ -164,6 +164,7 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_partial);
     cudaFree(c->d_wlo_a);
     cudaFree(c->d_gpart);
+    cudaFree(c->d_gtab);
     cudaFree(c->d_amp);
     cudaFree(c->d_y);
     cudaFree(c->d_delta);

@@ -798,6 +798,259 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     }
 }
 
+// ------------------------------------------------------------------ adjoint, lane-centred factorisation
+// k_adjoint_t's decomposition with the Gaussian factorised about the CENTRE of
+// the lane's residual column instead of each pair's centre.  Column index t,
+// tau = t - T (T = La / 2), G(tau) = 2^{K tau^2} (fp64 table).
+// For a pair with window start o and u = u_lo - i at t = o + i (u_lo in
+// (ku - 1, ku)), a = u_lo + o - T is its centre in column coordinates and
+//   u 2^{K u^2} = 2^{K u_lo^2} G(o - T)^{-1} * R^i G(o + i - T) (u_lo - i),
+//   R = 2^{-2 K a}.
+// The column is staged once per region as dtil_t = delta_t G(t - T), so
+//   g_ij = w 2^{K u_lo^2} / G(o - T) * (u_lo P - R P'),
+//   P = sum_i dtil_{o+i} R^i,  P' = dP/dR,
+// one simultaneous Horner step (two FFMA) per sample and no table in the loop.
+// R comes from an exact range reduction 2^n * poly(f), |f| <= 1/2, degree 7
+// (unbiased to fp32 rounding).  Valid while |K| max(T, La - T)^2 <= LCF_KMAX
+// (every factor stays a normal fp32); else k_adjoint_t is used.
+constexpr float LCF_KMAX = 90.f;
+
+__device__ __forceinline__ float rcpf(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// 2^x for |x| < 64: 2^rint(x) * e^{f ln2}, f = x - rint(x) in [-1/2, 1/2]
+__device__ __forceinline__ f2_t exp2_acc2(f2_t x) {
+    const f2_t t = add2(x, pk2(RND_MAGIC, RND_MAGIC));
+    const f2_t f = sub2(x, add2(t, pk2(-RND_MAGIC, -RND_MAGIC)));
+    f2_t p = fma2(f, pk2(1.5252733804059840e-5f, 1.5252733804059840e-5f), pk2(1.5403530393381609e-4f, 1.5403530393381609e-4f));
+    p = fma2(f, p, pk2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
+    p = fma2(f, p, pk2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
+    p = fma2(f, p, pk2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
+    p = fma2(f, p, pk2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
+    p = fma2(f, p, pk2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
+    p = fma2(f, p, pk2(1.f, 1.f));
+    float p0, p1, t0, t1;
+    upk2(p, p0, p1);
+    upk2(t, t0, t1);
+    p0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - RND_MAGIC_BITS) << 23));
+    p1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - RND_MAGIC_BITS) << 23));
+    return pk2(p0, p1);
+}
+
+template <int W>
+__global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
+                                                       const float* __restrict__ orig, const float* __restrict__ sens,
+                                                       const int32_t* __restrict__ wlo, const float* __restrict__ resid,
+                                                       const float* __restrict__ gtab, float* __restrict__ gpart,
+                                                       int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
+                                                       float K, float m2K) {
+    extern __shared__ float4 smem4[];
+    float* s_kx = (float*)smem4;                        // [STAGE_CELLS*32] SoA kernel offsets
+    float* s_ky = s_kx + STAGE_CELLS * CELL;
+    float* s_kz = s_ky + STAGE_CELLS * CELL;
+    float* s_kw = s_kz + STAGE_CELLS * CELL;
+    float4* s_grp = (float4*)(s_kw + STAGE_CELLS * CELL);  // [STAGE_CELLS*GPC]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    float* s_gt = s_g + nw * STAGE_CELLS * CELL;          // [2][La]: G(t - T), 1 / G(t - T)
+    float* col = s_gt + 2 * La + (size_t)warp * La * 32 + lane;  // this lane's column dtil_t at col[t * 32]
+    for (int t = threadIdx.x; t < 2 * La; t += blockDim.x) s_gt[t] = gtab[t];
+    __syncthreads();
+    const float* s_ginv = s_gt + La;
+
+    const int region = blockIdx.x;
+    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const bool jok = j < k.Nd;
+    const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    if (jok) {
+        sx = sens[j];
+        sy = sens[k.Nd + j];
+        sz = sens[2 * k.Nd + j];
+    }
+    {
+        const float* src = resid + (int64_t)j * k.Nt;
+        for (int t = 0; t < La; ++t) {
+            const int n = lo_j + t;
+            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] * s_gt[t] : 0.f;
+        }
+    }
+    const int Tc = La >> 1;
+    const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
+    const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
+    const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
+    const f2_t K2 = pk2(K, K), M2K = pk2(m2K, m2K);
+    const unsigned span = (unsigned)(k.Nt - k.cnt_int);
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
+        const int nc = min(STAGE_CELLS, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            const float4 v = kd[(int64_t)cb * CELL + t];
+            s_kx[t] = v.x;
+            s_ky[t] = v.y;
+            s_kz[t] = v.z;
+            s_kw[t] = v.w;
+        }
+        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        __syncthreads();
+        for (int gq = 0; gq < nc * GPC; ++gq) {
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            float gv[GROUP];
+            const bool exact_grp = __any_sync(0xffffffffu, a.na == NA_EXACT);
+            const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
+            const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
+            const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R);
+            const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // o = n_lo - lo_j = bits(tt) + nrel
+            const float cg = (float)(a.na - lo_j - Tc);            // a_pair = eu + cg (exact integer shift)
+            const f2_t CG = pk2(cg, cg);
+            // four kernels per step: two f32x2 packs whose Horner chains interleave (ILP)
+#pragma unroll
+            for (int t = 0; t < GROUP; t += 4) {
+                const int li = gq * GROUP + t;
+                bool rare = exact_grp;
+                f2_t eu[2], w[2], ulo[2];
+                int o[4];
+                if (!exact_grp) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const f2_t kx = *(const f2_t*)(s_kx + li + 2 * h), ky = *(const f2_t*)(s_ky + li + 2 * h);
+                        const f2_t kz = *(const f2_t*)(s_kz + li + 2 * h), kw = *(const f2_t*)(s_kw + li + 2 * h);
+                        const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
+                        const f2_t eps = mul2(q, iR2);
+                        const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
+                        const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                        eu[h] = fma2(mul2(q, i2Rh), S, Eu);
+                        w[h] = mul2(h2R, Tw);
+                        const f2_t x = add2(eu[h], clo);
+                        const f2_t tt = add2(x, mag);
+                        const f2_t fl = add2(tt, nmag);
+                        const f2_t d = sub2(x, fl);
+                        ulo[h] = sub2(eu[h], add2(fl, one));
+                        float d0, d1, t0, t1;
+                        upk2(d, d0, d1);
+                        upk2(tt, t0, t1);
+                        o[2 * h] = __float_as_int(t0) + nrel;
+                        o[2 * h + 1] = __float_as_int(t1) + nrel;
+                        rare = rare || fabsf(d0) > 0.5f - GAMMA || (unsigned)(o[2 * h] + lo_j) > span ||
+                               fabsf(d1) > 0.5f - GAMMA || (unsigned)(o[2 * h + 1] + lo_j) > span;
+                    }
+                }
+                if (!rare && lo_j >= 0) {
+                    // centred form: value = w 2^{K u_c^2} / G(o + C - T) * [u_c (U + L) - R U' + L#],
+                    // U = sum_{m>=0} at_m R^m, L = sum_{k>=1} at_{-k} S^k (S = 1/R), at_m = dtil_{o+C+m};
+                    // the two halves are independent Horner chains (ILP) with weights |m| <= C
+                    constexpr int C = W / 2;
+                    f2_t R2[2], S2[2], U[2], Ud[2], La_[2], Ld[2], UC[2];
+                    float sc[4];
+                    const float* rp[4];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        R2[h] = exp2_acc2(mul2(add2(eu[h], CG), M2K));  // R = 2^{-2 K a}, a = eu + cg
+                        float r0, r1;
+                        upk2(R2[h], r0, r1);
+                        float q0 = rcpf(r0), q1 = rcpf(r1);
+                        q0 = q0 * fmaf(-r0, q0, 2.f);  // one Newton step: S to fp32 rounding
+                        q1 = q1 * fmaf(-r1, q1, 2.f);
+                        S2[h] = pk2(q0, q1);
+                        UC[h] = add2(ulo[h], pk2(-(float)C, -(float)C));  // u_c, exact
+                        float e0, e1;
+                        upk2(mul2(mul2(UC[h], K2), UC[h]), e0, e1);
+                        upk2(mul2(w[h], pk2(ex2f(e0) * s_ginv[o[2 * h] + C], ex2f(e1) * s_ginv[o[2 * h + 1] + C])),
+                             sc[2 * h], sc[2 * h + 1]);
+                        rp[2 * h] = col + (o[2 * h] + C) * 32;
+                        rp[2 * h + 1] = col + (o[2 * h + 1] + C) * 32;
+                        U[h] = pk2(rp[2 * h][(W - C - 1) * 32], rp[2 * h + 1][(W - C - 1) * 32]);
+                        Ud[h] = pk2(0.f, 0.f);
+                        La_[h] = pk2(rp[2 * h][-C * 32], rp[2 * h + 1][-C * 32]);
+                        Ld[h] = pk2(0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int i = 1; i < C; ++i) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int mu = W - C - 1 - i;  // upper: m = W-C-2 .. 0
+                            Ud[h] = fma2(Ud[h], R2[h], U[h]);
+                            U[h] = fma2(U[h], R2[h], pk2(rp[2 * h][mu * 32], rp[2 * h + 1][mu * 32]));
+                            const int ml = -C + i;  // lower: m = -C+1 .. -1
+                            Ld[h] = fma2(Ld[h], S2[h], La_[h]);
+                            La_[h] = fma2(La_[h], S2[h], pk2(rp[2 * h][ml * 32], rp[2 * h + 1][ml * 32]));
+                        }
+                    }
+#pragma unroll
+                    for (int i = C; i < W - C; ++i) {  // upper chain longer than the lower one (W odd: never, W % 4 == 0)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int mu = W - C - 1 - i;
+                            Ud[h] = fma2(Ud[h], R2[h], U[h]);
+                            U[h] = fma2(U[h], R2[h], pk2(rp[2 * h][mu * 32], rp[2 * h + 1][mu * 32]));
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        // L = S Lacc, L# = S Lacc + S^2 Lacc'
+                        const f2_t Lv = mul2(S2[h], La_[h]);
+                        const f2_t Ls = fma2(mul2(S2[h], S2[h]), Ld[h], Lv);
+                        // u_c (U + L) - R U' + L#
+                        const f2_t v = add2(fma2(UC[h], add2(U[h], Lv), mul2(mul2(R2[h], Ud[h]), pk2(-1.f, -1.f))), Ls);
+                        float v0, v1;
+                        upk2(v, v0, v1);
+                        gv[t + 2 * h] = sc[2 * h] * v0;
+                        gv[t + 2 * h + 1] = sc[2 * h + 1] * v1;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {  // exact window edges / record clipping / exact-ToF groups
+                        float g = 0.f;
+                        if (lo_j >= 0) {
+                            const int64_t gi = (int64_t)cb * CELL + li + h;
+                            const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
+                            const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+                            float part = 0.f;
+                            const int oo = pw.n_lo - lo_j;
+                            for (int m = 0; m < pw.cnt; ++m) {
+                                const float um = pw.u_lo - (float)m;
+                                part = fmaf(um * ex2f((um * k.K1u) * um), col[(oo + m) * 32] * s_ginv[oo + m], part);
+                            }
+                            g = pw.w * part;
+                        }
+                        gv[t + h] = g;
+                    }
+                }
+            }
+            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                float h4[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+                float h2[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            float sum = 0.f;
+            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+        }
+    }
+}
+
 // sum of the sensor-group partial gradients (fixed order) + epilogue
 template <int MODE>
 __global__ void k_adj_gather(const float* __restrict__ gpart, int32_t ngroups, const int32_t* __restrict__ perm,
@@ -1112,6 +1365,30 @@ cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
     return cudaGetLastError();
 }
 
+size_t adj_lcf_smem(const gpair_ctx* c) {
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+           (size_t)2 * c->La * 4 + (size_t)ADJT_WARPS * c->La * 32 * 4;
+}
+
+template <int W, int MODE>
+cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    const int nw = ADJT_WARPS;
+    const size_t smem = adj_lcf_smem(c);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint_lcf<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
+    dim3 grid(c->a_regions, ngroups);
+    ++c->n_launch;
+    k_adjoint_lcf<W><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gtab,
+                                                  c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab.K,
+                                                  c->tab.m2K);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++c->n_launch;
+    k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    return cudaGetLastError();
+}
+
 template <int SER, int MODE>
 cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     switch (pick_wmax(c->k.wmax)) {
@@ -1144,6 +1421,17 @@ template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
+        if (c->ser == 0 && c->tab.on && c->d_gpart && c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 &&
+            !getenv_flag("GPAIR_ADJ_NO_LCF")) {
+            switch (c->k.cnt_int) {
+                case 12: return adj_lcf_launch<12, MODE>(c, resid, ep, st);
+                case 16: return adj_lcf_launch<16, MODE>(c, resid, ep, st);
+                case 20: return adj_lcf_launch<20, MODE>(c, resid, ep, st);
+                case 24: return adj_lcf_launch<24, MODE>(c, resid, ep, st);
+                case 32: return adj_lcf_launch<32, MODE>(c, resid, ep, st);
+                default: break;
+            }
+        }
         if (c->ser == 0 && c->tab.on && c->d_gpart && adj_t_smem(c) <= 227 * 1024 && !getenv_flag("GPAIR_ADJ_TAB_OLD")) {
             switch (c->k.cnt_int) {
                 case 12: return adj_t_launch<12, MODE>(c, resid, ep, st);

@@ -469,8 +469,24 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     }
 
     // ---- workspaces
-    if (c->ser == 0 && c->tab.on)  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t)
+    if (c->ser == 0 && c->tab.on) {  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t / k_adjoint_lcf)
         SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 255) / 256) * c->Mpad));
+        // lane-centred factorisation table G(tau) = 2^{K tau^2}, tau = t - La/2, in fp64
+        const double Kd = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
+        const int La = c->La, T = La / 2;
+        const double tmax = (double)std::max(T, La - T);
+        if (std::fabs(Kd) * tmax * tmax <= 90.0) {
+            std::vector<float> g(2 * (size_t)La);
+            for (int t = 0; t < La; ++t) {
+                const double tau = (double)(t - T);
+                g[t] = (float)std::exp2(Kd * tau * tau);
+                g[La + t] = (float)std::exp2(-Kd * tau * tau);
+            }
+            SETUP_CHECK(dmalloc(c, &c->d_gtab, g.size()));
+            SETUP_CHECK(cudaMemcpyAsync(c->d_gtab, g.data(), g.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+            SETUP_CHECK(cudaStreamSynchronize(st));
+        }
+    }
     SETUP_CHECK(dmalloc(c, &c->d_partial, (size_t)c->f_regions * Nd * c->Lf));
     SETUP_CHECK(dmalloc(c, &c->d_amp, c->Mpad));
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
