@@ -165,6 +165,10 @@ typedef struct {
     int32_t general;            /* 1: per-kernel sigma and/or near-field path (row f4)   */
     int32_t near_rows;          /* sensors with near-field pairs                        */
     int64_t near_pairs;         /* pairs evaluated with both Eq. 6 terms (r < k sigma_i) */
+    int32_t tab;                /* 1: factorised-Gaussian (TAB) forward path, 3 MUFU per pair */
+    int32_t adj_kernel;         /* adjoint kernel: 0 = lane per kernel (k_adjoint),
+                                   1 = sensor lanes + TAB (k_adjoint_t),
+                                   2 = sensor lanes + lane-centred factorisation (k_adjoint_lcf) */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial

@@ -28,13 +28,19 @@ thread_local std::string g_static_err;
 // precision (a 20-bit table measured 1e-3 elementwise at cfg4).  Enabled for
 // full windows of W = cnt_int samples with W % 4 == 0 and TAB_MIN <= W <=
 // TAB_MAX (the per-pair chain then spans |m| <= 16);
-// GPAIR_NO_TAB=1 in the environment keeps the per-sample MUFU path (A/B runs).
+// GPAIR_NO_TAB=1 in the environment keeps the per-sample MUFU path, GPAIR_ADJ_NO_LCF=1 /
+// GPAIR_ADJ_NO_T=1 skip the LCF / sensor-lane adjoints (A/B runs and the fallback tests).
 void build_tab(gpair_ctx* c) {
     gpair::TabConst t{};
     const gpair::OpConst& k = c->k;
     const int W = k.cnt_int;
-    const char* off = std::getenv("GPAIR_NO_TAB");
-    t.on = (W >= gpair::TAB_MIN && W % 4 == 0 && W <= gpair::TAB_MAX && !k.gen && !(off && off[0] == '1')) ? 1 : 0;
+    auto env1 = [](const char* n) {
+        const char* v = std::getenv(n);
+        return v && v[0] == '1';
+    };
+    c->dbg = (env1("GPAIR_NO_TAB") ? gpair::DBG_NO_TAB : 0) | (env1("GPAIR_ADJ_NO_LCF") ? gpair::DBG_ADJ_NO_LCF : 0) |
+             (env1("GPAIR_ADJ_NO_T") ? gpair::DBG_ADJ_NO_T : 0);
+    t.on = (W >= gpair::TAB_MIN && W % 4 == 0 && W <= gpair::TAB_MAX && !k.gen && !(c->dbg & gpair::DBG_NO_TAB)) ? 1 : 0;
     t.K = k.K1u;
     t.m2K = -2.0f * k.K1u;
     t.kappa = (float)(-2.0 * (double)k.K1u * 0.6931471805599453);
@@ -436,6 +442,8 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->general = c->gen;
     o->near_rows = c->n_near_rows;
     o->near_pairs = c->n_near;
+    o->tab = (c->ser == 0 && c->tab.on) ? 1 : 0;
+    o->adj_kernel = c->assa ? 0 : gpair::adjoint_kernel(c);
     return GPAIR_OK;
 }
 

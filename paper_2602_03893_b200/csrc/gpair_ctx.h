@@ -17,6 +17,7 @@ struct gpair_ctx_s {
     int device = 0;
     gpair::OpConst k{};
     gpair::TabConst tab{};  // factorised-Gaussian table of the TAB fast path (on = 0: per-sample MUFU path)
+    int dbg = 0;            // DBG_* switches (GPAIR_NO_TAB, GPAIR_ADJ_NO_LCF, GPAIR_ADJ_NO_T = 1)
     int64_t M = 0, Mpad = 0;
     int32_t ncells = 0, Nd = 0, Nt = 0;
     int32_t rank = 0, world = 1;
@@ -150,7 +151,12 @@ __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const Ep
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 int pick_wmax(int w);
-bool getenv_flag(const char* name);
+// adjoint kernel of a context: 0 = k_adjoint (lane = kernel), 1 = k_adjoint_t (TAB, sensor lanes),
+// 2 = k_adjoint_lcf (lane-centred factorisation)
+enum { ADJ_LANE_KERNEL = 0, ADJ_TAB_T = 1, ADJ_LCF = 2 };
+int adjoint_kernel(const gpair_ctx* c);
+// debug / A-B switches read once at create from the environment
+enum { DBG_NO_TAB = 1, DBG_ADJ_NO_LCF = 2, DBG_ADJ_NO_T = 4 };
 
 // ASSA operator (gpair_assa.cu)
 size_t assa_forward_smem(const gpair_ctx* c, int Lf);

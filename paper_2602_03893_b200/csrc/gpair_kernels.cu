@@ -116,10 +116,9 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
     float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
     float4* s_ks = (float4*)(s_amp + STAGE_CELLS * CELL);   // [STAGE_CELLS*32] (GEN only)
-    float* s_kx = (float*)s_kd;                             // FAST SoA views
-    float* s_ky = s_kx + STAGE_CELLS * CELL;
-    float* s_kz = s_ky + STAGE_CELLS * CELL;
-    float* s_kw = s_kz + STAGE_CELLS * CELL;
+    // FAST: kernel pairs interleaved, s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
+    float* s_kxy = (float*)s_kd;
+    float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_acc = (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0)) + (size_t)warp * Lf * 32;
     float* s_acc_lane = s_acc + lane;
@@ -143,10 +142,11 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             const float4 v = kd[(int64_t)cb * CELL + t];
             if (FAST) {
-                s_kx[t] = v.x;
-                s_ky[t] = v.y;
-                s_kz[t] = v.z;
-                s_kw[t] = v.w;
+                const int pb = (t >> 1) * 4 + (t & 1);
+                s_kxy[pb] = v.x;
+                s_kxy[pb + 2] = v.y;
+                s_kzw[pb] = v.z;
+                s_kzw[pb + 2] = v.w;
             } else {
                 s_kd[t] = v;
             }
@@ -172,8 +172,9 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
 #pragma unroll 1
                     for (int t = 0; t < GROUP; t += 2) {
                         const int li = gq * GROUP + t;
-                        const f2_t kx = *(const f2_t*)(s_kx + li), ky = *(const f2_t*)(s_ky + li);
-                        const f2_t kz = *(const f2_t*)(s_kz + li), kw = *(const f2_t*)(s_kw + li);
+                        const float4 pxy = *(const float4*)(s_kxy + 2 * li), pzw = *(const float4*)(s_kzw + 2 * li);
+                        const f2_t kx = pk2(pxy.x, pxy.y), ky = pk2(pxy.z, pxy.w);
+                        const f2_t kz = pk2(pzw.x, pzw.y), kw = pk2(pzw.z, pzw.w);
                         const f2_t A2 = *(const f2_t*)(s_amp + li);
                         const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                         const f2_t eps = mul2(q, iR2);
@@ -246,7 +247,8 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                 const int64_t gi = (int64_t)cb * CELL + li;
                 PairWin p;
                 float K1 = k.K1u;
-                const float4 kdt = FAST ? make_float4(s_kx[li], s_ky[li], s_kz[li], s_kw[li]) : kdg[t];
+                const int pb = (li >> 1) * 4 + (li & 1);
+                const float4 kdt = FAST ? make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]) : kdg[t];
                 if (GEN) {
                     const float4 ks4 = s_ks[li];
                     p = pair_gen(a, kdt, ampg[t], ks4, orig, gi, Mpad, sx, sy, sz, k);
@@ -566,25 +568,6 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     adjoint_epilogue<MODE>(acc, ic, ep);
 }
 
-// ------------------------------------------------------------------ adjoint, TAB path
-// Same decomposition as k_adjoint (lane = kernel, warp = one 32-kernel cell,
-// CTA = region of cells, sensors in batches of 32) for the common
-// configuration (degree-2 series, full windows of W = cnt_int samples,
-// TabConst on).  Per pair g_i += w E sum_m r^m Q_m(u_c) delta[n_c + m]
-// (gpair_internal.cuh TabConst), evaluated as two Horner chains in r^2 / s^2
-// (m >= 0 / m < 0) over (even, odd) sample pairs:
-//   * sensors are taken two at a time and set up in f32x2 (anchors staged in
-//     smem as sensor pairs, so each field is one 64-bit operand);
-//   * residual rows are staged "doubled", D[o] = (delta[lo+o], delta[lo+o+1]),
-//     so every lane reads its (even, odd) sample pairs with one aligned LDS.64
-//     whatever the parity of its window start;
-//   * no MUFU per sample: 2 per pair (E), plus the polynomial r, s.
-// Rare pairs (ambiguous window edges, record clipping, exact-ToF groups) take
-// pair_setup<2> and the per-sample loop, as in k_adjoint.
-__device__ __forceinline__ int s_wlo_read(const int32_t* wl, int jj) { return wl[jj]; }
-constexpr int ANC_SLOT = 16;                     // floats per (group, sensor pair) slot
-constexpr int ANC_G = 16 * ANC_SLOT + 4;         // floats per group (+16 B: groups on different banks)
-
 // ------------------------------------------------------------------ adjoint, TAB path, sensor lanes
 // The adjoint with the forward's decomposition: lane = sensor j, warp = 32
 // sensors, CTA = adjoint region of cells x 256 sensors (blockIdx.y = sensor
@@ -848,11 +831,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                                                        int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
                                                        float K, float m2K) {
     extern __shared__ float4 smem4[];
-    float* s_kx = (float*)smem4;                        // [STAGE_CELLS*32] SoA kernel offsets
-    float* s_ky = s_kx + STAGE_CELLS * CELL;
-    float* s_kz = s_ky + STAGE_CELLS * CELL;
-    float* s_kw = s_kz + STAGE_CELLS * CELL;
-    float4* s_grp = (float4*)(s_kw + STAGE_CELLS * CELL);  // [STAGE_CELLS*GPC]
+    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
+    float* s_kxy = (float*)smem4;
+    float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
+    float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
     float* s_gt = s_g + nw * STAGE_CELLS * CELL;          // [2][La]: G(t - T), 1 / G(t - T)
@@ -890,10 +872,11 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
         __syncthreads();
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             const float4 v = kd[(int64_t)cb * CELL + t];
-            s_kx[t] = v.x;
-            s_ky[t] = v.y;
-            s_kz[t] = v.z;
-            s_kw[t] = v.w;
+            const int pb = (t >> 1) * 4 + (t & 1);
+            s_kxy[pb] = v.x;
+            s_kxy[pb + 2] = v.y;
+            s_kzw[pb] = v.z;
+            s_kzw[pb + 2] = v.w;
         }
         if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
         __syncthreads();
@@ -917,8 +900,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                 if (!exact_grp) {
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
-                        const f2_t kx = *(const f2_t*)(s_kx + li + 2 * h), ky = *(const f2_t*)(s_ky + li + 2 * h);
-                        const f2_t kz = *(const f2_t*)(s_kz + li + 2 * h), kw = *(const f2_t*)(s_kw + li + 2 * h);
+                        const float4 pxy = *(const float4*)(s_kxy + 2 * (li + 2 * h));
+                        const float4 pzw = *(const float4*)(s_kzw + 2 * (li + 2 * h));
+                        const f2_t kx = pk2(pxy.x, pxy.y), ky = pk2(pxy.z, pxy.w);
+                        const f2_t kz = pk2(pzw.x, pzw.y), kw = pk2(pzw.z, pzw.w);
                         const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                         const f2_t eps = mul2(q, iR2);
                         const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
@@ -1007,7 +992,8 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                         float g = 0.f;
                         if (lo_j >= 0) {
                             const int64_t gi = (int64_t)cb * CELL + li + h;
-                            const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
+                            const int pb = ((li + h) >> 1) * 4 + ((li + h) & 1);
+                            const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
                             const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
                             float part = 0.f;
                             const int oo = pw.n_lo - lo_j;
@@ -1064,233 +1050,7 @@ __global__ void k_adj_gather(const float* __restrict__ gpart, int32_t ngroups, c
     adjoint_epilogue<MODE>(acc, ic, ep);
 }
 
-// cp.async (4 B, L1-allocating) for the residual rows of the next sensor batch
-__device__ __forceinline__ void cp_async4(void* dst_smem, const void* src) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-// Issue the raw residual rows of sensor batch jb (window starts in wl[32])
-// into raw[32][RAWW] (zero-filled outside [0, N_t) and for empty windows).
-constexpr int RAWW = 64;  // raw row capacity: La + 1 <= RAWW
-__device__ __forceinline__ void adj_issue_rows(float* raw, const int32_t* wl, const float* __restrict__ resid, int jb,
-                                               int nj, int La, int Nt, int nw, int warp, int lane) {
-    for (int jj = warp; jj < 32; jj += nw) {
-        const int lo = jj < nj ? wl[jj] : -1;
-        const float* src = resid + (int64_t)(jb + jj) * Nt;
-        for (int o = lane; o <= La; o += 32) {
-            const int n = lo + o;
-            if (lo >= 0 && n < Nt)
-                cp_async4(raw + jj * RAWW + o, src + n);
-            else
-                raw[jj * RAWW + o] = 0.f;
-        }
-    }
-}
-
-#ifndef GPAIR_ADJ_MINB
-#define GPAIR_ADJ_MINB 4
-#endif
-template <int W, int MODE>
-__global__ void __launch_bounds__(256, GPAIR_ADJ_MINB) k_adjoint_tab(const float4* __restrict__ kd, const float4* __restrict__ grp,
-                                                       const float* __restrict__ orig, const int32_t* __restrict__ perm,
-                                                       const float* __restrict__ sens, const int32_t* __restrict__ wlo,
-                                                       const float* __restrict__ resid, int32_t cpr, int32_t ncells,
-                                                       int32_t La, int64_t Mpad, OpConst k, EpiParams ep,
-                                                       const TabConst tab) {
-    constexpr int C = W / 2;
-    extern __shared__ float4 smem4[];
-    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_anc = (float*)smem4;                              // [nw][GPC][ANC_G]
-    float4* s_sen = (float4*)(s_anc + nw * GPC * ANC_G);       // [32]
-    int32_t* s_wlo = (int32_t*)(s_sen + 32);                   // [3][32] window starts, batch b in slot b % 3
-    float* s_raw = (float*)(s_wlo + 96);                       // [32][RAWW] raw rows of the next batch
-    f2_t* s_res2 = (f2_t*)(s_raw + 32 * RAWW);                 // [32][La] doubled rows of the current batch
-
-    const int cid = blockIdx.x * cpr + warp;
-    const bool cok = (warp < cpr) && (cid < ncells);
-    const int64_t gi = (int64_t)cid * CELL + lane;
-    float4 d4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (cok) d4 = kd[gi];
-    const f2_t kx = pk2(d4.x, d4.x), ky = pk2(d4.y, d4.y), kz = pk2(d4.z, d4.z), kw = pk2(d4.w, d4.w);
-    const float* my_anc = s_anc + (warp * GPC + lane / GROUP) * ANC_G;
-    const int32_t* wl_reg = wlo + (int64_t)blockIdx.x * k.Nd;
-
-    // prologue: window starts of batches 0 (and 1), raw rows of batch 0
-    for (int j = threadIdx.x; j < 64; j += blockDim.x)  // batch 0: [0, 32), batch 1: [32, 64)
-        s_wlo[j] = j < k.Nd ? wl_reg[j] : -1;
-    __syncthreads();
-    adj_issue_rows(s_raw, s_wlo, resid, 0, min(32, k.Nd), La, k.Nt, nw, warp, lane);
-    cp_async_commit();
-
-    float acc = 0.f;
-    for (int jb = 0; jb < k.Nd; jb += 32) {
-        const int nj = min(32, k.Nd - jb);
-        const int cur = (jb >> 5) % 3;
-        const int32_t* wl = s_wlo + cur * 32;
-        cp_async_wait_all();
-        __syncthreads();  // raw rows of this batch landed; previous batch's compute done
-        // doubled rows D[o] = (delta[lo+o], delta[lo+o+1]) from the raw rows
-        for (int jj = warp; jj < 32; jj += nw)
-            for (int o = lane; o < La; o += 32) s_res2[jj * La + o] = pk2(s_raw[jj * RAWW + o], s_raw[jj * RAWW + o + 1]);
-        if (threadIdx.x < nj) {
-            const int js = jb + threadIdx.x;
-            s_sen[threadIdx.x] = make_float4(sens[js], sens[k.Nd + js], sens[2 * k.Nd + js], 0.f);
-        }
-        if (cok) {
-            // lane = sensor: fp64 anchors of this cell's 4 groups, written as sensor pairs
-            const int j = jb + min(lane, nj - 1);
-            const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
-            float* slot = s_anc + warp * GPC * ANC_G + (lane >> 1) * ANC_SLOT + (lane & 1);
-#pragma unroll
-            for (int gq = 0; gq < GPC; ++gq) {
-                const Anchor a = make_anchor(grp[(int64_t)cid * GPC + gq], sx, sy, sz, k);
-                float* o = slot + gq * ANC_G;
-                o[0] = a.Ux;
-                o[2] = a.Uy;
-                o[4] = a.Uz;
-                o[6] = a.Eu;
-                o[8] = a.invR2;
-                o[10] = a.inv2Rh;
-                o[12] = a.h2R;
-                o[14] = __int_as_float(a.na);
-            }
-        }
-        __syncthreads();  // s_res2 / anchors ready, s_raw free
-        // prefetch: window starts of batch + 2, raw rows of batch + 1 (lands during this batch)
-        if (jb + 32 < k.Nd) {
-            if (threadIdx.x < 32) {  // slot of batch b - 1 (its compute ended before this batch's first barrier)
-                const int j = jb + 64 + threadIdx.x;
-                s_wlo[((cur + 2) % 3) * 32 + threadIdx.x] = j < k.Nd ? wl_reg[j] : -1;
-            }
-            adj_issue_rows(s_raw, s_wlo + ((cur + 1) % 3) * 32, resid, jb + 32, min(32, k.Nd - jb - 32), La, k.Nt, nw,
-                           warp, lane);
-        }
-        cp_async_commit();
-        if (!cok) continue;
-        float accb = 0.f;
-        const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
-        const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
-        const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
-        const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-#pragma unroll 1
-        for (int p = 0; p < 16; ++p) {
-            const int jj0 = 2 * p;
-            if (jj0 >= nj) break;
-            int lo0 = s_wlo_read(wl, jj0), lo1 = jj0 + 1 < nj ? s_wlo_read(wl, jj0 + 1) : -1;
-            if (lo0 < 0 && lo1 < 0) continue;
-            const float4* sl = (const float4*)(my_anc + p * ANC_SLOT);
-            const float4 v0 = sl[0], v1 = sl[1], v2 = sl[2], v3 = sl[3];
-            const f2_t Ux = pk2(v0.x, v0.y), Uy = pk2(v0.z, v0.w), Uz = pk2(v1.x, v1.y), Eu = pk2(v1.z, v1.w);
-            const f2_t iR2 = pk2(v2.x, v2.y), i2Rh = pk2(v2.z, v2.w), h2R = pk2(v3.x, v3.y);
-            const int na0 = __float_as_int(v3.z), na1 = __float_as_int(v3.w);
-            const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
-            const f2_t eps = mul2(q, iR2);
-            const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
-            const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
-            const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
-            const f2_t w = mul2(h2R, Tw);
-            const f2_t x = add2(eu, clo);
-            const f2_t tt = add2(x, mag);
-            const f2_t fl = add2(tt, nmag);
-            const f2_t d = sub2(x, fl);
-            const f2_t ulo = sub2(eu, add2(fl, one));
-            float d0, d1, t0, t1;
-            upk2(d, d0, d1);
-            upk2(tt, t0, t1);
-            const int n0 = __float_as_int(t0) + na0 - (RND_MAGIC_BITS - 1);
-            const int n1 = __float_as_int(t1) + na1 - (RND_MAGIC_BITS - 1);
-            const bool bad0 = lo0 >= 0 && (na0 == NA_EXACT || fabsf(d0) > 0.5f - GAMMA || (unsigned)n0 > span);
-            const bool bad1 = lo1 >= 0 && (na1 == NA_EXACT || fabsf(d1) > 0.5f - GAMMA || (unsigned)n1 > span);
-            if (!(bad0 || bad1)) {
-                const f2_t uc = add2(ulo, pk2(-(float)C, -(float)C));
-                f2_t r2p, s2p;
-                tab_rs(uc, tab, r2p, s2p);
-                float e0, e1, P00, P01, uc0, uc1, r0, r1, s0, s1;
-                upk2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), e0, e1);
-                upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), P00, P01);
-                upk2(uc, uc0, uc1);
-                upk2(r2p, r0, r1);
-                upk2(s2p, s0, s1);
-                // an empty half contributes 0 and reads a valid row
-                if (lo0 < 0) P00 = 0.f;
-                if (lo1 < 0) P01 = 0.f;
-                const f2_t* rp0 = s_res2 + jj0 * La + (lo0 >= 0 ? n0 - lo0 : 0);
-                const f2_t* rp1 = s_res2 + (jj0 + 1) * La + (lo1 >= 0 ? n1 - lo1 : 0);
-                const f2_t U0 = pk2(uc0, uc0), U1 = pk2(uc1, uc1);
-                const float rr0 = r0 * r0, ss0 = s0 * s0, rr1 = r1 * r1, ss1 = s1 * s1;
-                // both pairs interleaved: one table read per sample pair, two Horner chains each way
-                f2_t Q0 = fma2(U0, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
-                f2_t Q1 = fma2(U1, tab.c2[(W - 2) / 2], tab.d2[(W - 2) / 2]);
-                f2_t Sh0 = mul2(Q0, rp0[W - 2]), Sh1 = mul2(Q1, rp1[W - 2]);
-#pragma unroll
-                for (int i = W - 4; i >= C; i -= 2) {
-                    Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
-                    Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
-                    Sh0 = fma2(Sh0, pk2(rr0, rr0), mul2(Q0, rp0[i]));
-                    Sh1 = fma2(Sh1, pk2(rr1, rr1), mul2(Q1, rp1[i]));
-                }
-                Q0 = fma2(U0, tab.c2[0], tab.d2[0]);
-                Q1 = fma2(U1, tab.c2[0], tab.d2[0]);
-                f2_t Th0 = mul2(Q0, rp0[0]), Th1 = mul2(Q1, rp1[0]);
-#pragma unroll
-                for (int i = 2; i < C; i += 2) {
-                    Q0 = fma2(U0, tab.c2[i / 2], tab.d2[i / 2]);
-                    Q1 = fma2(U1, tab.c2[i / 2], tab.d2[i / 2]);
-                    Th0 = fma2(Th0, pk2(ss0, ss0), mul2(Q0, rp0[i]));
-                    Th1 = fma2(Th1, pk2(ss1, ss1), mul2(Q1, rp1[i]));
-                }
-                float se0, so0, te0, to0, se1, so1, te1, to1;
-                upk2(Sh0, se0, so0);
-                upk2(Th0, te0, to0);
-                upk2(Sh1, se1, so1);
-                upk2(Th1, te1, to1);
-                accb = fmaf(P00, fmaf(s0, to0, fmaf(ss0, te0, fmaf(r0, so0, se0))), accb);
-                accb = fmaf(P01, fmaf(s1, to1, fmaf(ss1, te1, fmaf(r1, so1, se1))), accb);
-            } else {
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    const int lo = h ? lo1 : lo0;
-                    if (lo < 0) continue;
-                    const int jj = jj0 + h;
-                    Anchor a;
-                    a.Ux = h ? v0.y : v0.x;
-                    a.Uy = h ? v0.w : v0.z;
-                    a.Uz = h ? v1.y : v1.x;
-                    a.Eu = h ? v1.w : v1.z;
-                    a.invR2 = h ? v2.y : v2.x;
-                    a.inv2Rh = h ? v2.w : v2.z;
-                    a.h2R = h ? v3.y : v3.x;
-                    a.na = h ? na1 : na0;
-                    const float4 sp = s_sen[jj];
-                    const PairWin pw = pair_setup<2>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
-                    if (pw.cnt <= 0) continue;
-                    const float* rq = (const float*)(s_res2 + jj * La + (pw.n_lo - lo));  // .x of D[o] = delta[lo+o]
-                    float part = 0.f;
-                    for (int m = 0; m < pw.cnt; ++m) {
-                        const float um = pw.u_lo - (float)m;
-                        part = fmaf(um * ex2f((um * k.K1u) * um), rq[2 * m], part);
-                    }
-                    accb = fmaf(pw.w, part, accb);
-                }
-            }
-        }
-        acc += accb;
-    }
-    cp_async_wait_all();
-    if (!cok) return;
-    const int32_t ic = perm[gi];
-    if (ic < 0) return;
-    adjoint_epilogue<MODE>(acc, ic, ep);
-}
-
 }  // namespace
-bool getenv_flag(const char* name) {
-    const char* v = std::getenv(name);
-    return v && v[0] == '1';
-}
 int pick_wmax(int w) {
     static const int opts[] = {5, 8, 12, 16, 20, 24, 32, 48, 64};
     for (int o : opts)
@@ -1324,19 +1084,6 @@ cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cu
     k_adjoint<W, SER, MODE><<<c->a_regions, threads, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
                                                            c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
                                                            c->k, ep, c->d_count, c->d_ksig);
-    return cudaGetLastError();
-}
-
-template <int W, int MODE>
-cudaError_t adj_tab_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
-    const int nw = std::max(c->a_cpr, 1);
-    size_t smem = (size_t)nw * GPC * ANC_G * 4 + 32 * 16 + 96 * 4 + (size_t)32 * RAWW * 4 + (size_t)32 * c->La * 8;
-    cudaError_t e = cudaFuncSetAttribute(k_adjoint_tab<W, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    ++c->n_launch;
-    k_adjoint_tab<W, MODE><<<c->a_regions, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_perm, c->d_sens,
-                                                             c->d_wlo_a, resid, c->a_cpr, c->ncells, c->La, c->Mpad,
-                                                             c->k, ep, c->tab);
     return cudaGetLastError();
 }
 
@@ -1417,12 +1164,25 @@ cudaError_t adj_dispatch_gen(gpair_ctx* c, const float* resid, const EpiParams& 
     }
 }
 
+}  // namespace
+
+// Which adjoint kernel a context uses (gpair_info.adj_kernel).
+int adjoint_kernel(const gpair_ctx* c) {
+    if (c->ser == SER_GEN) return ADJ_LANE_KERNEL;
+    if (c->ser == 0 && c->tab.on && c->d_gpart) {
+        if (c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_LCF)) return ADJ_LCF;
+        if (adj_t_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_T)) return ADJ_TAB_T;
+    }
+    return ADJ_LANE_KERNEL;
+}
+
+namespace {
+
 template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
-        if (c->ser == 0 && c->tab.on && c->d_gpart && c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 &&
-            !getenv_flag("GPAIR_ADJ_NO_LCF")) {
+        if (adjoint_kernel(c) == ADJ_LCF) {
             switch (c->k.cnt_int) {
                 case 12: return adj_lcf_launch<12, MODE>(c, resid, ep, st);
                 case 16: return adj_lcf_launch<16, MODE>(c, resid, ep, st);
@@ -1432,23 +1192,13 @@ cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
                 default: break;
             }
         }
-        if (c->ser == 0 && c->tab.on && c->d_gpart && adj_t_smem(c) <= 227 * 1024 && !getenv_flag("GPAIR_ADJ_TAB_OLD")) {
+        if (adjoint_kernel(c) == ADJ_TAB_T) {
             switch (c->k.cnt_int) {
                 case 12: return adj_t_launch<12, MODE>(c, resid, ep, st);
                 case 16: return adj_t_launch<16, MODE>(c, resid, ep, st);
                 case 20: return adj_t_launch<20, MODE>(c, resid, ep, st);
                 case 24: return adj_t_launch<24, MODE>(c, resid, ep, st);
                 case 32: return adj_t_launch<32, MODE>(c, resid, ep, st);
-                default: break;
-            }
-        }
-        if (c->ser == 0 && c->tab.on && c->La + 1 <= RAWW) {
-            switch (c->k.cnt_int) {
-                case 12: return adj_tab_launch<12, MODE>(c, resid, ep, st);
-                case 16: return adj_tab_launch<16, MODE>(c, resid, ep, st);
-                case 20: return adj_tab_launch<20, MODE>(c, resid, ep, st);
-                case 24: return adj_tab_launch<24, MODE>(c, resid, ep, st);
-                case 32: return adj_tab_launch<32, MODE>(c, resid, ep, st);
                 default: break;
             }
         }

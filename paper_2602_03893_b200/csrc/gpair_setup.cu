@@ -447,8 +447,6 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         SETUP_CHECK(cudaStreamSynchronize(st));
         int La = (std::max(h_flags[6], 1) + 3) / 4 * 4;
         size_t smem = (size_t)32 * La * 4 + (size_t)acpr * GPC * 33 * sizeof(Anchor) + 32 * 4;
-        // TAB adjoint (k_adjoint_tab): sensor-pair anchor slots + doubled residual rows
-        smem = std::max(smem, (size_t)acpr * GPC * (16 * 16 + 4) * 4 + 32 * 28 + 32 * 64 * 4 + (size_t)32 * La * 8);
         if (smem > 96 * 1024 && acpr > 1) {
             cudaFree(wlo);
             acpr /= 2;

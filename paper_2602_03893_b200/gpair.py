@@ -92,6 +92,8 @@ class Info(ctypes.Structure):
         ("general", ctypes.c_int32),
         ("near_rows", ctypes.c_int32),
         ("near_pairs", ctypes.c_int64),
+        ("tab", ctypes.c_int32),
+        ("adj_kernel", ctypes.c_int32),
     ]
 
     def as_dict(self):
