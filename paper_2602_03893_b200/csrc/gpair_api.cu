@@ -442,7 +442,7 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->general = c->gen;
     o->near_rows = c->n_near_rows;
     o->near_pairs = c->n_near;
-    o->tab = (c->ser == 0 && c->tab.on) ? 1 : 0;
+    o->tab = ((c->ser == 0 || c->ser == gpair::SER_FAST5) && c->tab.on) ? 1 : 0;
     o->adj_kernel = c->assa ? 0 : gpair::adjoint_kernel(c);
     return GPAIR_OK;
 }

@@ -26,7 +26,7 @@ struct gpair_ctx_s {
     int grid_detected = 0;
     double max_eps = 0.0;
     int series_small = 0;  // 1: every group's |eps| <= EPS_SMALL -> degree-2 series
-    int ser = 5;           // kernel path: 0 = pair_fast, 2 / 5 = pair_setup<SER> (gpair_kernels.cu)
+    int ser = 5;           // kernel path: 0 / SER_FAST5 = packed fast path (degree 2 / 5), 2 / 5 = pair_setup<SER>
     int assa = 0;          // 1: ASSA operator (row f1, gpair_assa.cu)
     float* d_taps = nullptr;   // [2K+1] ASSA taps h[k + K] (fp64-computed, fp32)
     float* d_dconv = nullptr;  // [Nd][alpha Nt] ASSA adjoint correlation buffer

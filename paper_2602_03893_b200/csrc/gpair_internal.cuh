@@ -67,7 +67,8 @@ struct OpConst {
     double sigma;          // scalar sigma (fp64, as given)
 };
 
-constexpr int SER_GEN = 7;  // kernel path of the general operator (pair_gen)
+constexpr int SER_GEN = 7;    // kernel path of the general operator (pair_gen)
+constexpr int SER_FAST5 = 6;  // fast packed path (exact-integer window) with the degree-5 series (|eps| <= EPS_FAST)
 
 // Near-pair threshold of reading N1: pairs with r < thr are evaluated with
 // both terms of Eq. 6 by gpair_near.cu; the rest carry only the outgoing
@@ -565,6 +566,28 @@ __device__ __forceinline__ void tab_rs(f2_t uc, const TabConst& t, f2_t& r, f2_t
     const f2_t xS = mul2(x, S);
     r = add2(C, xS);
     s = sub2(C, xS);
+}
+
+// Packed (two pairs) series S(eps) of (sqrt(1+eps)-1)/(eps/2) and T(eps) of
+// (1+eps)^-1/2: degree 2 / 2 (SER 0, |eps| <= EPS_SMALL) or 5 / 4 (SER_FAST5,
+// |eps| <= EPS_FAST) -- the same polynomials as pair_setup<2> / pair_setup<5>.
+template <int DEG>
+__device__ __forceinline__ void series2(f2_t eps, f2_t& S, f2_t& Tw) {
+    const f2_t one = pk2(1.f, 1.f);
+    if (DEG <= 2) {
+        S = fma2(eps, fma2(eps, pk2(1.f / 8.f, 1.f / 8.f), pk2(-0.25f, -0.25f)), one);
+        Tw = fma2(eps, fma2(eps, pk2(3.f / 8.f, 3.f / 8.f), pk2(-0.5f, -0.5f)), one);
+    } else {
+        S = fma2(eps, pk2(-21.f / 512.f, -21.f / 512.f), pk2(7.f / 128.f, 7.f / 128.f));
+        S = fma2(eps, S, pk2(-5.f / 64.f, -5.f / 64.f));
+        S = fma2(eps, S, pk2(1.f / 8.f, 1.f / 8.f));
+        S = fma2(eps, S, pk2(-0.25f, -0.25f));
+        S = fma2(eps, S, one);
+        Tw = fma2(eps, pk2(35.f / 128.f, 35.f / 128.f), pk2(-5.f / 16.f, -5.f / 16.f));
+        Tw = fma2(eps, Tw, pk2(3.f / 8.f, 3.f / 8.f));
+        Tw = fma2(eps, Tw, pk2(-0.5f, -0.5f));
+        Tw = fma2(eps, Tw, one);
+    }
 }
 
 // Forward accumulate of one pair's W samples into its smem column (lane stride

@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                                  int32_t Lf, int64_t Mpad, OpConst k,
                                                  const float4* __restrict__ ksig, const TabConst tab) {
     constexpr bool GEN = SER == SER_GEN;
-    constexpr bool FAST = SER == 0;  // two pairs per setup in f32x2 (common configuration)
+    // two pairs per setup in f32x2 (exact-integer window length): degree-2 or degree-5 series
+    constexpr bool FAST = SER == 0 || SER == SER_FAST5;
+    constexpr int SDEG = SER == 0 ? 2 : 5;
     // factorised Gaussian (TabConst): 3 MUFU per pair instead of WMAX
     constexpr bool TABW = FAST && (WMAX % 4 == 0) && WMAX >= TAB_MIN && WMAX <= TAB_MAX;
     extern __shared__ float4 smem4[];
@@ -178,8 +180,8 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                         const f2_t A2 = *(const f2_t*)(s_amp + li);
                         const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                         const f2_t eps = mul2(q, iR2);
-                        const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
-                        const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                        f2_t S, Tw;
+                        series2<SDEG>(eps, S, Tw);
                         const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
                         const f2_t w = mul2(A2, mul2(h2R, Tw));
                         const f2_t x = add2(eu, clo);
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                     p = pair_gen(a, kdt, ampg[t], ks4, orig, gi, Mpad, sx, sy, sz, k);
                     K1 = ks4.y;
                 } else {
-                    p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, kdt, ampg[t], orig, gi, Mpad, sx, sy, sz, k);
+                    p = pair_setup<(SER == 0 || GEN) ? 2 : 5>(a, kdt, ampg[t], orig, gi, Mpad, sx, sy, sz, k);
                 }
                 acc_pair<WMAX>(s_acc_lane, lo_j, p, K1);
             }
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
             else if (SER == 0 && a.na != NA_EXACT)
                 p = pair_fast(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             else
-                p = pair_setup<(SER == 0 || GEN) ? 2 : SER>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
+                p = pair_setup<(SER == 0 || GEN) ? 2 : 5>(a, d4, 1.f, orig, gi, Mpad, sp.x, sp.y, sp.z, k);
             if (p.cnt <= 0) continue;
             if (MODE == MODE_COUNT) {
                 npairs += real ? (unsigned long long)p.cnt : 0ull;
@@ -590,7 +592,7 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
 #endif
 constexpr int ADJT_DBL = GPAIR_ADJT_DBL;  // 1: doubled residual column (one LDS.64 per sample pair)
 
-template <int W>
+template <int W, int SDEG>
 __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                      const float* __restrict__ orig, const float* __restrict__ sens,
                                                      const int32_t* __restrict__ wlo, const float* __restrict__ resid,
@@ -669,8 +671,8 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
                     const f2_t kz = *(const f2_t*)(s_kz + li), kw = *(const f2_t*)(s_kw + li);
                     const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                     const f2_t eps = mul2(q, iR2);
-                    const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
-                    const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                    f2_t S, Tw;
+                    series2<SDEG>(eps, S, Tw);
                     const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
                     const f2_t w = mul2(h2R, Tw);
                     const f2_t x = add2(eu, clo);
@@ -737,7 +739,7 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
                     for (int h = 0; h < 2; ++h) {
                         const int64_t gi = (int64_t)cb * CELL + li + h;
                         const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
-                        const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+                        const PairWin pw = pair_setup<SDEG>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
                         float part = 0.f;
                         const float* rq = ADJT_DBL ? (const float*)(col2 + (pw.n_lo - lo_j) * 32) : col + (pw.n_lo - lo_j) * 32;
                         for (int m = 0; m < pw.cnt; ++m) {
@@ -823,7 +825,7 @@ __device__ __forceinline__ f2_t exp2_acc2(f2_t x) {
     return pk2(p0, p1);
 }
 
-template <int W>
+template <int W, int SDEG>
 __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                        const float* __restrict__ orig, const float* __restrict__ sens,
                                                        const int32_t* __restrict__ wlo, const float* __restrict__ resid,
@@ -906,8 +908,8 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                         const f2_t kz = pk2(pzw.x, pzw.y), kw = pk2(pzw.z, pzw.w);
                         const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                         const f2_t eps = mul2(q, iR2);
-                        const f2_t S = fma2(eps, fma2(eps, c8, c4), one);
-                        const f2_t Tw = fma2(eps, fma2(eps, c38, c2), one);
+                        f2_t S, Tw;
+                        series2<SDEG>(eps, S, Tw);
                         eu[h] = fma2(mul2(q, i2Rh), S, Eu);
                         w[h] = mul2(h2R, Tw);
                         const f2_t x = add2(eu[h], clo);
@@ -994,7 +996,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                             const int64_t gi = (int64_t)cb * CELL + li + h;
                             const int pb = ((li + h) >> 1) * 4 + ((li + h) & 1);
                             const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
-                            const PairWin pw = pair_setup<2>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+                            const PairWin pw = pair_setup<SDEG>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
                             float part = 0.f;
                             const int oo = pw.n_lo - lo_j;
                             for (int m = 0; m < pw.cnt; ++m) {
@@ -1094,16 +1096,16 @@ size_t adj_t_smem(const gpair_ctx* c) {
            (size_t)ADJT_WARPS * c->La * 32 * 4 * (1 + ADJT_DBL);
 }
 
-template <int W, int MODE>
+template <int W, int MODE, int SDEG>
 cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     const int nw = ADJT_WARPS;
     const size_t smem = adj_t_smem(c);
-    cudaError_t e = cudaFuncSetAttribute(k_adjoint_t<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint_t<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
     dim3 grid(c->a_regions, ngroups);
     ++c->n_launch;
-    k_adjoint_t<W><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gpart,
+    k_adjoint_t<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gpart,
                                                 c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -1117,16 +1119,16 @@ size_t adj_lcf_smem(const gpair_ctx* c) {
            (size_t)2 * c->La * 4 + (size_t)ADJT_WARPS * c->La * 32 * 4;
 }
 
-template <int W, int MODE>
+template <int W, int MODE, int SDEG>
 cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     const int nw = ADJT_WARPS;
     const size_t smem = adj_lcf_smem(c);
-    cudaError_t e = cudaFuncSetAttribute(k_adjoint_lcf<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint_lcf<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
     dim3 grid(c->a_regions, ngroups);
     ++c->n_launch;
-    k_adjoint_lcf<W><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gtab,
+    k_adjoint_lcf<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gtab,
                                                   c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab.K,
                                                   c->tab.m2K);
     e = cudaGetLastError();
@@ -1169,7 +1171,7 @@ cudaError_t adj_dispatch_gen(gpair_ctx* c, const float* resid, const EpiParams& 
 // Which adjoint kernel a context uses (gpair_info.adj_kernel).
 int adjoint_kernel(const gpair_ctx* c) {
     if (c->ser == SER_GEN) return ADJ_LANE_KERNEL;
-    if (c->ser == 0 && c->tab.on && c->d_gpart) {
+    if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on && c->d_gpart) {
         if (c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_LCF)) return ADJ_LCF;
         if (adj_t_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_T)) return ADJ_TAB_T;
     }
@@ -1182,23 +1184,24 @@ template <int MODE>
 cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
+        const bool deg5 = c->ser == SER_FAST5;
         if (adjoint_kernel(c) == ADJ_LCF) {
             switch (c->k.cnt_int) {
-                case 12: return adj_lcf_launch<12, MODE>(c, resid, ep, st);
-                case 16: return adj_lcf_launch<16, MODE>(c, resid, ep, st);
-                case 20: return adj_lcf_launch<20, MODE>(c, resid, ep, st);
-                case 24: return adj_lcf_launch<24, MODE>(c, resid, ep, st);
-                case 32: return adj_lcf_launch<32, MODE>(c, resid, ep, st);
+                case 12: return deg5 ? adj_lcf_launch<12, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<12, MODE, 2>(c, resid, ep, st);
+                case 16: return deg5 ? adj_lcf_launch<16, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<16, MODE, 2>(c, resid, ep, st);
+                case 20: return deg5 ? adj_lcf_launch<20, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<20, MODE, 2>(c, resid, ep, st);
+                case 24: return deg5 ? adj_lcf_launch<24, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<24, MODE, 2>(c, resid, ep, st);
+                case 32: return deg5 ? adj_lcf_launch<32, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<32, MODE, 2>(c, resid, ep, st);
                 default: break;
             }
         }
         if (adjoint_kernel(c) == ADJ_TAB_T) {
             switch (c->k.cnt_int) {
-                case 12: return adj_t_launch<12, MODE>(c, resid, ep, st);
-                case 16: return adj_t_launch<16, MODE>(c, resid, ep, st);
-                case 20: return adj_t_launch<20, MODE>(c, resid, ep, st);
-                case 24: return adj_t_launch<24, MODE>(c, resid, ep, st);
-                case 32: return adj_t_launch<32, MODE>(c, resid, ep, st);
+                case 12: return deg5 ? adj_t_launch<12, MODE, 5>(c, resid, ep, st) : adj_t_launch<12, MODE, 2>(c, resid, ep, st);
+                case 16: return deg5 ? adj_t_launch<16, MODE, 5>(c, resid, ep, st) : adj_t_launch<16, MODE, 2>(c, resid, ep, st);
+                case 20: return deg5 ? adj_t_launch<20, MODE, 5>(c, resid, ep, st) : adj_t_launch<20, MODE, 2>(c, resid, ep, st);
+                case 24: return deg5 ? adj_t_launch<24, MODE, 5>(c, resid, ep, st) : adj_t_launch<24, MODE, 2>(c, resid, ep, st);
+                case 32: return deg5 ? adj_t_launch<32, MODE, 5>(c, resid, ep, st) : adj_t_launch<32, MODE, 2>(c, resid, ep, st);
                 default: break;
             }
         }
@@ -1241,6 +1244,7 @@ cudaError_t launch_forward(gpair_ctx* c, cudaStream_t st) {
             default: return fwd_launch<64, SER_GEN>(c, st);
         }
     }
+    if (c->ser == SER_FAST5) return fwd_dispatch<SER_FAST5>(c, st);
     return c->ser == 0 ? fwd_dispatch<0>(c, st) : (c->ser == 2 ? fwd_dispatch<2>(c, st) : fwd_dispatch<5>(c, st));
 }
 

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -148,7 +149,8 @@ __device__ __forceinline__ bool cell_window(float4 C, float sx, float sy, float 
 __global__ void k_region_windows(const float4* __restrict__ cell, const float4* __restrict__ grp, int32_t ncells,
                                  const float* __restrict__ sens, int32_t cpr, int32_t nregions,
                                  OpConst k, int32_t* wlo, int* maxlen, int check, int* geom_bad,
-                                 unsigned int* max_eps_bits) {
+                                 unsigned int* max_eps_bits, unsigned int* rmin_bits = nullptr,
+                                 unsigned int* rmax_bits = nullptr) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= (int64_t)nregions * k.Nd) return;
     int j = (int)(t % k.Nd);
@@ -156,6 +158,7 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
     float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
     int lo = INT_MAX, hi = INT_MIN;
     float eps_max = 0.f;
+    float rmin = 3.0e38f, rmax = 0.f;
     int bad = 0;
     int c1 = min((r + 1) * cpr, ncells);
     for (int cc = r * cpr; cc < c1; ++cc) {
@@ -175,6 +178,8 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
             R = sqrt(dx * dx + dy * dy + dz * dz);
         }
         if (check) {
+            rmin = fminf(rmin, (float)fmax(R - (double)C.w, 0.0));
+            rmax = fmaxf(rmax, (float)(R + (double)C.w));
             if (!k.nf && !(R - (double)C.w > k.ks)) bad = 1;  // near field: any r > 0 (row f4)
             for (int gq = 0; gq < GPC; ++gq) {  // anchor-expansion bound per 8-kernel group
                 const float4 G = grp[(int64_t)cc * GPC + gq];
@@ -196,8 +201,18 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
     if (check) {
         if (bad) atomicOr(geom_bad, 1);
         atomicMax(max_eps_bits, __float_as_uint(eps_max));
+        if (rmin_bits) atomicMin(rmin_bits, __float_as_uint(rmin));  // non-negative floats order as uints
+        if (rmax_bits) atomicMax(rmax_bits, __float_as_uint(rmax));
     }
 }
+
+// Forward regions of 512 kernels bound each fp32 partial to ~128 terms per
+// sample; when r_max / r_min over the geometry exceeds FWD_WIDE_RATIO (planar
+// near-field arrays, cfg5: ~18) the 1/r weights span enough that cancelling
+// partials exceed the 1e-4 elementwise bar (measured 1.3e-4 at cfg5), so the
+// regions shrink to FWD_CPR_WIDE cells (6.9e-5).
+constexpr int FWD_CPR_WIDE = 4;
+constexpr float FWD_WIDE_RATIO = 4.f;
 
 // Reducer table (gpair_kernels.cu k_reduce): per sensor j the forward regions
 // sorted by window start, as (lo, region) entries.  Regions with an empty
@@ -255,15 +270,15 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     const int Nd = c->Nd;
     auto pol = thrust::cuda::par.on(st);
 
-    SETUP_CHECK(dmalloc(c, &c->d_flags, 8));
+    SETUP_CHECK(dmalloc(c, &c->d_flags, 16));
     SETUP_CHECK(dmalloc(c, &c->d_count, 1));
-    SETUP_CHECK(cudaMemsetAsync(c->d_flags, 0, 8 * sizeof(int32_t), st));
+    SETUP_CHECK(cudaMemsetAsync(c->d_flags, 0, 16 * sizeof(int32_t), st));
     SETUP_CHECK(dmalloc(c, &c->d_sens, (size_t)3 * Nd));
     SETUP_CHECK(cudaMemcpyAsync(c->d_sens, sensors, sizeof(float) * 3 * Nd, cudaMemcpyDeviceToDevice, st));
     k_check_finite<<<(unsigned)((3 * M + 255) / 256), 256, 0, st>>>(centers, 3 * M, c->d_flags);
     k_check_finite<<<(unsigned)((3 * Nd + 255) / 256), 256, 0, st>>>(c->d_sens, 3 * Nd, c->d_flags);
     SETUP_CHECK(cudaGetLastError());
-    int h_flags[8];
+    int h_flags[16];
     SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
     SETUP_CHECK(cudaStreamSynchronize(st));
     if (h_flags[0]) {
@@ -353,6 +368,11 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     c->f_warps = std::min(c->assa ? assa_forward_warps() : 8, (Nd + 31) / 32);
     c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
     int cpr = 16;  // 512 kernels (8x8x8 on a grid): bounds fp32 accumulation chains
+    bool cpr_forced = false;
+    if (const char* ev = std::getenv("GPAIR_FWD_CPR")) {  // A/B experiments
+        cpr = std::max(1, std::min(16, atoi(ev)));
+        cpr_forced = true;
+    }
     while (cpr > 1 && (int64_t)((c->ncells + cpr - 1) / cpr) * c->f_sgroups < 4LL * dev_sms) cpr /= 2;
     const size_t smem_limit = 220 * 1024;
     for (;;) {
@@ -360,10 +380,12 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         int32_t* wlo = nullptr;
         SETUP_CHECK(cudaMalloc(&wlo, sizeof(int32_t) * (size_t)nreg * Nd));
         SETUP_CHECK(cudaMemsetAsync(c->d_flags + 2, 0, 6 * sizeof(int32_t), st));
+        SETUP_CHECK(cudaMemsetAsync(c->d_flags + 8, 0x7f, sizeof(int32_t), st));  // r_min bits (large)
+        SETUP_CHECK(cudaMemsetAsync(c->d_flags + 9, 0, sizeof(int32_t), st));     // r_max bits
         int64_t nt = (int64_t)nreg * Nd;
         k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
             c->d_cell, c->d_grp, c->ncells, c->d_sens, cpr, nreg, c->k, wlo, c->d_flags + 2, 1, c->d_flags + 3,
-            (unsigned int*)(c->d_flags + 4));
+            (unsigned int*)(c->d_flags + 4), (unsigned int*)(c->d_flags + 8), (unsigned int*)(c->d_flags + 9));
         SETUP_CHECK(cudaGetLastError());
         SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
         SETUP_CHECK(cudaStreamSynchronize(st));
@@ -374,12 +396,28 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
             geom_err = GPAIR_ERR_GEOMETRY;
             return cudaSuccess;
         }
+        {
+            // accumulation-chain bound: a wide spread of 1/r weights (near-field
+            // arrays) makes the fp32 region partials cancel more; use 128-kernel regions there
+            float rmn, rmx;
+            unsigned b0 = (unsigned)h_flags[8], b1 = (unsigned)h_flags[9];
+            memcpy(&rmn, &b0, 4);
+            memcpy(&rmx, &b1, 4);
+            if (cpr > FWD_CPR_WIDE && !cpr_forced && rmx > FWD_WIDE_RATIO * rmn) {
+                cudaFree(wlo);
+                cpr = FWD_CPR_WIDE;
+                continue;
+            }
+        }
         float me;
         unsigned bits = (unsigned)h_flags[4];
         memcpy(&me, &bits, 4);
         c->max_eps = me;
         c->series_small = me <= EPS_SMALL ? 1 : 0;
-        c->ser = c->series_small ? ((c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int) ? 0 : 2) : 5;
+        {
+            const bool cnt_ok = c->k.cnt_int > 0 && pick_wmax(c->k.cnt_int) == c->k.cnt_int;
+            c->ser = c->series_small ? (cnt_ok ? 0 : 2) : (cnt_ok ? SER_FAST5 : 5);
+        }
         if (c->gen) c->ser = SER_GEN;
         int L = std::max(h_flags[2], 1);
         int Lf = (L + 15) / 16 * 16;  // the flush transposes 32-row blocks plus a 16-row tail
@@ -467,7 +505,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     }
 
     // ---- workspaces
-    if (c->ser == 0 && c->tab.on) {  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t / k_adjoint_lcf)
+    if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on) {  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t / k_adjoint_lcf)
         SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 255) / 256) * c->Mpad));
         // lane-centred factorisation table G(tau) = 2^{K tau^2}, tau = t - La/2, in fp64
         const double Kd = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
