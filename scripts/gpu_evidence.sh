@@ -15,7 +15,7 @@ echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv \
     python bench.py --config $CFG --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list rc=$?"
-for K in k_forward k_adjoint_t "k_reduce\$"; do
+for K in k_forward k_adjoint_lcf "k_reduce\$"; do
   KN=$(echo "$K" | tr -d '$\\')
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -c 1 \
       -o gpurun_out/prof_${CFG}_${KN}_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${KN}_${TAG}.log 2>&1
