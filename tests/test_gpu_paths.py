@@ -141,3 +141,33 @@ def test_bench_configuration_uses_fast_paths(monkeypatch):
     info = ctx.info()
     assert info["tab"] == 1 and info["adj_kernel"] == 2, info
     ctx.close()
+
+
+# randomized geometries on the fast paths: W in {12, 16, 20, 24, 32} (sigma = W h / 6), grid or
+# jittered (non-grid sort) kernels, hemisphere or planar arrays, t0 > 0 and records that clip
+@pytest.mark.parametrize("seed", range(10))
+def test_fast_paths_random_geometry(seed, monkeypatch):
+    rng = np.random.default_rng(1000 + seed)
+    W = int(rng.choice([12, 16, 20, 24, 32]))
+    fs, v = 40e6, 1500.0
+    sigma = W * (v / fs) / 6.0
+    n = rng.integers(5, 13, size=3)
+    c = inputs.grid_centers(int(n[0]), int(n[1]), int(n[2]), sigma, jitter=0.4 if seed % 3 == 0 else 0.0, seed=seed)
+    if seed % 4 == 3:
+        s = inputs.planar_checkerboard(n_side=8, pitch=6e-3, z=-30e-3)
+    else:
+        s = inputs.hemisphere(int(rng.integers(20, 70)), float(rng.uniform(40e-3, 80e-3)))
+    t0 = float(rng.uniform(0.0, 15e-6))
+    rmax = float(np.max(np.linalg.norm(s[:, :, None] - c[:, None, :].mean(axis=2, keepdims=True), axis=0)))
+    n_samples = int((rmax / v - t0) * fs) + int(rng.integers(-8, 24))  # some windows reach past the record
+    op = dict(sigma=sigma, v=v, fs=fs, n_samples=n_samples, t0=t0, k=3.0)
+    ctx = make_ctx(c, s, op, monkeypatch, {})
+    info = ctx.info()
+    x = rng.random(c.shape[1]).astype(np.float32)
+    check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"seed {seed} W {W} forward")
+    d = rng.standard_normal((s.shape[1], n_samples)).astype(np.float32)
+    akw = {k: v for k, v in op.items() if k != "n_samples"}
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
+          elementwise=False)
+    assert info["tab"] == 1, info  # every case is on the fast (TAB) path
+    ctx.close()
