@@ -168,7 +168,8 @@ typedef struct {
     int32_t tab;                /* 1: factorised-Gaussian (TAB) forward path, 3 MUFU per pair */
     int32_t adj_kernel;         /* adjoint kernel: 0 = lane per kernel (k_adjoint),
                                    1 = sensor lanes + TAB (k_adjoint_t),
-                                   2 = sensor lanes + lane-centred factorisation (k_adjoint_lcf) */
+                                   2 = sensor lanes + lane-centred factorisation (k_adjoint_lcf),
+                                   3 = sensor lanes + per-sample exponential (k_adjoint_sl) */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial

@@ -152,8 +152,8 @@ cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const Epi
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 int pick_wmax(int w);
 // adjoint kernel of a context: 0 = k_adjoint (lane = kernel), 1 = k_adjoint_t (TAB, sensor lanes),
-// 2 = k_adjoint_lcf (lane-centred factorisation)
-enum { ADJ_LANE_KERNEL = 0, ADJ_TAB_T = 1, ADJ_LCF = 2 };
+// 2 = k_adjoint_lcf (lane-centred factorisation), 3 = k_adjoint_sl (sensor lanes, per-sample exponential)
+enum { ADJ_LANE_KERNEL = 0, ADJ_TAB_T = 1, ADJ_LCF = 2, ADJ_SL = 3 };
 int adjoint_kernel(const gpair_ctx* c);
 // debug / A-B switches read once at create from the environment
 enum { DBG_NO_TAB = 1, DBG_ADJ_NO_LCF = 2, DBG_ADJ_NO_T = 4 };

@@ -62,7 +62,7 @@ __device__ __forceinline__ void acc_packed(float* ap, float u_lo, float w, float
     const f2_t K2 = pk2(K1, K1), W2 = pk2(w, w), step = pk2(-2.f, -2.f);
     f2_t u2 = pk2(u_lo, u_lo - 1.f);
 #pragma unroll
-    for (int m = 0; m < WMAX; m += 2) {
+    for (int m = 0; m + 1 < WMAX; m += 2) {
         f2_t acc2 = pk2(ap[m * 32], ap[(m + 1) * 32]);
         acc2 = fma2(mul2(W2, u2), gauss2(u2, K2), acc2);
         float v0, v1;
@@ -70,6 +70,10 @@ __device__ __forceinline__ void acc_packed(float* ap, float u_lo, float w, float
         ap[m * 32] = v0;
         ap[(m + 1) * 32] = v1;
         u2 = add2(u2, step);
+    }
+    if (WMAX & 1) {  // odd window length: the last sample alone (exactly WMAX samples are in the window)
+        const float um = u_lo - (float)(WMAX - 1);
+        ap[(WMAX - 1) * 32] = fmaf(w * um, ex2f((um * K1) * um), ap[(WMAX - 1) * 32]);
     }
 }
 
@@ -1039,6 +1043,181 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
     }
 }
 
+// ------------------------------------------------------------------ adjoint, sensor lanes, per-sample exponential
+// k_adjoint_lcf's decomposition (lane = sensor, residual column per lane, fp64
+// anchor per group in registers, two kernels per f32x2 setup, warp
+// reduce-scatter, per-sensor-group partials) with one MUFU.EX2 per sample: the
+// fast adjoint for exact-integer windows outside the LCF range (W = 5 of cfg4',
+// W > 32 of the desk workload, or |K| (La/2)^2 > LCF_KMAX).
+template <int W, int SDEG>
+__global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict__ kd, const float4* __restrict__ grp,
+                                                       const float* __restrict__ orig, const float* __restrict__ sens,
+                                                       const int32_t* __restrict__ wlo, const float* __restrict__ resid,
+                                                       float* __restrict__ gpart,
+                                                       int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
+                                                       float K) {
+    const float m2K = -2.f * K;
+    extern __shared__ float4 smem4[];
+    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
+    float* s_kxy = (float*)smem4;
+    float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
+    float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    float* col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 + lane;  // this lane's column delta_t
+    const int region = blockIdx.x;
+    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const bool jok = j < k.Nd;
+    const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    if (jok) {
+        sx = sens[j];
+        sy = sens[k.Nd + j];
+        sz = sens[2 * k.Nd + j];
+    }
+    {
+        const float* src = resid + (int64_t)j * k.Nt;
+        for (int t = 0; t < La; ++t) {
+            const int n = lo_j + t;
+            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] : 0.f;
+        }
+    }
+    const int Tc = La >> 1;
+    const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
+    const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
+    const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
+    const f2_t K2 = pk2(K, K), M2K = pk2(m2K, m2K);
+    const unsigned span = (unsigned)(k.Nt - k.cnt_int);
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
+        const int nc = min(STAGE_CELLS, c1 - cb);
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            const float4 v = kd[(int64_t)cb * CELL + t];
+            const int pb = (t >> 1) * 4 + (t & 1);
+            s_kxy[pb] = v.x;
+            s_kxy[pb + 2] = v.y;
+            s_kzw[pb] = v.z;
+            s_kzw[pb + 2] = v.w;
+        }
+        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        __syncthreads();
+        for (int gq = 0; gq < nc * GPC; ++gq) {
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+            float gv[GROUP];
+            const bool exact_grp = __any_sync(0xffffffffu, a.na == NA_EXACT);
+            const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
+            const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
+            const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R);
+            const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // o = n_lo - lo_j = bits(tt) + nrel
+            const float cg = (float)(a.na - lo_j - Tc);            // a_pair = eu + cg (exact integer shift)
+            const f2_t CG = pk2(cg, cg);
+            // four kernels per step: two f32x2 packs whose Horner chains interleave (ILP)
+#pragma unroll
+            for (int t = 0; t < GROUP; t += 4) {
+                const int li = gq * GROUP + t;
+                bool rare = exact_grp;
+                f2_t eu[2], w[2], ulo[2];
+                int o[4];
+                if (!exact_grp) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float4 pxy = *(const float4*)(s_kxy + 2 * (li + 2 * h));
+                        const float4 pzw = *(const float4*)(s_kzw + 2 * (li + 2 * h));
+                        const f2_t kx = pk2(pxy.x, pxy.y), ky = pk2(pxy.z, pxy.w);
+                        const f2_t kz = pk2(pzw.x, pzw.y), kw = pk2(pzw.z, pzw.w);
+                        const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
+                        const f2_t eps = mul2(q, iR2);
+                        f2_t S, Tw;
+                        series2<SDEG>(eps, S, Tw);
+                        eu[h] = fma2(mul2(q, i2Rh), S, Eu);
+                        w[h] = mul2(h2R, Tw);
+                        const f2_t x = add2(eu[h], clo);
+                        const f2_t tt = add2(x, mag);
+                        const f2_t fl = add2(tt, nmag);
+                        const f2_t d = sub2(x, fl);
+                        ulo[h] = sub2(eu[h], add2(fl, one));
+                        float d0, d1, t0, t1;
+                        upk2(d, d0, d1);
+                        upk2(tt, t0, t1);
+                        o[2 * h] = __float_as_int(t0) + nrel;
+                        o[2 * h + 1] = __float_as_int(t1) + nrel;
+                        rare = rare || fabsf(d0) > 0.5f - GAMMA || (unsigned)(o[2 * h] + lo_j) > span ||
+                               fabsf(d1) > 0.5f - GAMMA || (unsigned)(o[2 * h + 1] + lo_j) > span;
+                    }
+                }
+                if (!rare && lo_j >= 0) {
+                    // one MUFU.EX2 per sample: g = w sum_m u_m 2^{K u_m^2} delta[o + m], u_m = u_lo - m
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const float* rp0 = col + o[2 * h] * 32;
+                        const float* rp1 = col + o[2 * h + 1] * 32;
+                        f2_t u2 = ulo[h];
+                        f2_t acc2 = pk2(0.f, 0.f);
+#pragma unroll
+                        for (int m = 0; m < W; ++m) {
+                            float a0, a1;
+                            upk2(mul2(mul2(u2, K2), u2), a0, a1);
+                            acc2 = fma2(mul2(u2, pk2(ex2f(a0), ex2f(a1))), pk2(rp0[m * 32], rp1[m * 32]), acc2);
+                            u2 = add2(u2, pk2(-1.f, -1.f));
+                        }
+                        float v0, v1, w0, w1;
+                        upk2(acc2, v0, v1);
+                        upk2(w[h], w0, w1);
+                        gv[t + 2 * h] = w0 * v0;
+                        gv[t + 2 * h + 1] = w1 * v1;
+                    }
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {  // exact window edges / record clipping / exact-ToF groups
+                        float g = 0.f;
+                        if (lo_j >= 0) {
+                            const int64_t gi = (int64_t)cb * CELL + li + h;
+                            const int pb = ((li + h) >> 1) * 4 + ((li + h) & 1);
+                            const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
+                            const PairWin pw = pair_setup<SDEG>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+                            float part = 0.f;
+                            const int oo = pw.n_lo - lo_j;
+                            for (int m = 0; m < pw.cnt; ++m) {
+                                const float um = pw.u_lo - (float)m;
+                                part = fmaf(um * ex2f((um * k.K1u) * um), col[(oo + m) * 32], part);
+                            }
+                            g = pw.w * part;
+                        }
+                        gv[t + h] = g;
+                    }
+                }
+            }
+            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
+            {
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                float h4[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                }
+                float h2[2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                }
+                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+            float sum = 0.f;
+            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+        }
+    }
+}
+
 // sum of the sensor-group partial gradients (fixed order) + epilogue
 template <int MODE>
 __global__ void k_adj_gather(const float* __restrict__ gpart, int32_t ngroups, const int32_t* __restrict__ perm,
@@ -1138,6 +1317,45 @@ cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
     return cudaGetLastError();
 }
 
+size_t adj_sl_smem(const gpair_ctx* c) {
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+           (size_t)ADJT_WARPS * c->La * 32 * 4;
+}
+
+template <int W, int MODE, int SDEG>
+cudaError_t adj_sl_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    const int nw = ADJT_WARPS;
+    const size_t smem = adj_sl_smem(c);
+    cudaError_t e = cudaFuncSetAttribute(k_adjoint_sl<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
+    dim3 grid(c->a_regions, ngroups);
+    ++c->n_launch;
+    k_adjoint_sl<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid,
+                                                       c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, c->k,
+                                                       c->k.K1u);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    ++c->n_launch;
+    k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    return cudaGetLastError();
+}
+
+template <int MODE, int SDEG>
+cudaError_t adj_sl_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
+    switch (c->k.cnt_int) {
+        case 5: return adj_sl_launch<5, MODE, SDEG>(c, resid, ep, st);
+        case 8: return adj_sl_launch<8, MODE, SDEG>(c, resid, ep, st);
+        case 12: return adj_sl_launch<12, MODE, SDEG>(c, resid, ep, st);
+        case 16: return adj_sl_launch<16, MODE, SDEG>(c, resid, ep, st);
+        case 20: return adj_sl_launch<20, MODE, SDEG>(c, resid, ep, st);
+        case 24: return adj_sl_launch<24, MODE, SDEG>(c, resid, ep, st);
+        case 32: return adj_sl_launch<32, MODE, SDEG>(c, resid, ep, st);
+        case 48: return adj_sl_launch<48, MODE, SDEG>(c, resid, ep, st);
+        default: return adj_sl_launch<64, MODE, SDEG>(c, resid, ep, st);
+    }
+}
+
 template <int SER, int MODE>
 cudaError_t adj_dispatch2(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
     switch (pick_wmax(c->k.wmax)) {
@@ -1171,10 +1389,13 @@ cudaError_t adj_dispatch_gen(gpair_ctx* c, const float* resid, const EpiParams& 
 // Which adjoint kernel a context uses (gpair_info.adj_kernel).
 int adjoint_kernel(const gpair_ctx* c) {
     if (c->ser == SER_GEN) return ADJ_LANE_KERNEL;
-    if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on && c->d_gpart) {
+    const bool fast = c->ser == 0 || c->ser == SER_FAST5;
+    if (fast && c->tab.on && c->d_gpart) {
         if (c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_LCF)) return ADJ_LCF;
         if (adj_t_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_T)) return ADJ_TAB_T;
     }
+    if (fast && c->d_gpart && c->k.cnt_int <= 64 && adj_sl_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_T))
+        return ADJ_SL;
     return ADJ_LANE_KERNEL;
 }
 
@@ -1195,6 +1416,8 @@ cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
                 default: break;
             }
         }
+        if (adjoint_kernel(c) == ADJ_SL)
+            return deg5 ? adj_sl_dispatch<MODE, 5>(c, resid, ep, st) : adj_sl_dispatch<MODE, 2>(c, resid, ep, st);
         if (adjoint_kernel(c) == ADJ_TAB_T) {
             switch (c->k.cnt_int) {
                 case 12: return deg5 ? adj_t_launch<12, MODE, 5>(c, resid, ep, st) : adj_t_launch<12, MODE, 2>(c, resid, ep, st);

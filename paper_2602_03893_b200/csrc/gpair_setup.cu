@@ -505,8 +505,10 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     }
 
     // ---- workspaces
-    if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on) {  // sensor-lane TAB adjoint (gpair_kernels.cu k_adjoint_t / k_adjoint_lcf)
+    if (c->ser == 0 || c->ser == SER_FAST5) {  // sensor-lane adjoints (k_adjoint_lcf / _t / _sl) group partials
         SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 255) / 256) * c->Mpad));
+    }
+    if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on) {
         // lane-centred factorisation table G(tau) = 2^{K tau^2}, tau = t - La/2, in fp64
         const double Kd = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
         const int La = c->La, T = La / 2;

@@ -254,7 +254,7 @@ def test_iterate_trajectory_cfg1_reports_loss_decrease():
 
 
 # ----------------------------------------------------------------- full size, sampled
-@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg5"])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4", "cfg4p", "cfg5"])
 def test_full_size_sampled_rows(name):
     """At the bench's size and launch configuration: exact oracle rows for a
     sensor subset (forward) and exact columns for a kernel subset (adjoint)."""

@@ -3,9 +3,10 @@
 The bench configuration (degree-2 series, full windows of W = 16 samples)
 runs the factorised-Gaussian forward (TAB) and the lane-centred adjoint
 (k_adjoint_lcf).  The other kernels of the same configuration -- the TAB
-sensor-lane adjoint (k_adjoint_t), the lane-per-kernel adjoint (k_adjoint)
-and the per-sample-exponential forward -- are the fallbacks for contexts the
-fast kernels do not cover; the library selects them at create time, and the
+sensor-lane adjoint (k_adjoint_t), the per-sample sensor-lane adjoint
+(k_adjoint_sl), the lane-per-kernel adjoint (k_adjoint) and the
+per-sample-exponential forward -- are the fallbacks for contexts the fast
+kernels do not cover; the library selects them at create time, and the
 environment switches GPAIR_NO_TAB / GPAIR_ADJ_NO_LCF / GPAIR_ADJ_NO_T force
 them here so each is held to the same oracle gate (DESIGN.md sections 5, 6).
 """
@@ -28,7 +29,8 @@ PATHS = {
     "tab+lcf": ({}, (1, 2)),
     "tab+lane_t": ({"GPAIR_ADJ_NO_LCF": "1"}, (1, 1)),
     "tab+lane_kernel": ({"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, (1, 0)),
-    "per_sample_exp": ({"GPAIR_NO_TAB": "1"}, (0, 0)),
+    "per_sample_exp+lane_sl": ({"GPAIR_NO_TAB": "1"}, (0, 3)),
+    "per_sample_exp+lane_kernel": ({"GPAIR_NO_TAB": "1", "GPAIR_ADJ_NO_T": "1"}, (0, 0)),
 }
 ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T")
 
@@ -170,4 +172,25 @@ def test_fast_paths_random_geometry(seed, monkeypatch):
     check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
           elementwise=False)
     assert info["tab"] == 1, info  # every case is on the fast (TAB) path
+    ctx.close()
+
+
+# window lengths outside the TAB range (W = 5 of cfg4', W = 8, W = 48 / 64 of desk-like sigma):
+# the per-sample sensor-lane adjoint (k_adjoint_sl) and the per-sample forward
+@pytest.mark.parametrize("W", [5, 8, 48, 64])
+def test_per_sample_sensor_lane_adjoint(W, monkeypatch):
+    fs, v = 40e6, 1500.0
+    sigma = W * (v / fs) / 6.0
+    c = inputs.grid_centers(10, 9, 8, sigma)
+    s = inputs.hemisphere(48, 60e-3)
+    op = dict(sigma=sigma, v=v, fs=fs, n_samples=1900 + 2 * W, t0=2e-6, k=3.0)
+    ctx = make_ctx(c, s, op, monkeypatch, {})
+    info = ctx.info()
+    assert info["adj_kernel"] == 3 and info["tab"] == 0, info
+    rng = np.random.default_rng(W)
+    x = rng.random(c.shape[1]).astype(np.float32)
+    check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"W {W} forward")
+    d = rng.standard_normal((s.shape[1], op["n_samples"])).astype(np.float32)
+    akw = {k: v for k, v in op.items() if k != "n_samples"}
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"W {W} adjoint", elementwise=False)
     ctx.close()
