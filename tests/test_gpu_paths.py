@@ -194,3 +194,28 @@ def test_per_sample_sensor_lane_adjoint(W, monkeypatch):
     akw = {k: v for k, v in op.items() if k != "n_samples"}
     check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"W {W} adjoint", elementwise=False)
     ctx.close()
+
+
+# any window length (fast packed paths where W is a template size, generic paths otherwise),
+# degree-2 or degree-5 series (array radius), jitter, t0 > 0, clipped records
+@pytest.mark.parametrize("seed", range(8))
+def test_random_geometry_any_window(seed, monkeypatch):
+    rng = np.random.default_rng(2000 + seed)
+    W = int([5, 6, 7, 8, 9, 10, 13, 40][seed])
+    fs, v = float(rng.choice([20e6, 40e6])), 1500.0
+    sigma = W * (v / fs) / 6.0
+    n = rng.integers(4, 10, size=3)
+    c = inputs.grid_centers(int(n[0]), int(n[1]), int(n[2]), sigma, jitter=0.3 if seed % 2 else 0.0, seed=seed)
+    s = inputs.hemisphere(int(rng.integers(16, 48)), float(rng.uniform(15e-3, 70e-3)))
+    t0 = float(rng.uniform(0.0, 5e-6))
+    rmax = float(np.max(np.linalg.norm(s[:, :, None] - c[:, None, :].mean(axis=2, keepdims=True), axis=0)))
+    n_samples = int((rmax / v - t0) * fs) + int(rng.integers(-4, 16))
+    op = dict(sigma=sigma, v=v, fs=fs, n_samples=n_samples, t0=t0, k=3.0)
+    ctx = make_ctx(c, s, op, monkeypatch, {})
+    x = rng.random(c.shape[1]).astype(np.float32)
+    check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"seed {seed} W {W} forward")
+    d = rng.standard_normal((s.shape[1], n_samples)).astype(np.float32)
+    akw = {k: v for k, v in op.items() if k != "n_samples"}
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
+          elementwise=False)
+    ctx.close()
