@@ -14,7 +14,10 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "lts__t_bytes.sum", "smsp__sass_inst_executed_op_global_red.sum", "smsp__sass_inst_executed_op_global_atom.sum",
-        "smsp__sass_inst_executed_op_shared_atom.sum", "sm__cycles_elapsed.avg.per_second"]
+        "smsp__sass_inst_executed_op_shared_atom.sum", "sm__cycles_elapsed.avg.per_second",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+        "smsp__inst_executed_op_global_red.sum"]
 
 
 def main(rep):
