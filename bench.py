@@ -276,10 +276,12 @@ def main():
         e2e_s = max_over_ranks(dist, e2e_s, dev)
 
     # ---- roofline of the dominant kernel (forward or adjoint) on this rank
+    # per-step totals: with the sensor-group pipeline the forward is 4 equal launches per step
     fwd_ms, fwd_n = prof["forward"]
     adj_ms, adj_n = prof["adjoint"]
     dom = "forward" if fwd_ms >= adj_ms else "adjoint"
-    dom_ms = (fwd_ms / max(fwd_n, 1)) if dom == "forward" else (adj_ms / max(adj_n, 1))
+    dom_ms = (fwd_ms if dom == "forward" else adj_ms) / args.steps
+    dom_launches = (fwd_n if dom == "forward" else adj_n) / args.steps
     achieved = pair_samples_local / (dom_ms * 1e-3)
     clocks = clk.summary()
     f_max = (clocks["sm_max_mhz"] or 1965) * 1e6
@@ -301,8 +303,8 @@ def main():
                         "exp per pair-sample (SURVEY 8d) = the shared-memory accumulator rate of one 4-B load + 4-B "
                         "store per pair-sample at 128 B/clk/SM (the forward's binding unit on the TAB path); "
                         "DESIGN.md section 6",
-            "pair_samples_per_launch": pair_samples_local,
-            "kernel_ms": {k: (v[0] / max(v[1], 1)) for k, v in prof.items() if v[1]},
+            "pair_samples_per_step": pair_samples_local, "dominant_launches_per_step": dom_launches,
+            "kernel_ms": {k: (v[0] / args.steps) for k, v in prof.items() if v[1]},
             "share_of_step": {k: (v[0] / args.steps) / ms for k, v in prof.items() if v[1]}}
 
     line = {

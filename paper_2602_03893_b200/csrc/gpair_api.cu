@@ -192,8 +192,50 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_vcr_g);
     prof_drain(c);
     for (auto e : c->prof_free) cudaEventDestroy(e);
+    for (auto e : c->ev_f)
+        if (e) cudaEventDestroy(e);
+    for (auto e : c->ev_r)
+        if (e) cudaEventDestroy(e);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->st2) cudaStreamDestroy(c->st2);
     delete c;
 }
+
+// The sensor-group pipeline of gpair_iterate (opt-in): the forward and the
+// sensor-lane adjoint run group by group (256 sensors) on the caller's stream while the
+// reducer (and, at world > 1, the all-reduce of that group's y rows and its residual) of
+// group g runs on an internal high-priority stream as soon as forward group g is done; the
+// adjoint of group g waits only for its own residual rows.  Memory-bound reduction and the
+// collective overlap the shared-memory / FMA-bound kernels.
+gpair_status pipeline_init(gpair_ctx* c) {
+    if (c->st2) return GPAIR_OK;
+    int lo = 0, hi = 0;
+    cudaError_t e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->st2, cudaStreamNonBlocking, hi);
+    for (int g = 0; g < 64 && e == cudaSuccess; ++g) {
+        e = cudaEventCreateWithFlags(&c->ev_f[g], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_r[g], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    return e == cudaSuccess ? GPAIR_OK : cuda_fail(c, e, "pipeline streams/events");
+}
+
+bool pipeline_eligible(const gpair_ctx* c) {
+    const int ak = gpair::adjoint_kernel(c);
+    return c->pipeline && !c->assa && !c->n_near && c->f_warps == 8 &&
+           (ak == gpair::ADJ_LCF || ak == gpair::ADJ_TAB_T || ak == gpair::ADJ_SL) && gpair::adjoint_groups(c) <= 64 &&
+           (c->Nd + 255) / 256 == c->f_sgroups;
+}
+
+struct WindowReset {
+    gpair_ctx* c;
+    ~WindowReset() {
+        c->lg0 = c->lng = c->lj0 = c->lnj = 0;
+        c->lskip_gather = false;
+    }
+};
 
 gpair_status sticky_check(gpair_ctx* c) {
     cudaError_t e = cudaGetLastError();
@@ -394,6 +436,17 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
         free_ctx(c);
         return fail(nullptr, (gpair_status)geom_err, why);
     }
+    {
+        // opt-in (GPAIR_PIPELINE=1): measured 74.6 vs 74.1 ms at cfg4 on one GPU -- the forward fills
+        // every SM, so the reducer finds no room to overlap and four group launches add tails
+        const char* pp = std::getenv("GPAIR_PIPELINE");
+        c->pipeline = (pp && pp[0] == '1') ? 1 : 0;
+        if (c->pipeline && pipeline_eligible(c) && pipeline_init(c) != GPAIR_OK) {
+            std::string m = c->err;
+            free_ctx(c);
+            return fail(nullptr, GPAIR_ERR_CUDA, m);
+        }
+    }
     if (assa) {
         e = cudaMalloc(&c->d_taps, sizeof(float) * taps.size());
         if (e == cudaSuccess)
@@ -558,22 +611,6 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
         API_CUDA(c, gpair::launch_vcr(c, s->grid, z, npc, s->eps_npc, s->beta, s->eps_reg, c->d_vcr_g, nullptr, st),
                  "vcr");
     }
-    gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (c->world == 1 && !signals_out) ? nullptr : y, b, st);
-    if (r) return r;
-    if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
-        ProfScope ps(c, GPAIR_PROF_LOSS, st);
-        float* lo = loss_out ? loss_out : (float*)(c->d_count);  // scratch word when only checking
-        API_CUDA(c,
-                 reg ? gpair::launch_loss(c, lo, st, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
-                     : gpair::launch_loss(c, lo, st),
-                 "loss");
-        if (c->flags & GPAIR_CHECK_FINITE) {
-            float h = 0.f;
-            API_CUDA(c, cudaMemcpyAsync(&h, lo, sizeof(float), cudaMemcpyDeviceToHost, st), "loss readback");
-            API_CUDA(c, cudaStreamSynchronize(st), "loss sync");
-            if (!std::isfinite(h)) return fail(c, GPAIR_ERR_NUMERICAL, "loss is not finite");
-        }
-    }
     EpiParams ep{};
     const double N = (double)c->Nd * (double)c->Nt;
     ep.scale = s->grad_scale > 0.f ? s->grad_scale : (float)(2.0 / N);
@@ -592,12 +629,102 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     ep.x_out = x_out;
     ep.g_reg = reg ? c->d_vcr_g : nullptr;
     ep.lam = s->lam;
+    const int emode = npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP;
+    if (c->st2 && pipeline_eligible(c)) {
+        WindowReset wr{c};
+        cudaStream_t s2 = c->st2;
+        float* yy = (c->world == 1 && !signals_out) ? nullptr : y;
+        {
+            ProfScope ps(c, GPAIR_PROF_GATHER, st);
+            API_CUDA(c, gpair::launch_gather(c, z, npc, s->eps_npc, st), "gather");
+        }
+        const int G = c->f_sgroups;
+        for (int g = 0; g < G; ++g) {
+            {
+                ProfScope ps(c, GPAIR_PROF_FORWARD, st);
+                c->lg0 = g;
+                c->lng = 1;
+                API_CUDA(c, gpair::launch_forward(c, st), "forward (group)");
+            }
+            API_CUDA(c, cudaEventRecord(c->ev_f[g], st), "event");
+            API_CUDA(c, cudaStreamWaitEvent(s2, c->ev_f[g], 0), "event wait");
+            c->lj0 = g * 256;
+            c->lnj = std::min(256, c->Nd - g * 256);
+            if (c->world == 1) {
+                ProfScope ps(c, GPAIR_PROF_REDUCE, s2);
+                API_CUDA(c, gpair::launch_reduce(c, yy, b, c->d_delta, s2), "reduce (group)");
+            } else {
+                {
+                    ProfScope ps(c, GPAIR_PROF_REDUCE, s2);
+                    API_CUDA(c, gpair::launch_reduce(c, y, nullptr, nullptr, s2), "reduce (group)");
+                }
+                {
+                    ProfScope ps(c, GPAIR_PROF_ALLREDUCE, s2);
+                    nccl_res_t rr = g_nccl.AllReduce(y + (size_t)c->lj0 * c->Nt, y + (size_t)c->lj0 * c->Nt,
+                                                     (size_t)c->lnj * c->Nt, NCCL_FLOAT32, NCCL_SUM, c->nccl, s2);
+                    if (rr != 0)
+                        return fail(c, GPAIR_ERR_NCCL, std::string("ncclAllReduce failed: ") +
+                                                           (g_nccl.GetErrorString ? g_nccl.GetErrorString(rr) : "?"));
+                }
+                ProfScope ps(c, GPAIR_PROF_RESIDUAL, s2);
+                API_CUDA(c, gpair::launch_residual(c, y, b, c->d_delta, s2), "residual (group)");
+            }
+            API_CUDA(c, cudaEventRecord(c->ev_r[g], s2), "event");
+        }
+        c->n_loss_part = c->Nd;  // per-sensor loss partials, all groups written on s2
+        c->lj0 = c->lnj = 0;
+        if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
+            ProfScope ps(c, GPAIR_PROF_LOSS, s2);
+            float* lo = loss_out ? loss_out : (float*)(c->d_count);
+            API_CUDA(c,
+                     reg ? gpair::launch_loss(c, lo, s2, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
+                         : gpair::launch_loss(c, lo, s2),
+                     "loss");
+        }
+        API_CUDA(c, cudaEventRecord(c->ev_join, s2), "event");
+        c->lskip_gather = true;
+        for (int g = 0; g < G; ++g) {
+            API_CUDA(c, cudaStreamWaitEvent(st, c->ev_r[g], 0), "event wait");
+            ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+            c->lg0 = g;
+            c->lng = 1;
+            API_CUDA(c, gpair::launch_adjoint(c, c->d_delta, emode, ep, st), "adjoint (group)");
+        }
+        API_CUDA(c, cudaStreamWaitEvent(st, c->ev_join, 0), "event wait");
+        {
+            ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
+            API_CUDA(c, gpair::launch_adjoint_gather(c, emode, ep, st), "adjoint gather + update");
+        }
+        if (c->flags & GPAIR_CHECK_FINITE) {
+            float h = 0.f;
+            float* lo = loss_out ? loss_out : (float*)(c->d_count);
+            API_CUDA(c, cudaMemcpyAsync(&h, lo, sizeof(float), cudaMemcpyDeviceToHost, st), "loss readback");
+            API_CUDA(c, cudaStreamSynchronize(st), "loss sync");
+            if (!std::isfinite(h)) return fail(c, GPAIR_ERR_NUMERICAL, "loss is not finite");
+        }
+        return GPAIR_OK;
+    }
+    gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (c->world == 1 && !signals_out) ? nullptr : y, b, st);
+    if (r) return r;
+    if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
+        ProfScope ps(c, GPAIR_PROF_LOSS, st);
+        float* lo = loss_out ? loss_out : (float*)(c->d_count);  // scratch word when only checking
+        API_CUDA(c,
+                 reg ? gpair::launch_loss(c, lo, st, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
+                     : gpair::launch_loss(c, lo, st),
+                 "loss");
+        if (c->flags & GPAIR_CHECK_FINITE) {
+            float h = 0.f;
+            API_CUDA(c, cudaMemcpyAsync(&h, lo, sizeof(float), cudaMemcpyDeviceToHost, st), "loss readback");
+            API_CUDA(c, cudaStreamSynchronize(st), "loss sync");
+            if (!std::isfinite(h)) return fail(c, GPAIR_ERR_NUMERICAL, "loss is not finite");
+        }
+    }
     ProfScope ps(c, GPAIR_PROF_ADJOINT, st);
     if (c->n_near) {
         API_CUDA(c, gpair::launch_near_adjoint(c, c->d_delta, st), "near-field adjoint");
         ep.g_add = c->d_gnear;
     }
-    const int emode = npc ? gpair::EPI_NPC_ADAM : gpair::EPI_CLAMP;
     API_CUDA(c,
              c->assa ? gpair::launch_assa_adjoint(c, c->d_delta, emode, ep, st)
                      : gpair::launch_adjoint(c, c->d_delta, emode, ep, st),

@@ -87,6 +87,13 @@ struct gpair_ctx_s {
     // profiling
     bool prof_on = false;
     int64_t n_launch = 0;  // library kernels launched by per-call entry points (gpair_profile.kernels)
+    // sensor-group pipeline of gpair_iterate (gpair_api.cu): launch windows read by the launchers
+    int32_t lg0 = 0, lng = 0;   // forward / sensor-lane adjoint: sensor groups [lg0, lg0 + lng) (lng = 0: all)
+    int32_t lj0 = 0, lnj = 0;   // reducer / residual: sensors [lj0, lj0 + lnj) (lnj = 0: all)
+    bool lskip_gather = false;  // sensor-lane adjoint: leave k_adj_gather to the caller
+    cudaStream_t st2 = nullptr; // internal high-priority stream (reducer / collective side of the pipeline)
+    cudaEvent_t ev_f[64] = {}, ev_r[64] = {}, ev_fork = nullptr, ev_join = nullptr;
+    int pipeline = 0;           // 1: GPAIR_PIPELINE=1 (sensor-group pipeline of gpair_iterate, opt-in)
     std::vector<GpairEventPair> prof_pending;
     std::vector<cudaEvent_t> prof_free;
     double prof_ms[GPAIR_PROF_N] = {0};
@@ -150,6 +157,8 @@ __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const Ep
 
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
+cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st);
+int adjoint_groups(const gpair_ctx* c);
 int pick_wmax(int w);
 // adjoint kernel of a context: 0 = k_adjoint (lane = kernel), 1 = k_adjoint_t (TAB, sensor lanes),
 // 2 = k_adjoint_lcf (lane-centred factorisation), 3 = k_adjoint_sl (sensor lanes, per-sample exponential)

@@ -65,6 +65,10 @@ struct OpConst {
     double nf_thr_max;     // bound of every pair's near threshold; -1 when nf = 0
     int32_t per_sigma;     // 1: sigma_i from the table (desc.sigmas); 0: the scalar sigma
     double sigma;          // scalar sigma (fp64, as given)
+    // launch-local offsets of the sensor-group pipeline (gpair_api.cu iterate_pipelined):
+    // forward / sensor-lane adjoint CTAs use sensor group blockIdx.y + grp0, reducer CTAs sensor blockIdx.x + j0
+    int32_t grp0;
+    int32_t j0;
 };
 
 constexpr int SER_GEN = 7;    // kernel path of the general operator (pair_gen)

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     float* s_acc_lane = s_acc + lane;
 
     const int region = blockIdx.x;
-    const int jbase = (blockIdx.y * nw + warp) * 32;
+    const int jbase = ((blockIdx.y + k.grp0) * nw + warp) * 32;
     const int j = jbase + lane;
     const bool jok = j < k.Nd;
     for (int t = lane; t < Lf * 32; t += 32) s_acc[t] = 0.f;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(32 * RED_WARPS, 2) k_reduce(const float* __res
     __shared__ int s_k0;
     __shared__ int s_base[RED_WARPS], s_len[RED_WARPS], s_off[RED_WARPS];
     __shared__ double s_red[RED_WARPS];
-    const int j = blockIdx.x;
+    const int j = blockIdx.x + k.j0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int2* e = ent + (int64_t)j * nregions;
     if (threadIdx.x == 0) s_k0 = red_lower_bound(e, nregions, 0);  // first non-empty window
@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(32 * RED_WARPS, 2) k_reduce(const float* __res
 
 // residual + loss partials for world > 1 (y already all-reduced)
 __global__ void k_residual(const float* __restrict__ y, const float* __restrict__ b, int32_t Nt,
-                           float* __restrict__ delta, double* __restrict__ loss_part) {
-    const int j = blockIdx.x;
+                           float* __restrict__ delta, double* __restrict__ loss_part, int32_t j0) {
+    const int j = blockIdx.x + j0;
     const int64_t row = (int64_t)j * Nt;
     double lsum = 0.0;
     for (int n = threadIdx.x; n < Nt; n += blockDim.x) {
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     f2_t* col2 = (f2_t*)s_col + lane;
 
     const int region = blockIdx.x;
-    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
     const bool jok = j < k.Nd;
     const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
     float sx = 0.f, sy = 0.f, sz = 0.f;
@@ -782,7 +782,7 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             float sum = 0.f;
             for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
         }
     }
 }
@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
     const float* s_ginv = s_gt + La;
 
     const int region = blockIdx.x;
-    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
     const bool jok = j < k.Nd;
     const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
     float sx = 0.f, sy = 0.f, sz = 0.f;
@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             float sum = 0.f;
             for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
         }
     }
 }
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
     float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
     float* col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 + lane;  // this lane's column delta_t
     const int region = blockIdx.x;
-    const int j = (blockIdx.y * nw + warp) * 32 + lane;
+    const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
     const bool jok = j < k.Nd;
     const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
     float sx = 0.f, sy = 0.f, sz = 0.f;
@@ -1213,7 +1213,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
             float sum = 0.f;
             for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)blockIdx.y * Mpad + (int64_t)cb * CELL + t] = sum;
+            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
         }
     }
 }
@@ -1246,11 +1246,13 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
                   (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0);
     cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid(c->f_regions, c->f_sgroups);
+    dim3 grid(c->f_regions, c->lng > 0 ? c->lng : c->f_sgroups);  // lng / lg0: sensor-group window (pipeline)
+    OpConst kk = c->k;
+    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
     ++c->n_launch;
     k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
-                                                      c->Mpad, c->k, c->d_ksig, c->tab);
+                                                      c->Mpad, kk, c->d_ksig, c->tab);
     return cudaGetLastError();
 }
 
@@ -1282,12 +1284,15 @@ cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_t<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
-    dim3 grid(c->a_regions, ngroups);
+    dim3 grid(c->a_regions, c->lng > 0 ? c->lng : ngroups);
+    OpConst kk = c->k;
+    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
     ++c->n_launch;
     k_adjoint_t<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gpart,
-                                                c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab);
+                                                c->a_cpr, c->ncells, c->La, c->Mpad, kk, c->tab);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (c->lskip_gather) return cudaSuccess;  // pipelined iterate: launched once after all groups
     ++c->n_launch;
     k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
     return cudaGetLastError();
@@ -1305,13 +1310,16 @@ cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_lcf<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
-    dim3 grid(c->a_regions, ngroups);
+    dim3 grid(c->a_regions, c->lng > 0 ? c->lng : ngroups);
+    OpConst kk = c->k;
+    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
     ++c->n_launch;
     k_adjoint_lcf<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gtab,
-                                                  c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, c->k, c->tab.K,
+                                                  c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, kk, c->tab.K,
                                                   c->tab.m2K);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (c->lskip_gather) return cudaSuccess;  // pipelined iterate: launched once after all groups
     ++c->n_launch;
     k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
     return cudaGetLastError();
@@ -1329,13 +1337,16 @@ cudaError_t adj_sl_launch(gpair_ctx* c, const float* resid, const EpiParams& ep,
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_sl<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
-    dim3 grid(c->a_regions, ngroups);
+    dim3 grid(c->a_regions, c->lng > 0 ? c->lng : ngroups);
+    OpConst kk = c->k;
+    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
     ++c->n_launch;
     k_adjoint_sl<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid,
-                                                       c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, c->k,
+                                                       c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, kk,
                                                        c->k.K1u);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (c->lskip_gather) return cudaSuccess;  // pipelined iterate: launched once after all groups
     ++c->n_launch;
     k_adj_gather<MODE><<<(unsigned)((c->Mpad + 255) / 256), 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
     return cudaGetLastError();
@@ -1476,8 +1487,10 @@ cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, 
     const size_t smem = (size_t)(std::max(c->jlen_max, 1) + RED_WARPS * (c->Lf + 1)) * 8;
     cudaError_t e = cudaFuncSetAttribute(k_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    OpConst kk = c->k;
+    kk.j0 = c->lnj > 0 ? c->lj0 : 0;  // lnj / lj0: sensor window (pipeline)
     ++c->n_launch;
-    k_reduce<<<c->Nd, 32 * RED_WARPS, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, c->k, y, b, delta,
+    k_reduce<<<c->lnj > 0 ? c->lnj : c->Nd, 32 * RED_WARPS, smem, st>>>(c->d_partial, c->d_rent, c->f_regions, c->Lf, kk, y, b, delta,
                                                   c->d_loss_part, c->n_near ? c->d_near_row : nullptr, c->d_ynear);
     if (b) c->n_loss_part = c->Nd;
     return cudaGetLastError();
@@ -1485,7 +1498,8 @@ cudaError_t launch_reduce(gpair_ctx* c, float* y, const float* b, float* delta, 
 
 cudaError_t launch_residual(gpair_ctx* c, const float* y, const float* b, float* delta, cudaStream_t st) {
     ++c->n_launch;
-    k_residual<<<c->Nd, 256, 0, st>>>(y, b, c->Nt, delta, c->d_loss_part);
+    k_residual<<<c->lnj > 0 ? c->lnj : c->Nd, 256, 0, st>>>(y, b, c->Nt, delta, c->d_loss_part,
+                                                            c->lnj > 0 ? c->lj0 : 0);
     c->n_loss_part = c->Nd;
     return cudaGetLastError();
 }
@@ -1503,6 +1517,21 @@ cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const Epi
     if (mode == EPI_NPC_ADAM) return adj_dispatch<EPI_NPC_ADAM>(c, resid, ep, st);
     return adj_dispatch<EPI_CLAMP>(c, resid, ep, st);
 }
+
+cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st) {
+    const int ngroups = (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS);
+    const unsigned nb = (unsigned)((c->Mpad + 255) / 256);
+    ++c->n_launch;
+    if (mode == EPI_GRAD)
+        k_adj_gather<EPI_GRAD><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    else if (mode == EPI_NPC_ADAM)
+        k_adj_gather<EPI_NPC_ADAM><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    else
+        k_adj_gather<EPI_CLAMP><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+    return cudaGetLastError();
+}
+
+int adjoint_groups(const gpair_ctx* c) { return (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS); }
 
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), st);

@@ -31,8 +31,11 @@ PATHS = {
     "tab+lane_kernel": ({"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, (1, 0)),
     "per_sample_exp+lane_sl": ({"GPAIR_NO_TAB": "1"}, (0, 3)),
     "per_sample_exp+lane_kernel": ({"GPAIR_NO_TAB": "1", "GPAIR_ADJ_NO_T": "1"}, (0, 0)),
+    # sensor-group pipeline of gpair_iterate (opt-in): forward / reducer / adjoint per 256-sensor group
+    "tab+lcf+pipeline": ({"GPAIR_PIPELINE": "1"}, (1, 2)),
+    "per_sample_exp+lane_sl+pipeline": ({"GPAIR_NO_TAB": "1", "GPAIR_PIPELINE": "1"}, (0, 3)),
 }
-ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T")
+ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE")
 
 
 @pytest.fixture(scope="module", autouse=True)
