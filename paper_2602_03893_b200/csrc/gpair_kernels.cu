@@ -299,7 +299,13 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
 // read once, RED_U rows in flight per warp.  The overlapping copies are summed
 // in warp order (deterministic, no atomics).  Fuses the near-field rows, y,
 // the residual delta = y - b and one fp64 loss partial per sensor.
-constexpr int RED_U = 8;      // rows in flight per warp
+#ifndef GPAIR_RED_U
+#define GPAIR_RED_U 8
+#endif
+#ifndef GPAIR_RED_MINB
+#define GPAIR_RED_MINB 2
+#endif
+constexpr int RED_U = GPAIR_RED_U;  // rows in flight per warp
 constexpr int RED_WARPS = 16; // warps per CTA
 
 __device__ __forceinline__ int red_lower_bound(const int2* e, int n, int v) {
@@ -311,7 +317,7 @@ __device__ __forceinline__ int red_lower_bound(const int2* e, int n, int v) {
     return a;
 }
 
-__global__ void __launch_bounds__(32 * RED_WARPS, 2) k_reduce(const float* __restrict__ partial,
+__global__ void __launch_bounds__(32 * RED_WARPS, GPAIR_RED_MINB) k_reduce(const float* __restrict__ partial,
                                                               const int2* __restrict__ ent, int32_t nregions,
                                                               int32_t Lf, OpConst k, float* __restrict__ y,
                                                               const float* __restrict__ b, float* __restrict__ delta,
