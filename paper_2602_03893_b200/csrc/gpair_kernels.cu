@@ -104,6 +104,21 @@ __device__ __forceinline__ void acc_pair(float* s_acc_lane, int lo_j, const Pair
         acc_generic<WMAX>(ap, p.u_lo, p.w, K1, p.cnt);
 }
 
+// cp.async helpers (L1-allocating 4-B and 16-B copies into shared memory)
+__device__ __forceinline__ void cp_async_f32(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_16(float* dst, const float4* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_group() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+constexpr int FWD_STAGE = 6;                                        // cells per double-buffered tile (FAST)
+constexpr int FWD_BUF = FWD_STAGE * CELL * 5 + FWD_STAGE * GPC * 4;  // floats per tile buffer
+
 template <int WMAX, int SER>
 __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
@@ -118,15 +133,20 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     // factorised Gaussian (TabConst): 3 MUFU per pair instead of WMAX
     constexpr bool TABW = FAST && (WMAX % 4 == 0) && WMAX >= TAB_MIN && WMAX <= TAB_MAX;
     extern __shared__ float4 smem4[];
-    float4* s_kd = smem4;                                   // [STAGE_CELLS*32] (FAST: SoA x, y, z, |d|^2)
+    // FAST: double-buffered parameter tiles of FWD_STAGE cells, filled by cp.async while the
+    // previous tile is evaluated; kernel pairs interleaved, s_kxy[p] = (x0, x1, y0, y1),
+    // s_kzw[p] = (z0, z1, w0, w1), then amplitudes and the group anchors.
+    // Other paths: one synchronous tile of STAGE_CELLS cells (s_kd AoS).
+    constexpr int STG = FAST ? FWD_STAGE : STAGE_CELLS;
+    float4* s_kd = smem4;                                   // [STAGE_CELLS*32] (non-FAST)
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
     float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
     float4* s_ks = (float4*)(s_amp + STAGE_CELLS * CELL);   // [STAGE_CELLS*32] (GEN only)
-    // FAST: kernel pairs interleaved, s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
     float* s_kxy = (float*)s_kd;
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_acc = (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0)) + (size_t)warp * Lf * 32;
+    float* s_acc = (FAST ? (float*)smem4 + 2 * FWD_BUF : (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0))) +
+                   (size_t)warp * Lf * 32;
     float* s_acc_lane = s_acc + lane;
 
     const int region = blockIdx.x;
@@ -142,24 +162,45 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         sz = sens[2 * k.Nd + j];
     }
     const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
-    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
-        const int nc = min(STAGE_CELLS, c1 - cb);
-        __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            const float4 v = kd[(int64_t)cb * CELL + t];
-            if (FAST) {
-                const int pb = (t >> 1) * 4 + (t & 1);
-                s_kxy[pb] = v.x;
-                s_kxy[pb + 2] = v.y;
-                s_kzw[pb] = v.z;
-                s_kzw[pb + 2] = v.w;
-            } else {
-                s_kd[t] = v;
-            }
-            s_amp[t] = amp[(int64_t)cb * CELL + t];
-            if (GEN) s_ks[t] = ksig[(int64_t)cb * CELL + t];
+    auto issue_tile = [&](int cbs, int buf) {  // FAST: cp.async of one parameter tile into buffer buf
+        const int ncs = min(FWD_STAGE, c1 - cbs);
+        float* bxy = (float*)smem4 + buf * FWD_BUF;
+        float* bzw = bxy + FWD_STAGE * CELL * 2;
+        float* bam = bzw + FWD_STAGE * CELL * 2;
+        float* bgr = bam + FWD_STAGE * CELL;
+        for (int t = threadIdx.x; t < ncs * CELL; t += blockDim.x) {
+            const float* src = (const float*)(kd + (int64_t)cbs * CELL + t);
+            const int pb = (t >> 1) * 4 + (t & 1);
+            cp_async_f32(bxy + pb, src);
+            cp_async_f32(bxy + pb + 2, src + 1);
+            cp_async_f32(bzw + pb, src + 2);
+            cp_async_f32(bzw + pb + 2, src + 3);
+            cp_async_f32(bam + t, amp + (int64_t)cbs * CELL + t);
         }
-        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        if (threadIdx.x < ncs * GPC) cp_async_16(bgr + 4 * threadIdx.x, grp + (int64_t)cbs * GPC + threadIdx.x);
+    };
+    if (FAST && c0 < c1) issue_tile(c0, 0);
+    cp_async_commit_group();
+    int stage = 0;
+    for (int cb = c0; cb < c1; cb += STG, ++stage) {
+        const int nc = min(STG, c1 - cb);
+        __syncthreads();  // every warp is done with the previous tile (FAST: buffer (stage + 1) & 1)
+        if constexpr (FAST) {
+            if (cb + STG < c1) issue_tile(cb + STG, (stage + 1) & 1);
+            cp_async_commit_group();
+            cp_async_wait_1();  // this tile's copies (this thread's) have landed
+            s_kxy = (float*)smem4 + (stage & 1) * FWD_BUF;
+            s_kzw = s_kxy + FWD_STAGE * CELL * 2;
+            s_amp = s_kzw + FWD_STAGE * CELL * 2;
+            s_grp = (float4*)(s_amp + FWD_STAGE * CELL);
+        } else {
+            for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+                s_kd[t] = kd[(int64_t)cb * CELL + t];
+                s_amp[t] = amp[(int64_t)cb * CELL + t];
+                if (GEN) s_ks[t] = ksig[(int64_t)cb * CELL + t];
+            }
+            if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -1248,8 +1289,11 @@ namespace {
 
 template <int W, int SER>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
-    size_t smem = (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 + (size_t)c->f_warps * c->Lf * 32 * 4 +
-                  (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0);
+    constexpr bool FASTL = SER == 0 || SER == SER_FAST5;
+    size_t smem = (FASTL ? (size_t)2 * FWD_BUF * 4
+                         : (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 +
+                               (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0)) +
+                  (size_t)c->f_warps * c->Lf * 32 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(c->f_regions, c->lng > 0 ? c->lng : c->f_sgroups);  // lng / lg0: sensor-group window (pipeline)
