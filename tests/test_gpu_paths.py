@@ -222,3 +222,41 @@ def test_random_geometry_any_window(seed, monkeypatch):
     check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
           elementwise=False)
     ctx.close()
+
+
+@pytest.mark.parametrize("pipeline", ["0", "1"])
+def test_iterate_cuda_graph_capture(pipeline, monkeypatch):
+    """gpair_iterate is asynchronous on the caller's stream and capturable in a CUDA graph
+    (with the opt-in sensor-group pipeline too: fork/join through events); replaying the
+    graph gives bit-identical state to eager calls."""
+    monkeypatch.setenv("GPAIR_PIPELINE", pipeline)
+    c, s, op = small_tab_case()
+    M = c.shape[1]
+    ctx = gpair.Context(T(c), T(s), sigma=op["sigma"], v=op["v"], fs=op["fs"], n_samples=op["n_samples"],
+                        t0=op["t0"], k=op["k"])
+    rng = np.random.default_rng(5)
+    b = T(oracle.forward(c, rng.random(M).astype(np.float32), s, **op).astype(np.float32))
+    z0 = rng.uniform(0.2, 0.9, M).astype(np.float32)
+
+    def run(use_graph):
+        z, m, v = T(z0), torch.zeros(M, device="cuda"), torch.zeros(M, device="cuda")
+        loss = torch.zeros(1, device="cuda")
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            ctx.iterate(z, m, v, b, lr=0.01, step=1, loss_out=loss, stream=st)  # warm-up / first step
+            if use_graph:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    ctx.iterate(z, m, v, b, lr=0.01, step=2, loss_out=loss, stream=st)
+                for _ in range(3):
+                    g.replay()
+            else:
+                for _ in range(3):
+                    ctx.iterate(z, m, v, b, lr=0.01, step=2, loss_out=loss, stream=st)
+        torch.cuda.synchronize()
+        return z.cpu().numpy(), loss.cpu().numpy()
+
+    ze, le = run(False)
+    zg, lg = run(True)
+    assert np.array_equal(ze, zg) and np.array_equal(le, lg)
+    ctx.close()
