@@ -621,6 +621,54 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     adjoint_epilogue<MODE>(acc, ic, ep);
 }
 
+// ------------------------------------------------------------------ sensor-lane adjoint helpers
+// Reduce-scatter of 8 per-lane values (one group of 8 kernels) over the warp's 32
+// sensors: xor 16 / 8 / 4 halve the value set, xor 2 / 1 finish the sums; lane 4k
+// ends with kernel k's sum and writes it to dst[k] (fixed order: deterministic).
+__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, float* dst) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    float h4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+        h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float h2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+        h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+    if ((lane & 3) == 0) dst[lane >> 2] = h1;  // lane bits (4, 3, 2) = kernel index
+}
+
+// Kernel tile of nc cells into shared memory, kernel pairs interleaved:
+// s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1), plus the group anchors.
+__device__ __forceinline__ void stage_kernel_tile(const float4* __restrict__ kd, const float4* __restrict__ grp, int cb,
+                                                  int nc, float* s_kxy, float* s_kzw, float4* s_grp) {
+    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+        const float4 v = kd[(int64_t)cb * CELL + t];
+        const int pb = (t >> 1) * 4 + (t & 1);
+        s_kxy[pb] = v.x;
+        s_kxy[pb + 2] = v.y;
+        s_kzw[pb] = v.z;
+        s_kzw[pb + 2] = v.w;
+    }
+    if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+}
+
+// Sum of the CTA's per-warp kernel sums in warp order -> this sensor group's partial gradient.
+__device__ __forceinline__ void write_group_partials(const float* s_g, int nw, int nc, float* __restrict__ dst) {
+    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+        float sum = 0.f;
+        for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+        dst[t] = sum;
+    }
+}
+
 // ------------------------------------------------------------------ adjoint, TAB path, sensor lanes
 // The adjoint with the forward's decomposition: lane = sensor j, warp = 32
 // sensors, CTA = adjoint region of cells x 256 sensors (blockIdx.y = sensor
@@ -651,11 +699,10 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
                                                      int32_t La, int64_t Mpad, OpConst k, const TabConst tab) {
     constexpr int C = W / 2;
     extern __shared__ float4 smem4[];
-    float* s_kx = (float*)smem4;                        // [STAGE_CELLS*32] SoA kernel offsets
-    float* s_ky = s_kx + STAGE_CELLS * CELL;
-    float* s_kz = s_ky + STAGE_CELLS * CELL;
-    float* s_kw = s_kz + STAGE_CELLS * CELL;
-    float4* s_grp = (float4*)(s_kw + STAGE_CELLS * CELL);  // [STAGE_CELLS*GPC]
+    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
+    float* s_kxy = (float*)smem4;
+    float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
+    float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
     // this warp's residual column [La][32] (ADJT_DBL: [La][32] float2 (delta_t, delta_{t+1}))
@@ -695,14 +742,7 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            const float4 v = kd[(int64_t)cb * CELL + t];
-            s_kx[t] = v.x;
-            s_ky[t] = v.y;
-            s_kz[t] = v.z;
-            s_kw[t] = v.w;
-        }
-        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -718,8 +758,9 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
                 float g0 = 0.f, g1 = 0.f;
                 bool rare = exact_grp;
                 if (!exact_grp) {
-                    const f2_t kx = *(const f2_t*)(s_kx + li), ky = *(const f2_t*)(s_ky + li);
-                    const f2_t kz = *(const f2_t*)(s_kz + li), kw = *(const f2_t*)(s_kw + li);
+                    const float4 pxy = *(const float4*)(s_kxy + 2 * li), pzw = *(const float4*)(s_kzw + 2 * li);
+                    const f2_t kx = pk2(pxy.x, pxy.y), ky = pk2(pxy.z, pxy.w);
+                    const f2_t kz = pk2(pzw.x, pzw.y), kw = pk2(pzw.z, pzw.w);
                     const f2_t q = fma2(Ux, kx, fma2(Uy, ky, fma2(Uz, kz, kw)));
                     const f2_t eps = mul2(q, iR2);
                     f2_t S, Tw;
@@ -789,7 +830,8 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
 #pragma unroll 1
                     for (int h = 0; h < 2; ++h) {
                         const int64_t gi = (int64_t)cb * CELL + li + h;
-                        const float4 kdt = make_float4(s_kx[li + h], s_ky[li + h], s_kz[li + h], s_kw[li + h]);
+                        const int pb = ((li + h) >> 1) * 4 + ((li + h) & 1);
+                        const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
                         const PairWin pw = pair_setup<SDEG>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
                         float part = 0.f;
                         const float* rq = ADJT_DBL ? (const float*)(col2 + (pw.n_lo - lo_j) * 32) : col + (pw.n_lo - lo_j) * 32;
@@ -803,34 +845,10 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
                 gv[t] = g0;
                 gv[t + 1] = g1;
             }
-            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
-            {
-                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-                float h4[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
-                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                float h2[2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
-                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-                // lane bits (4, 3, 2) hold the kernel index (b4 * 4 + b3 * 2 + b2)
-                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
-            }
+            warp_reduce_scatter8(gv, lane, s_g + warp * (STAGE_CELLS * CELL) + gq * GROUP);
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            float sum = 0.f;
-            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
-        }
+        write_group_partials(s_g, nw, nc, gpart + (int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL);
     }
 }
 
@@ -923,15 +941,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            const float4 v = kd[(int64_t)cb * CELL + t];
-            const int pb = (t >> 1) * 4 + (t & 1);
-            s_kxy[pb] = v.x;
-            s_kxy[pb + 2] = v.y;
-            s_kzw[pb] = v.z;
-            s_kzw[pb + 2] = v.w;
-        }
-        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -1060,33 +1070,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
                     }
                 }
             }
-            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
-            {
-                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-                float h4[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
-                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                float h2[2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
-                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
-            }
+            warp_reduce_scatter8(gv, lane, s_g + warp * (STAGE_CELLS * CELL) + gq * GROUP);
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            float sum = 0.f;
-            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
-        }
+        write_group_partials(s_g, nw, nc, gpart + (int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL);
     }
 }
 
@@ -1139,15 +1126,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            const float4 v = kd[(int64_t)cb * CELL + t];
-            const int pb = (t >> 1) * 4 + (t & 1);
-            s_kxy[pb] = v.x;
-            s_kxy[pb + 2] = v.y;
-            s_kzw[pb] = v.z;
-            s_kzw[pb + 2] = v.w;
-        }
-        if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -1235,33 +1214,10 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
                     }
                 }
             }
-            // reduce-scatter of the 8 values over the warp: lane 4k ends with kernel k's sum
-            {
-                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-                float h4[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
-                    h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-                }
-                float h2[2];
-#pragma unroll
-                for (int i = 0; i < 2; ++i) {
-                    const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
-                    h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-                }
-                float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-                h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-                if ((lane & 3) == 0) s_g[warp * (STAGE_CELLS * CELL) + gq * GROUP + (lane >> 2)] = h1;
-            }
+            warp_reduce_scatter8(gv, lane, s_g + warp * (STAGE_CELLS * CELL) + gq * GROUP);
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            float sum = 0.f;
-            for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-            gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL + t] = sum;
-        }
+        write_group_partials(s_g, nw, nc, gpart + (int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL);
     }
 }
 
