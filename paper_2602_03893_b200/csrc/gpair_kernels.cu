@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     // previous tile is evaluated; kernel pairs interleaved, s_kxy[p] = (x0, x1, y0, y1),
     // s_kzw[p] = (z0, z1, w0, w1), then amplitudes and the group anchors.
     // Other paths: one synchronous tile of STAGE_CELLS cells (s_kd AoS).
-    constexpr int STG = FAST ? FWD_STAGE : STAGE_CELLS;
+    // double buffering pays when the per-tile evaluation is long (W >= 12); short windows
+    // (W = 5, 8) keep one synchronous tile of STAGE_CELLS cells (fewer barriers per kernel)
+    constexpr bool DBUF = FAST && WMAX >= 12;
+    constexpr int STG = DBUF ? FWD_STAGE : STAGE_CELLS;
     float4* s_kd = smem4;                                   // [STAGE_CELLS*32] (non-FAST)
     float4* s_grp = s_kd + STAGE_CELLS * CELL;              // [STAGE_CELLS*GPC]
     float* s_amp = (float*)(s_grp + STAGE_CELLS * GPC);     // [STAGE_CELLS*32]
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     float* s_kxy = (float*)s_kd;
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_acc = (FAST ? (float*)smem4 + 2 * FWD_BUF : (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0))) +
+    float* s_acc = (DBUF ? (float*)smem4 + 2 * FWD_BUF : (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0))) +
                    (size_t)warp * Lf * 32;
     float* s_acc_lane = s_acc + lane;
 
@@ -179,13 +182,13 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         }
         if (threadIdx.x < ncs * GPC) cp_async_16(bgr + 4 * threadIdx.x, grp + (int64_t)cbs * GPC + threadIdx.x);
     };
-    if (FAST && c0 < c1) issue_tile(c0, 0);
+    if (DBUF && c0 < c1) issue_tile(c0, 0);
     cp_async_commit_group();
     int stage = 0;
     for (int cb = c0; cb < c1; cb += STG, ++stage) {
         const int nc = min(STG, c1 - cb);
         __syncthreads();  // every warp is done with the previous tile (FAST: buffer (stage + 1) & 1)
-        if constexpr (FAST) {
+        if constexpr (DBUF) {
             if (cb + STG < c1) issue_tile(cb + STG, (stage + 1) & 1);
             cp_async_commit_group();
             cp_async_wait_1();  // this tile's copies (this thread's) have landed
@@ -195,7 +198,16 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
             s_grp = (float4*)(s_amp + FWD_STAGE * CELL);
         } else {
             for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-                s_kd[t] = kd[(int64_t)cb * CELL + t];
+                const float4 v = kd[(int64_t)cb * CELL + t];
+                if (FAST) {  // pair-interleaved, as in the double-buffered tiles
+                    const int pb = (t >> 1) * 4 + (t & 1);
+                    s_kxy[pb] = v.x;
+                    s_kxy[pb + 2] = v.y;
+                    s_kzw[pb] = v.z;
+                    s_kzw[pb + 2] = v.w;
+                } else {
+                    s_kd[t] = v;
+                }
                 s_amp[t] = amp[(int64_t)cb * CELL + t];
                 if (GEN) s_ks[t] = ksig[(int64_t)cb * CELL + t];
             }
@@ -1245,8 +1257,8 @@ namespace {
 
 template <int W, int SER>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
-    constexpr bool FASTL = SER == 0 || SER == SER_FAST5;
-    size_t smem = (FASTL ? (size_t)2 * FWD_BUF * 4
+    constexpr bool DBUFL = (SER == 0 || SER == SER_FAST5) && W >= 12;
+    size_t smem = (DBUFL ? (size_t)2 * FWD_BUF * 4
                          : (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 +
                                (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0)) +
                   (size_t)c->f_warps * c->Lf * 32 * 4;
