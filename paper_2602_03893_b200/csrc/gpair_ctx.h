@@ -158,6 +158,8 @@ __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const Ep
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st);
+cudaError_t launch_group_gather(gpair_ctx* c, const float* gpart, int ngroups, int mode, const EpiParams& ep,
+                                cudaStream_t st);
 int adjoint_groups(const gpair_ctx* c);
 int pick_wmax(int w);
 // adjoint kernel of a context: 0 = k_adjoint (lane = kernel), 1 = k_adjoint_t (TAB, sensor lanes),

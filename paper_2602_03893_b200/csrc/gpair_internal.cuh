@@ -628,4 +628,53 @@ __device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, 
     }
 }
 
+// ---- sensor-lane adjoint helpers (gpair_kernels.cu, gpair_assa.cu)
+constexpr int STAGE_CELLS = 8;  // cells per staged kernel tile
+// Reduce-scatter of 8 per-lane values (one group of 8 kernels) over the warp's 32
+// sensors: xor 16 / 8 / 4 halve the value set, xor 2 / 1 finish the sums; lane 4k
+// ends with kernel k's sum and writes it to dst[k] (fixed order: deterministic).
+__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, float* dst) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+    float h4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+        h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float h2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+        h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
+    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
+    if ((lane & 3) == 0) dst[lane >> 2] = h1;  // lane bits (4, 3, 2) = kernel index
+}
+
+// Kernel tile of nc cells into shared memory, kernel pairs interleaved:
+// s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1), plus the group anchors.
+__device__ __forceinline__ void stage_kernel_tile(const float4* __restrict__ kd, const float4* __restrict__ grp, int cb,
+                                                  int nc, float* s_kxy, float* s_kzw, float4* s_grp) {
+    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+        const float4 v = kd[(int64_t)cb * CELL + t];
+        const int pb = (t >> 1) * 4 + (t & 1);
+        s_kxy[pb] = v.x;
+        s_kxy[pb + 2] = v.y;
+        s_kzw[pb] = v.z;
+        s_kzw[pb + 2] = v.w;
+    }
+    if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
+}
+
+// Sum of the CTA's per-warp kernel sums in warp order -> this sensor group's partial gradient.
+__device__ __forceinline__ void write_group_partials(const float* s_g, int nw, int nc, float* __restrict__ dst) {
+    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
+        float sum = 0.f;
+        for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+        dst[t] = sum;
+    }
+}
+
 }  // namespace gpair

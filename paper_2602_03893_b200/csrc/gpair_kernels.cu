@@ -31,7 +31,6 @@ namespace gpair {
 
 namespace {
 
-constexpr int STAGE_CELLS = 8;  // cells staged per forward pipeline step
 
 __global__ void k_gather(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t Mpad,
                          int npc, float eps, float* __restrict__ amp) {
@@ -631,54 +630,6 @@ __global__ void __launch_bounds__(256) k_adjoint(const float4* __restrict__ kd, 
     const int32_t ic = perm[gi];
     if (ic < 0) return;
     adjoint_epilogue<MODE>(acc, ic, ep);
-}
-
-// ------------------------------------------------------------------ sensor-lane adjoint helpers
-// Reduce-scatter of 8 per-lane values (one group of 8 kernels) over the warp's 32
-// sensors: xor 16 / 8 / 4 halve the value set, xor 2 / 1 finish the sums; lane 4k
-// ends with kernel k's sum and writes it to dst[k] (fixed order: deterministic).
-__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, float* dst) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    float h4[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
-        h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-    float h2[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
-        h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
-    h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
-    h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
-    if ((lane & 3) == 0) dst[lane >> 2] = h1;  // lane bits (4, 3, 2) = kernel index
-}
-
-// Kernel tile of nc cells into shared memory, kernel pairs interleaved:
-// s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1), plus the group anchors.
-__device__ __forceinline__ void stage_kernel_tile(const float4* __restrict__ kd, const float4* __restrict__ grp, int cb,
-                                                  int nc, float* s_kxy, float* s_kzw, float4* s_grp) {
-    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-        const float4 v = kd[(int64_t)cb * CELL + t];
-        const int pb = (t >> 1) * 4 + (t & 1);
-        s_kxy[pb] = v.x;
-        s_kxy[pb + 2] = v.y;
-        s_kzw[pb] = v.z;
-        s_kzw[pb + 2] = v.w;
-    }
-    if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
-}
-
-// Sum of the CTA's per-warp kernel sums in warp order -> this sensor group's partial gradient.
-__device__ __forceinline__ void write_group_partials(const float* s_g, int nw, int nc, float* __restrict__ dst) {
-    for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-        float sum = 0.f;
-        for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
-        dst[t] = sum;
-    }
 }
 
 // ------------------------------------------------------------------ adjoint, TAB path, sensor lanes
@@ -1536,17 +1487,21 @@ cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const Epi
     return adj_dispatch<EPI_CLAMP>(c, resid, ep, st);
 }
 
-cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st) {
-    const int ngroups = (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS);
+cudaError_t launch_group_gather(gpair_ctx* c, const float* gpart, int ngroups, int mode, const EpiParams& ep,
+                                cudaStream_t st) {
     const unsigned nb = (unsigned)((c->Mpad + 255) / 256);
     ++c->n_launch;
     if (mode == EPI_GRAD)
-        k_adj_gather<EPI_GRAD><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+        k_adj_gather<EPI_GRAD><<<nb, 256, 0, st>>>(gpart, ngroups, c->d_perm, c->Mpad, ep);
     else if (mode == EPI_NPC_ADAM)
-        k_adj_gather<EPI_NPC_ADAM><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+        k_adj_gather<EPI_NPC_ADAM><<<nb, 256, 0, st>>>(gpart, ngroups, c->d_perm, c->Mpad, ep);
     else
-        k_adj_gather<EPI_CLAMP><<<nb, 256, 0, st>>>(c->d_gpart, ngroups, c->d_perm, c->Mpad, ep);
+        k_adj_gather<EPI_CLAMP><<<nb, 256, 0, st>>>(gpart, ngroups, c->d_perm, c->Mpad, ep);
     return cudaGetLastError();
+}
+
+cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st) {
+    return launch_group_gather(c, c->d_gpart, (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS), mode, ep, st);
 }
 
 int adjoint_groups(const gpair_ctx* c) { return (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS); }
