@@ -674,6 +674,8 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     f2_t* col2 = (f2_t*)s_col + lane;
 
     const int region = blockIdx.x;
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(STAGE_CELLS, c1 - c0), s_kxy, s_kzw, s_grp);
     const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
     const bool jok = j < k.Nd;
     const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
@@ -701,11 +703,12 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
-        __syncthreads();
-        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        if (cb != c0) {  // the first tile was staged with the residual columns
+            __syncthreads();  // every warp is done with the previous tile and its s_g sums
+            stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -874,8 +877,9 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
     float* s_gt = s_g + nw * STAGE_CELLS * CELL;          // [2][La]: G(t - T), 1 / G(t - T)
     float* col = s_gt + 2 * La + (size_t)warp * La * 32 + lane;  // this lane's column dtil_t at col[t * 32]
     for (int t = threadIdx.x; t < 2 * La; t += blockDim.x) s_gt[t] = gtab[t];
-    __syncthreads();
     const float* s_ginv = s_gt + La;
+    const int c0 = blockIdx.x * cpr, c1 = min(c0 + cpr, ncells);
+    if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(STAGE_CELLS, c1 - c0), s_kxy, s_kzw, s_grp);
 
     const int region = blockIdx.x;
     const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
@@ -891,7 +895,7 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
         const float* src = resid + (int64_t)j * k.Nt;
         for (int t = 0; t < La; ++t) {
             const int n = lo_j + t;
-            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] * s_gt[t] : 0.f;
+            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] * __ldg(gtab + t) : 0.f;
         }
     }
     const int Tc = La >> 1;
@@ -900,11 +904,12 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
     const f2_t K2 = pk2(K, K), M2K = pk2(m2K, m2K);
     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
-        __syncthreads();
-        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        if (cb != c0) {  // the first tile was staged with the residual columns
+            __syncthreads();  // every warp is done with the previous tile and its s_g sums
+            stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
@@ -1063,6 +1068,8 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
     float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
     float* col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 + lane;  // this lane's column delta_t
     const int region = blockIdx.x;
+    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
+    if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(STAGE_CELLS, c1 - c0), s_kxy, s_kzw, s_grp);
     const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
     const bool jok = j < k.Nd;
     const int lo_j = jok ? wlo[(int64_t)region * k.Nd + j] : -1;
@@ -1085,11 +1092,12 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
     const f2_t K2 = pk2(K, K), M2K = pk2(m2K, m2K);
     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-    const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
     for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
         const int nc = min(STAGE_CELLS, c1 - cb);
-        __syncthreads();
-        stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        if (cb != c0) {  // the first tile was staged with the residual columns
+            __syncthreads();  // every warp is done with the previous tile and its s_g sums
+            stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
+        }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
