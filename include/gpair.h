@@ -113,13 +113,20 @@ typedef struct {
     int32_t mode;      /* 0 = NPC x=(z+eps)^2 + Adam (paper);
                           1 = clamp: state z holds x, x <- max(x - lr g, 0) (R15)       */
     /* Vessel continuity regularisation (Eqs. 20-23; row f2).
-     * lam = 0 disables it (the paper's lambda = 0 runs); lam > 0 needs
-     * world == 1 and grid[0] grid[1] grid[2] == M with the kernels in grid
-     * order i = ix + nx (iy + ny iz) (the order R_VCR's differences use). */
+     * lam = 0 disables it (the paper's lambda = 0 runs).  lam > 0 needs the
+     * kernels in grid order i = ix + nx (iy + ny iz) (the order R_VCR's
+     * differences use): at world == 1 grid[0] grid[1] grid[2] == M; at
+     * world > 1 grid is the GLOBAL grid and each rank's M_local kernels are
+     * the z planes [z0, z0 + M_local / (nx ny)) (>= 2 planes), ranks in z
+     * order (rank 0 from z0 = 0, the last rank up to n_z).  The library then
+     * exchanges 2 halo planes of z with ranks r-1 and r+1 (ncclSend/ncclRecv)
+     * and all-reduces the fp64 value of R_VCR (8 bytes); the gradient stays
+     * rank-local. */
     float lam;         /* lambda of Eq. 23 (>= 0)                                        */
     float beta;        /* beta of Eq. 20: R_VCR = R_H + beta R_TV                        */
     float eps_reg;     /* smoothing epsilon inside both square roots (V4), > 0           */
     int32_t grid[3];   /* (n_x, n_y, n_z) voxel grid of the kernel order                 */
+    int32_t z0;        /* world > 1, lam > 0: first global z plane of this rank's slab    */
 } gpair_step;
 
 /* Accumulated device time of the library's own kernels (gpair_profile_*). */
@@ -205,6 +212,23 @@ gpair_status gpair_adjoint(gpair_ctx* ctx, const float* residual, float* grad, v
  * Errors: INVALID_ARGUMENT (NULL x, bad grid, eps <= 0, non-finite beta), CUDA. */
 gpair_status gpair_vcr(gpair_ctx* ctx, const int32_t* grid, const float* x, float beta, float eps,
                        float* grad, float* value, void* stream);
+
+/* R_VCR restricted to a z slab (the kernel-sharded form of gpair_vcr, row f2;
+ * the same operators and readings V1-V4).  The own planes [z0, z0 + nz_own)
+ * of the GLOBAL grid get their exact gradient entries of the whole-grid
+ * R_VCR, and value receives the whole-grid sum restricted to the own voxels,
+ * so the slabs' values add up to gpair_vcr's value and their gradients
+ * concatenate to its gradient.
+ * grid:   HOST int32[3] global (n_x, n_y, n_z).
+ * x_ext:  DEVICE image on the planes [ext_z0, ext_z0 + ext_nz), which must
+ *         contain [max(0, z0 - 2), min(n_z, z0 + nz_own + 2)) (the halo the
+ *         stencils and their adjoints reach); index ix + n_x (iy + n_y (iz - ext_z0)).
+ * grad:   DEVICE [n_x n_y nz_own] output, or NULL.  value: DEVICE float, or NULL.
+ * Errors: INVALID_ARGUMENT (as gpair_vcr; slab outside the grid; halo not
+ * covered), CUDA. */
+gpair_status gpair_vcr_slab(gpair_ctx* ctx, const int32_t* grid, int32_t z0, int32_t nz_own,
+                            const float* x_ext, int32_t ext_z0, int32_t ext_nz, float beta,
+                            float eps, float* grad, float* value, void* stream);
 
 /* One iteration of Algorithm 2:
  *   x = (z + eps)^2 (mode 0) or x = z (mode 1);  y = A x  [+ allreduce];

@@ -74,9 +74,14 @@ struct NcclApi {
     nccl_res_t (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     nccl_res_t (*CommDestroy)(void*) = nullptr;
     const char* (*GetErrorString)(nccl_res_t) = nullptr;
+    // point-to-point (VCR z-slab halo exchange, row f2)
+    nccl_res_t (*Send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    nccl_res_t (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    nccl_res_t (*GroupStart)() = nullptr;
+    nccl_res_t (*GroupEnd)() = nullptr;
 };
 NcclApi g_nccl;
-constexpr int NCCL_FLOAT32 = 7, NCCL_SUM = 0;
+constexpr int NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 bool nccl_load() {
     if (g_nccl.tried) return g_nccl.ok;
@@ -89,7 +94,12 @@ bool nccl_load() {
     g_nccl.AllReduce = (nccl_res_t(*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
     g_nccl.CommDestroy = (nccl_res_t(*)(void*))dlsym(h, "ncclCommDestroy");
     g_nccl.GetErrorString = (const char* (*)(nccl_res_t))dlsym(h, "ncclGetErrorString");
-    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+    g_nccl.Send = (nccl_res_t(*)(const void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclSend");
+    g_nccl.Recv = (nccl_res_t(*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclRecv");
+    g_nccl.GroupStart = (nccl_res_t(*)())dlsym(h, "ncclGroupStart");
+    g_nccl.GroupEnd = (nccl_res_t(*)())dlsym(h, "ncclGroupEnd");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy && g_nccl.Send &&
+                g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd;
     return g_nccl.ok;
 }
 
@@ -190,6 +200,7 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_vcr_u);
     cudaFree(c->d_vcr_part);
     cudaFree(c->d_vcr_g);
+    cudaFree(c->d_vcr_x);
     prof_drain(c);
     for (auto e : c->prof_free) cudaEventDestroy(e);
     for (auto e : c->ev_f)
@@ -251,6 +262,61 @@ gpair_status allreduce(gpair_ctx* c, float* y, cudaStream_t st) {
         return fail(c, GPAIR_ERR_NCCL,
                     std::string("ncclAllReduce failed: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
     return GPAIR_OK;
+}
+
+gpair_status nccl_check(gpair_ctx* c, nccl_res_t r, const char* what) {
+    if (r == 0) return GPAIR_OK;
+    return fail(c, GPAIR_ERR_NCCL, std::string(what) + " failed: " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+}
+
+// R_VCR under kernel sharding (row f2): rank r owns the
+// z planes [z0, z0 + nzo) of the global grid, ranks in z order.  Its state's
+// own planes are copied into c->d_vcr_x between HALO planes received from each
+// neighbour (ncclSend/ncclRecv in one group: the 2 planes next to the slab
+// boundary go to and come from ranks r - 1 and r + 1), then the slab kernels
+// give the own planes' gradient and the slab's value, which one 8-byte
+// all-reduce sums into the global R_VCR (d_vcr_part[vcr_nb]).
+gpair_status vcr_sharded(gpair_ctx* c, const gpair_step* s, const float* z, int npc, cudaStream_t st) {
+    constexpr int HALO = 2;  // the stencils' reach (gpair_vcr.cu)
+    const int64_t P = (int64_t)s->grid[0] * s->grid[1];
+    const int nzo = (int)(c->M / P), z0 = s->z0;
+    const int lo = c->rank > 0 ? HALO : 0, hi = c->rank < c->world - 1 ? HALO : 0;
+    const int64_t n = P * (lo + nzo + hi);
+    if (c->vcr_x_n != n) {
+        cudaFree(c->d_vcr_x);
+        c->d_vcr_x = nullptr;
+        c->vcr_x_n = 0;
+        API_CUDA(c, cudaMalloc(&c->d_vcr_x, sizeof(float) * (size_t)n), "vcr halo buffer");
+        c->vcr_x_n = n;
+        c->workspace_bytes += (int64_t)sizeof(float) * n;
+    }
+    float* xb = c->d_vcr_x;
+    API_CUDA(c, gpair::vcr_slab_ensure(c, s->grid, z0, nzo), "vcr workspace");  // d_vcr_g exists
+    API_CUDA(c, cudaMemcpyAsync(xb + P * lo, z, sizeof(float) * (size_t)c->M, cudaMemcpyDeviceToDevice, st),
+             "vcr own planes");
+    gpair_status gs = nccl_check(c, g_nccl.GroupStart(), "ncclGroupStart");
+    if (gs) return gs;
+    if (lo) {
+        gs = nccl_check(c, g_nccl.Send(z, (size_t)(P * HALO), NCCL_FLOAT32, c->rank - 1, c->nccl, st), "ncclSend");
+        if (!gs) gs = nccl_check(c, g_nccl.Recv(xb, (size_t)(P * HALO), NCCL_FLOAT32, c->rank - 1, c->nccl, st), "ncclRecv");
+    }
+    if (hi && !gs) {
+        gs = nccl_check(c, g_nccl.Send(z + P * (nzo - HALO), (size_t)(P * HALO), NCCL_FLOAT32, c->rank + 1, c->nccl, st),
+                        "ncclSend");
+        if (!gs)
+            gs = nccl_check(c, g_nccl.Recv(xb + P * (lo + nzo), (size_t)(P * HALO), NCCL_FLOAT32, c->rank + 1, c->nccl, st),
+                            "ncclRecv");
+    }
+    gpair_status ge = nccl_check(c, g_nccl.GroupEnd(), "ncclGroupEnd");
+    if (gs) return gs;
+    if (ge) return ge;
+    API_CUDA(c, gpair::launch_vcr_slab(c, s->grid, z0, nzo, xb, z0 - lo, npc, s->eps_npc, s->beta, s->eps_reg,
+                                       c->d_vcr_g, nullptr, st),
+             "vcr (slab)");
+    API_CUDA(c, gpair::launch_vcr_total(c, st), "vcr total");
+    return nccl_check(c, g_nccl.AllReduce(c->d_vcr_part + c->vcr_nb, c->d_vcr_part + c->vcr_nb, 1, NCCL_FLOAT64, NCCL_SUM,
+                                          c->nccl, st),
+                      "ncclAllReduce (R_VCR)");
 }
 
 }  // namespace
@@ -583,6 +649,27 @@ gpair_status gpair_vcr(gpair_ctx* c, const int32_t* grid, const float* x, float 
     return GPAIR_OK;
 }
 
+gpair_status gpair_vcr_slab(gpair_ctx* c, const int32_t* grid, int32_t z0, int32_t nz_own, const float* x_ext,
+                            int32_t ext_z0, int32_t ext_nz, float beta, float eps, float* grad, float* value,
+                            void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    if (!x_ext) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "x_ext is NULL");
+    gpair_status gs = check_vcr_args(c, grid, beta, eps);
+    if (gs) return gs;
+    int zu0, zu1, zx0, zx1;
+    if (gpair::vcr_slab_ranges(grid, z0, nz_own, &zu0, &zu1, &zx0, &zx1) != cudaSuccess)
+        return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "own planes [z0, z0 + nz_own) not inside the grid");
+    if (ext_z0 > zx0 || (int64_t)ext_z0 + ext_nz < zx1 || ext_z0 < 0 || (int64_t)ext_z0 + ext_nz > grid[2])
+        return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "x_ext must cover planes [max(0, z0-2), min(n_z, z0+nz_own+2))");
+    gs = sticky_check(c);
+    if (gs) return gs;
+    cudaStream_t st = (cudaStream_t)stream;
+    ProfScope ps(c, GPAIR_PROF_VCR, st);
+    API_CUDA(c, gpair::launch_vcr_slab(c, grid, z0, nz_own, x_ext, ext_z0, 0, 0.f, beta, eps, grad, value, st),
+             "vcr (slab)");
+    return GPAIR_OK;
+}
+
 gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const float* b, const gpair_step* s,
                            float* signals_out, float* x_out, float* loss_out, void* stream) {
     if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
@@ -596,21 +683,37 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     const bool reg = s->lam != 0.f;
     if (reg) {
         if (!(s->lam > 0.f) || !std::isfinite(s->lam)) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam must be >= 0");
-        if (c->world != 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam > 0 needs world == 1 (whole grid per rank)");
         gpair_status gs = check_vcr_args(c, s->grid, s->beta, s->eps_reg);
         if (gs) return gs;
-        if ((int64_t)s->grid[0] * s->grid[1] * s->grid[2] != c->M)
-            return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid[0] grid[1] grid[2] != n_kernels");
+        const int64_t P = (int64_t)s->grid[0] * s->grid[1];
+        if (c->world == 1) {
+            if (P * s->grid[2] != c->M) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid[0] grid[1] grid[2] != n_kernels");
+        } else {  // z slab of the global grid (ranks in z order)
+            if (c->M % P) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "n_kernels is not whole z planes of grid");
+            const int64_t nzo = c->M / P;
+            if (nzo < 2) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam > 0 at world > 1 needs >= 2 z planes per rank");
+            if (s->z0 < 0 || s->z0 + nzo > s->grid[2] || (c->rank == 0 && s->z0 != 0) ||
+                (c->rank == c->world - 1 && s->z0 + nzo != s->grid[2]))
+                return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "z0 / slab does not fit the global grid in rank order");
+        }
     }
     cudaStream_t st = (cudaStream_t)stream;
     const int npc = s->mode == 0;
     float* y = signals_out ? signals_out : c->d_y;
     if (reg) {  // R_VCR and its gradient at the pre-update x (Alg. 2)
         ProfScope ps(c, GPAIR_PROF_VCR, st);
-        API_CUDA(c, gpair::vcr_ensure(c, c->M), "vcr workspace");
-        API_CUDA(c, gpair::launch_vcr(c, s->grid, z, npc, s->eps_npc, s->beta, s->eps_reg, c->d_vcr_g, nullptr, st),
-                 "vcr");
+        if (c->world == 1) {
+            API_CUDA(c, gpair::vcr_slab_ensure(c, s->grid, 0, s->grid[2]), "vcr workspace");  // d_vcr_g exists
+            API_CUDA(c, gpair::launch_vcr(c, s->grid, z, npc, s->eps_npc, s->beta, s->eps_reg, c->d_vcr_g, nullptr, st),
+                     "vcr");
+        } else {
+            gpair_status gs = vcr_sharded(c, s, z, npc, st);
+            if (gs) return gs;
+        }
     }
+    // fp64 R_VCR for the loss: the per-block partials (world 1) or the all-reduced total
+    const double* reg_part = reg ? (c->world == 1 ? c->d_vcr_part : c->d_vcr_part + c->vcr_nb) : nullptr;
+    const int32_t reg_n = reg ? (c->world == 1 ? c->vcr_nb : 1) : 0;
     EpiParams ep{};
     const double N = (double)c->Nd * (double)c->Nt;
     ep.scale = s->grad_scale > 0.f ? s->grad_scale : (float)(2.0 / N);
@@ -677,7 +780,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
             ProfScope ps(c, GPAIR_PROF_LOSS, s2);
             float* lo = loss_out ? loss_out : (float*)(c->d_count);
             API_CUDA(c,
-                     reg ? gpair::launch_loss(c, lo, s2, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
+                     reg ? gpair::launch_loss(c, lo, s2, reg_part, reg_n, (double)s->lam)
                          : gpair::launch_loss(c, lo, s2),
                      "loss");
         }
@@ -710,7 +813,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
         ProfScope ps(c, GPAIR_PROF_LOSS, st);
         float* lo = loss_out ? loss_out : (float*)(c->d_count);  // scratch word when only checking
         API_CUDA(c,
-                 reg ? gpair::launch_loss(c, lo, st, c->d_vcr_part, gpair::vcr_blocks(c->M), (double)s->lam)
+                 reg ? gpair::launch_loss(c, lo, st, reg_part, reg_n, (double)s->lam)
                      : gpair::launch_loss(c, lo, st),
                  "loss");
         if (c->flags & GPAIR_CHECK_FINITE) {

@@ -76,10 +76,13 @@ struct gpair_ctx_s {
     float* d_gnear = nullptr;       // [M] near-field adjoint terms, caller order
 
     // VCR regulariser workspaces (row f2, gpair_vcr.cu), allocated on first use
-    int64_t vcr_M = 0;
-    float* d_vcr_u = nullptr;     // [9][M] normalised difference fields
-    double* d_vcr_part = nullptr; // [ceil(M/256)] per-block fp64 values
-    float* d_vcr_g = nullptr;     // [M] dR/dx (caller order)
+    int64_t vcr_M = 0, vcr_Mo = 0; // voxels of the u planes / of the own planes
+    int32_t vcr_nb = 0;           // per-block partials of the last launch_vcr_slab
+    float* d_vcr_u = nullptr;     // [9][vcr_M] normalised difference fields
+    double* d_vcr_part = nullptr; // [vcr_nb + 1] per-block fp64 values, then the slab total
+    float* d_vcr_g = nullptr;     // [vcr_Mo] dR/dx (caller order)
+    float* d_vcr_x = nullptr;     // world > 1: own z planes + halos (NCCL send/recv)
+    int64_t vcr_x_n = 0;
 
     int64_t workspace_bytes = 0;
     std::string err;
@@ -182,7 +185,12 @@ cudaError_t launch_near_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_near_adjoint(gpair_ctx* c, const float* resid, cudaStream_t st);
 
 // VCR regulariser (gpair_vcr.cu); partial values stay in c->d_vcr_part
-cudaError_t vcr_ensure(gpair_ctx* c, int64_t M);
+cudaError_t vcr_ensure(gpair_ctx* c, int64_t Mu, int64_t Mo);
+cudaError_t vcr_slab_ranges(const int32_t* dims, int z0, int nzo, int* zu0, int* zu1, int* zx0, int* zx1);
+cudaError_t launch_vcr_slab(gpair_ctx* c, const int32_t* dims, int z0, int nzo, const float* src, int zb, int npc,
+                            float eps_npc, float beta, float eps, float* grad, float* value, cudaStream_t st);
+cudaError_t launch_vcr_total(gpair_ctx* c, cudaStream_t st);
+cudaError_t vcr_slab_ensure(gpair_ctx* c, const int32_t* dims, int z0, int nzo);
 cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int npc, float eps_npc, float beta,
                        float eps, float* grad, float* value, cudaStream_t st);
 inline int32_t vcr_blocks(int64_t M) { return (int32_t)((M + 255) / 256); }

@@ -13,6 +13,16 @@
 //                per-block partial values (fixed-order reduction later)
 //   k_vcr_grad   gather of the adjoint stencils: g = sum_pq D_pq^T u_pq
 //                + beta sum_d D_d^T u_d.
+// Slab form (kernel sharding): the grid is the GLOBAL
+// (nx, ny, NZ) grid; x is given on planes [zb, zb + nzb) (the rank's own
+// planes [zo0, zo1) plus halos), u is computed on the planes [zu0, zu1) =
+// [zo0 - 1, zo1 + 1), extended to plane 0 when zo0 <= 2 and to plane NZ-1
+// when zo1 >= NZ-2 (every plane the adjoint stencils of the own planes reach,
+// including the clamped-centre folds of u(0) and u(NZ-1)); u(p) reads x on
+// [p-1, p+1] (clamped centres stay inside [0, 2] / [NZ-3, NZ-1]), so x is
+// needed on [zo0 - 2, zo1 + 2) clipped: a 2-plane halo.  Values and gradients
+// are produced for the own planes only.  A whole grid is the slab zb = zu0 =
+// zo0 = 0, zo1 = NZ, with identical arithmetic.
 #include "gpair_ctx.h"
 
 namespace gpair {
@@ -20,7 +30,10 @@ namespace gpair {
 namespace {
 
 struct Grid {
-    int nx, ny, nz;
+    int nx, ny, nz;  // global grid
+    int zb;          // global z of plane 0 of the x buffer
+    int zu0;         // global z of plane 0 of u
+    int zo0, zo1;    // own planes (values and gradients)
 };
 
 __device__ __forceinline__ float xval(const float* __restrict__ src, int npc, float eps_npc, int64_t i) {
@@ -28,15 +41,16 @@ __device__ __forceinline__ float xval(const float* __restrict__ src, int npc, fl
     return npc ? (v + eps_npc) * (v + eps_npc) : v;  // x = (z + eps)^2 (Eq. 18) when the state is z
 }
 
+// u is [9][M] over the planes [zu0, zu0 + M / (nx ny)).
 __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_npc, Grid G, float beta, float eps,
                             float* __restrict__ u, int64_t M, double* __restrict__ part) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double val = 0.0;
     if (i < M) {
-        const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = (int)(i / ((int64_t)G.nx * G.ny));
+        const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = G.zu0 + (int)(i / ((int64_t)G.nx * G.ny));
         const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
-        const float x0 = xval(src, npc, eps_npc, i);
-        auto at = [&](int a, int b, int c) { return xval(src, npc, eps_npc, a * sx + b * sy + c * sz); };
+        auto at = [&](int a, int b, int c) { return xval(src, npc, eps_npc, a * sx + b * sy + (c - G.zb) * sz); };
+        const float x0 = at(ix, iy, iz);
         // forward differences (V1)
         const int xp = min(ix + 1, G.nx - 1), yp = min(iy + 1, G.ny - 1), zp = min(iz + 1, G.nz - 1);
         const float dx = at(xp, iy, iz) - x0, dy = at(ix, yp, iz) - x0, dz = at(ix, iy, zp) - x0;
@@ -71,7 +85,7 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
         u[6 * M + i] = 2.f * dxy * ih;
         u[7 * M + i] = 2.f * dxz * ih;
         u[8 * M + i] = 2.f * dyz * ih;
-        val = (double)sh + (double)beta * (double)stv;
+        if (iz >= G.zo0 && iz < G.zo1) val = (double)sh + (double)beta * (double)stv;
     }
     __shared__ double s_red[32];
     for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
@@ -95,11 +109,14 @@ __device__ __forceinline__ float fold_pp(const float* __restrict__ up, int64_t i
     return s;
 }
 
-__global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int64_t M, float* __restrict__ g) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= M) return;
-    const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = (int)(i / ((int64_t)G.nx * G.ny));
+// u: [9][M] over the planes from zu0; g: [Mo] over the own planes.
+__global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int64_t M, int64_t Mo,
+                           float* __restrict__ g) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= Mo) return;
     const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
+    const int ix = (int)(j % G.nx), iy = (int)((j / G.nx) % G.ny), iz = G.zo0 + (int)(j / sz);
+    const int64_t i = j + (int64_t)(G.zo0 - G.zu0) * sz;  // index into u
     const float* ux = u;
     const float* uy = u + M;
     const float* uz = u + 2 * M;
@@ -121,8 +138,8 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
         if (G.ny >= 3) gh += fold_pp(up, r0, sy, iy - 1, G.ny) - 2.f * fold_pp(up, r0, sy, iy, G.ny) + fold_pp(up, r0, sy, iy + 1, G.ny);
     }
     {
-        const int64_t r0 = i - (int64_t)iz * sz;
-        const float* up = u + 5 * M;
+        const int64_t r0 = i - (int64_t)iz * sz;  // global plane 0 (may precede u's first plane;
+        const float* up = u + 5 * M;                // fold_pp only reads planes inside u)
         if (G.nz >= 3) gh += fold_pp(up, r0, sz, iz - 1, G.nz) - 2.f * fold_pp(up, r0, sz, iz, G.nz) + fold_pp(up, r0, sz, iz + 1, G.nz);
     }
     // mixed: taps (+1 at (a+1,b+1), -1 at (a+1,b), -1 at (a,b+1), +1 at (a,b)),
@@ -139,10 +156,11 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
     gh += mixed_T(u + 6 * M, ix, G.nx, sx, iy, G.ny, sy);
     gh += mixed_T(u + 7 * M, ix, G.nx, sx, iz, G.nz, sz);
     gh += mixed_T(u + 8 * M, iy, G.ny, sy, iz, G.nz, sz);
-    g[i] = gh + beta * gtv;
+    g[j] = gh + beta * gtv;
 }
 
-__global__ void k_vcr_sum(const double* __restrict__ part, int n, float* __restrict__ value) {
+__global__ void k_vcr_sum(const double* __restrict__ part, int n, float* __restrict__ value,
+                          double* __restrict__ total) {
     __shared__ double s[1024];
     double a = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) a += part[i];
@@ -152,56 +170,101 @@ __global__ void k_vcr_sum(const double* __restrict__ part, int n, float* __restr
         if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) value[0] = (float)s[0];
+    if (threadIdx.x == 0) {
+        if (value) value[0] = (float)s[0];
+        if (total) total[0] = s[0];
+    }
 }
 
 }  // namespace
 
-cudaError_t vcr_ensure(gpair_ctx* c, int64_t M) {
-    if (c->vcr_M == M && c->d_vcr_u) return cudaSuccess;
+cudaError_t vcr_ensure(gpair_ctx* c, int64_t Mu, int64_t Mo) {
+    if (c->vcr_M == Mu && c->vcr_Mo == Mo && c->d_vcr_u) return cudaSuccess;
     cudaFree(c->d_vcr_u);
     cudaFree(c->d_vcr_part);
     cudaFree(c->d_vcr_g);
     c->d_vcr_u = nullptr;
     c->d_vcr_part = nullptr;
     c->d_vcr_g = nullptr;
-    const int nb = (int)((M + 255) / 256);
-    cudaError_t e = cudaMalloc(&c->d_vcr_u, sizeof(float) * 9 * (size_t)M);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_part, sizeof(double) * nb);
-    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_g, sizeof(float) * (size_t)M);
+    c->vcr_M = c->vcr_Mo = 0;
+    const int nb = vcr_blocks(Mu);
+    // d_vcr_part carries one extra double: the (all-reduced) total of a slab
+    cudaError_t e = cudaMalloc(&c->d_vcr_u, sizeof(float) * 9 * (size_t)Mu);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_part, sizeof(double) * (nb + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_g, sizeof(float) * (size_t)Mo);
     if (e == cudaSuccess) {
-        c->vcr_M = M;
-        c->workspace_bytes += (int64_t)(sizeof(float) * 10 * M + sizeof(double) * nb);
+        c->vcr_M = Mu;
+        c->vcr_Mo = Mo;
+        c->workspace_bytes += (int64_t)(sizeof(float) * (9 * Mu + Mo) + sizeof(double) * (nb + 1));
     }
     return e;
 }
 
-// value (device float, nullable) and gradient (device [M], nullable) of
-// R_VCR at x (npc: x = (src + eps_npc)^2).  Returns the per-block partials in
-// c->d_vcr_part (count = blocks) for fusion into the IR loss.
-cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int npc, float eps_npc, float beta,
-                       float eps, float* grad, float* value, cudaStream_t st) {
-    const int64_t M = (int64_t)dims[0] * dims[1] * dims[2];
-    cudaError_t e = vcr_ensure(c, M);
+cudaError_t vcr_slab_ranges(const int32_t* dims, int z0, int nzo, int* zu0, int* zu1, int* zx0, int* zx1) {
+    const int NZ = dims[2];
+    if (z0 < 0 || nzo < 1 || z0 + nzo > NZ) return cudaErrorInvalidValue;
+    const int z1 = z0 + nzo;
+    *zu0 = z0 <= 2 ? 0 : z0 - 1;
+    *zu1 = z1 >= NZ - 2 ? NZ : z1 + 1;
+    *zx0 = z0 - 2 > 0 ? z0 - 2 : 0;
+    *zx1 = z1 + 2 < NZ ? z1 + 2 : NZ;
+    return cudaSuccess;
+}
+
+// Workspaces of the slab (call before passing c->d_vcr_g as the gradient).
+cudaError_t vcr_slab_ensure(gpair_ctx* c, const int32_t* dims, int z0, int nzo) {
+    int zu0, zu1, zx0, zx1;
+    cudaError_t e = vcr_slab_ranges(dims, z0, nzo, &zu0, &zu1, &zx0, &zx1);
     if (e != cudaSuccess) return e;
-    const Grid G{dims[0], dims[1], dims[2]};
-    const int nb = (int)((M + 255) / 256);
+    const int64_t P = (int64_t)dims[0] * dims[1];
+    return vcr_ensure(c, P * (zu1 - zu0), P * nzo);
+}
+
+// R_VCR terms of the own planes [z0, z0 + nzo) of the global grid dims, with
+// src on the planes [zb, ...) covering vcr_slab_ranges' [zx0, zx1) (npc:
+// x = (src + eps_npc)^2).  Gradient -> grad ([nx ny nzo], nullable); the
+// slab's value -> value (device float, nullable); per-block partials of the
+// slab's value stay in c->d_vcr_part (count c->vcr_nb) for the IR loss.
+cudaError_t launch_vcr_slab(gpair_ctx* c, const int32_t* dims, int z0, int nzo, const float* src, int zb, int npc,
+                            float eps_npc, float beta, float eps, float* grad, float* value, cudaStream_t st) {
+    int zu0, zu1, zx0, zx1;
+    cudaError_t e = vcr_slab_ranges(dims, z0, nzo, &zu0, &zu1, &zx0, &zx1);
+    if (e != cudaSuccess) return e;
+    const int64_t P = (int64_t)dims[0] * dims[1];
+    const int64_t Mu = P * (zu1 - zu0), Mo = P * nzo;
+    e = vcr_ensure(c, Mu, Mo);
+    if (e != cudaSuccess) return e;
+    const Grid G{dims[0], dims[1], dims[2], zb, zu0, z0, z0 + nzo};
+    const int nb = vcr_blocks(Mu);
+    c->vcr_nb = nb;
     ++c->n_launch;
-    k_vcr_terms<<<nb, 256, 0, st>>>(src, npc, eps_npc, G, beta, eps, c->d_vcr_u, M, c->d_vcr_part);
+    k_vcr_terms<<<nb, 256, 0, st>>>(src, npc, eps_npc, G, beta, eps, c->d_vcr_u, Mu, c->d_vcr_part);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (grad) {
         ++c->n_launch;
-        k_vcr_grad<<<nb, 256, 0, st>>>(c->d_vcr_u, G, beta, M, grad);
+        k_vcr_grad<<<vcr_blocks(Mo), 256, 0, st>>>(c->d_vcr_u, G, beta, Mu, Mo, grad);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     if (value) {
         ++c->n_launch;
-        k_vcr_sum<<<1, 1024, 0, st>>>(c->d_vcr_part, nb, value);
+        k_vcr_sum<<<1, 1024, 0, st>>>(c->d_vcr_part, nb, value, nullptr);
         e = cudaGetLastError();
     }
     return e;
+}
+
+// The slab's fp64 value -> c->d_vcr_part[c->vcr_nb] (for the all-reduce).
+cudaError_t launch_vcr_total(gpair_ctx* c, cudaStream_t st) {
+    ++c->n_launch;
+    k_vcr_sum<<<1, 1024, 0, st>>>(c->d_vcr_part, c->vcr_nb, nullptr, c->d_vcr_part + c->vcr_nb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vcr(gpair_ctx* c, const int32_t* dims, const float* src, int npc, float eps_npc, float beta,
+                       float eps, float* grad, float* value, cudaStream_t st) {
+    return launch_vcr_slab(c, dims, 0, dims[2], src, 0, npc, eps_npc, beta, eps, grad, value, st);
 }
 
 }  // namespace gpair

@@ -61,6 +61,7 @@ class Step(ctypes.Structure):
         ("beta", ctypes.c_float),
         ("eps_reg", ctypes.c_float),
         ("grid", ctypes.c_int32 * 3),
+        ("z0", ctypes.c_int32),
     ]
 
 
@@ -119,6 +120,8 @@ def lib():
             "gpair_iterate": (st, [vp, vp, vp, vp, vp, ctypes.POINTER(Step), vp, vp, vp, vp]),
             "gpair_count_pair_samples": (st, [vp, ctypes.POINTER(i64), vp]),
             "gpair_vcr": (st, [vp, ctypes.POINTER(i32), vp, ctypes.c_float, ctypes.c_float, vp, vp, vp]),
+            "gpair_vcr_slab": (st, [vp, ctypes.POINTER(i32), i32, i32, vp, i32, i32, ctypes.c_float, ctypes.c_float,
+                                    vp, vp, vp]),
             "gpair_get_info": (st, [vp, ctypes.POINTER(Info)]),
             "gpair_destroy": (st, [vp]),
             "gpair_profile_enable": (st, [vp, ctypes.c_int]),
@@ -251,13 +254,14 @@ class Context:
         return out
 
     def iterate(self, z, m, v, b, *, lr, step, mode=0, beta1=0.9, beta2=0.999, adam_eps=1e-8, eps_npc=1e-8,
-                grad_scale=0.0, lam=0.0, beta=0.0, eps_reg=1e-8, grid=None, signals_out=None, x_out=None,
+                grad_scale=0.0, lam=0.0, beta=0.0, eps_reg=1e-8, grid=None, z0=0, signals_out=None, x_out=None,
                 loss_out=None, stream=None):
         """One Alg. 2 iteration; lam > 0 adds lam R_VCR (Eqs. 20-23) over the
-        voxel grid `grid` = (nx, ny, nz) of the kernel order."""
+        voxel grid `grid` = (nx, ny, nz) of the kernel order; at world > 1
+        `grid` is the global grid and `z0` this rank's first z plane."""
         g3 = (ctypes.c_int32 * 3)(*(grid if grid is not None else (0, 0, 0)))
         s = Step(lr=lr, beta1=beta1, beta2=beta2, adam_eps=adam_eps, eps_npc=eps_npc, grad_scale=grad_scale,
-                 step=int(step), mode=int(mode), lam=lam, beta=beta, eps_reg=eps_reg, grid=g3)
+                 step=int(step), mode=int(mode), lam=lam, beta=beta, eps_reg=eps_reg, grid=g3, z0=int(z0))
         n = self.M
         _check(lib().gpair_iterate(self._h, _ptr(z, numel=n, name="z"), _ptr(m, numel=n, name="m"),
                                    _ptr(v, numel=n, name="v"), _ptr(b, numel=self.Nd * self.Nt, name="b"),
@@ -274,6 +278,17 @@ class Context:
         _check(lib().gpair_vcr(self._h, g3, _ptr(x, numel=n, name="x"), float(beta), float(eps),
                                _ptr(grad, numel=n, name="grad"), _ptr(value, numel=1, name="value"),
                                _stream(stream)), self._h)
+
+    def vcr_slab(self, x_ext, grid, z0, nz_own, ext_z0, *, beta, eps=1e-8, grad=None, value=None, stream=None):
+        """R_VCR's own-plane part of the z slab [z0, z0 + nz_own) of the global
+        grid (gpair_vcr_slab): x_ext holds the planes from ext_z0 (the slab and
+        its halos), grad gets [nx ny nz_own] entries, value the slab's share."""
+        P = int(grid[0]) * int(grid[1])
+        ext_nz = int(x_ext.numel()) // P if P > 0 else 0
+        g3 = (ctypes.c_int32 * 3)(*(int(d) for d in grid))
+        _check(lib().gpair_vcr_slab(self._h, g3, int(z0), int(nz_own), _ptr(x_ext, name="x_ext"), int(ext_z0), ext_nz,
+                                    float(beta), float(eps), _ptr(grad, numel=P * int(nz_own), name="grad"),
+                                    _ptr(value, numel=1, name="value"), _stream(stream)), self._h)
 
     def count_pair_samples(self, stream=None):
         out = ctypes.c_int64()

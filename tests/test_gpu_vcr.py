@@ -85,6 +85,60 @@ def test_vcr_constant_image_closed_form(ctx):
     assert np.abs(g).max() == 0.0
 
 
+SLABS = [((6, 5, 14), [0, 4, 6, 9, 14]), ((6, 5, 14), [0, 1, 2, 3, 11, 12, 13, 14]), ((33, 17, 9), [0, 2, 5, 9]),
+         ((70, 50, 40), [0, 5, 10, 15, 20, 25, 30, 35, 40]), ((4, 3, 2), [0, 1, 2]), ((3, 4, 5), [0, 5])]
+
+
+@pytest.mark.parametrize("dims,cuts", SLABS)
+@pytest.mark.parametrize("halo", ["exact", "whole"])
+def test_vcr_slabs_match_whole_grid(ctx, dims, cuts, halo):
+    """Kernel-sharded R_VCR (row f2, gpair_vcr_slab): each z slab, given its
+    2-plane halo ('exact') or the whole grid ('whole'), yields the own-plane
+    entries of the whole-grid gradient, and the slab values add up to the
+    whole-grid value (oracle/vcr.py on the whole grid)."""
+    nx, ny, nz = dims
+    P = nx * ny
+    rng = np.random.default_rng(len(cuts) + nz)
+    x = rng.uniform(0.0, 1.0, P * nz).astype(np.float32)
+    v_ref, g_ref = vcr.r_vcr(x.astype(np.float64), dims, 0.6, 1e-3)
+    xs = T(x)
+    total, grads = 0.0, []
+    for z0, z1 in zip(cuts[:-1], cuts[1:]):
+        e0, e1 = (max(0, z0 - 2), min(nz, z1 + 2)) if halo == "exact" else (0, nz)
+        g = torch.empty(P * (z1 - z0), device=dev())
+        val = torch.empty(1, device=dev())
+        ctx.vcr_slab(xs[e0 * P:e1 * P].contiguous(), dims, z0, z1 - z0, e0, beta=0.6, eps=1e-3, grad=g, value=val)
+        torch.cuda.synchronize()
+        total += float(val.item())
+        grads.append(g.cpu().numpy())
+    assert abs(total - v_ref) <= 1e-6 * abs(v_ref), (total, v_ref)
+    assert_parity(np.concatenate(grads), g_ref, f"VCR slab grad {dims} {cuts}", elementwise=False)
+
+
+def test_vcr_whole_slab_is_bit_identical_to_gpair_vcr(ctx):
+    """The whole grid as one slab runs the same arithmetic as gpair_vcr."""
+    dims = (33, 17, 9)
+    M = int(np.prod(dims))
+    x = T(np.random.default_rng(5).uniform(0.0, 1.0, M).astype(np.float32))
+    g1, g2 = torch.empty(M, device=dev()), torch.empty(M, device=dev())
+    v1, v2 = torch.empty(1, device=dev()), torch.empty(1, device=dev())
+    ctx.vcr(x, dims, beta=0.4, eps=1e-4, grad=g1, value=v1)
+    ctx.vcr_slab(x, dims, 0, dims[2], 0, beta=0.4, eps=1e-4, grad=g2, value=v2)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(v1, v2)
+
+
+def test_vcr_slab_invalid_arguments(ctx):
+    dims = (4, 4, 10)
+    x = torch.zeros(16 * 10, device=dev())
+    g = torch.empty(16 * 3, device=dev())
+    with pytest.raises(gpair.GpairError):  # halo not covered (needs planes 2..9 for the slab 4..7)
+        ctx.vcr_slab(x[16 * 3:16 * 9].contiguous(), dims, 4, 3, 3, beta=1.0, grad=g)
+    with pytest.raises(gpair.GpairError):  # slab outside the grid
+        ctx.vcr_slab(x, dims, 8, 3, 0, beta=1.0, grad=g)
+    ctx.vcr_slab(x[16 * 2:16 * 9].contiguous(), dims, 4, 3, 2, beta=1.0, grad=g)
+
+
 def test_vcr_invalid_arguments(ctx):
     x = torch.zeros(8, device=dev())
     with pytest.raises(gpair.GpairError):

@@ -102,3 +102,31 @@ def test_ir_gradient_with_vcr_vs_finite_differences():
         zm[i] -= h
         fd = (ir.loss_and_grad(zp, b, geom, hp)[0] - ir.loss_and_grad(zm, b, geom, hp)[0]) / (2 * h)
         assert fd == pytest.approx(gz[i], rel=1e-6, abs=1e-9 * np.abs(gz).max())
+
+
+@pytest.mark.parametrize("z0,z1", [(0, 4), (3, 6), (5, 9), (9, 14), (12, 14)])
+def test_gradient_halo_is_two_planes(z0, z1):
+    """Kernel sharding of R_VCR (z-slab halo exchange,
+    2 planes): the gradient on the z planes [z0, z1) of the
+    whole-grid R_VCR depends on x only through the planes [z0-2, z1+2), so a
+    2-plane halo per side is enough and a 1-plane halo is not.  Pinned on the
+    oracle alone: perturbing every plane outside the halo leaves the own-plane
+    gradient bit-identical, perturbing plane z0-2 (or z1+1) changes it."""
+    dims = (5, 4, 14)
+    nx, ny, nz = dims
+    rng = np.random.default_rng(100 + z0)
+    a = rng.uniform(0.0, 1.0, (nz, ny, nx))
+    own = slice(z0 * nx * ny, z1 * nx * ny)
+    _, g = vcr.r_vcr(a.ravel(), dims, 0.7, 1e-3)
+    b = a.copy()
+    lo, hi = max(0, z0 - 2), min(nz, z1 + 2)
+    b[:lo] = rng.uniform(0.0, 1.0, b[:lo].shape)
+    b[hi:] = rng.uniform(0.0, 1.0, b[hi:].shape)
+    _, gb = vcr.r_vcr(b.ravel(), dims, 0.7, 1e-3)
+    assert np.array_equal(g[own], gb[own])
+    for p in (z0 - 2, z1 + 1):
+        if 0 <= p < nz and not (z0 <= p < z1):
+            c = a.copy()
+            c[p] += 0.5
+            _, gc = vcr.r_vcr(c.ravel(), dims, 0.7, 1e-3)
+            assert np.abs(gc[own] - g[own]).max() > 1e-6, p
