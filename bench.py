@@ -38,6 +38,8 @@ def parse():
     p.add_argument("--op", default="exact", choices=["exact", "assa"],
                    help="exact: Eq. 7 windows (north_star); assa: the paper's ASSA operator (row f1)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--lam", type=float, default=0.0,
+                   help="lambda of Eq. 23: adds R_VCR (beta 0.5) to every iteration; at N > 1 z-slab halo exchange")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU oracle sample time")
     return p.parse_args()
@@ -179,7 +181,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2602_03893_b200 import build, gpair, inputs
-    from paper_2602_03893_b200.shard import kernel_shard, max_over_ranks, nccl_bootstrap
+    from paper_2602_03893_b200.shard import kernel_shard, max_over_ranks, nccl_bootstrap, slab_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -201,6 +203,12 @@ def main():
     s = cfg.sensors()
     M = cfg.M
     lo, hi = kernel_shard(M, world, rank)  # contiguous z-slab shard
+    vcr_kw = {}
+    if args.lam > 0:  # whole z planes per rank, the layout R_VCR's halo exchange assumes
+        P = cfg.grid[0] * cfg.grid[1]
+        z0, nzr = slab_shard(cfg.grid, world, rank)
+        lo, hi = z0 * P, (z0 + nzr) * P
+        vcr_kw = dict(lam=args.lam, beta=0.5, eps_reg=1e-8, grid=tuple(cfg.grid), z0=z0)
     c = np.ascontiguousarray(c_all[:, lo:hi])
     Ml = hi - lo
     ctx = gpair.Context(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), sigma=cfg.sig, v=cfg.v,
@@ -220,7 +228,7 @@ def main():
 
     def one_iter():
         t = step[0]
-        ctx.iterate(z, m, v, b, lr=gpair.cawr_lr(t, **eta), step=t + 1, loss_out=loss)
+        ctx.iterate(z, m, v, b, lr=gpair.cawr_lr(t, **eta), step=t + 1, loss_out=loss, **vcr_kw)
         step[0] += 1
 
     for _ in range(args.warmup):
@@ -266,7 +274,7 @@ def main():
     for _ in range(args.steps):
         b_dev.copy_(b_host, non_blocking=True)
         t = step[0]
-        ctx.iterate(z, m, v, b_dev, lr=gpair.cawr_lr(t, **eta), step=t + 1, loss_out=loss)
+        ctx.iterate(z, m, v, b_dev, lr=gpair.cawr_lr(t, **eta), step=t + 1, loss_out=loss, **vcr_kw)
         step[0] += 1
         loss_host.copy_(loss, non_blocking=True)
         torch.cuda.synchronize()
@@ -313,7 +321,8 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "operator": args.op, "kernels": M, "sensors": cfg.n_sensors, "samples": cfg.n_samples,
                    "array": cfg.array, "fs_hz": cfg.fs, "sigma_m": cfg.sig, "k": cfg.k,
-                   "step": "gpair_iterate (NPC + forward + residual/loss + adjoint + Adam)",
+                   "step": "gpair_iterate (NPC + forward + residual/loss + adjoint + Adam)"
+                           + (f" + lam {args.lam:g} R_VCR (beta 0.5)" if args.lam > 0 else ""),
                    "parallelism": f"kernel-sharded x{world}" if world > 1 else "single GPU",
                    "l2": f"working set {info['workspace_bytes'] / 2**20:.0f} MiB > 126 MB L2 (no flush needed)",
                    "layout": {k: info[k] for k in ("fwd_regions", "fwd_window", "adj_regions", "adj_window", "wmax")}},

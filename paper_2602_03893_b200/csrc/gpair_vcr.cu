@@ -47,7 +47,10 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double val = 0.0;
     if (i < M) {
-        const int ix = (int)(i % G.nx), iy = (int)((i / G.nx) % G.ny), iz = G.zu0 + (int)(i / ((int64_t)G.nx * G.ny));
+        // 32-bit coordinate division (M < 2^31 / 9 is validated at the API)
+        const unsigned q = (unsigned)i / (unsigned)G.nx;
+        const int ix = (int)((unsigned)i - q * (unsigned)G.nx), iy = (int)(q % (unsigned)G.ny),
+                  iz = G.zu0 + (int)(q / (unsigned)G.ny);
         const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
         auto at = [&](int a, int b, int c) { return xval(src, npc, eps_npc, a * sx + b * sy + (c - G.zb) * sz); };
         const float x0 = at(ix, iy, iz);
@@ -115,7 +118,9 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= Mo) return;
     const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
-    const int ix = (int)(j % G.nx), iy = (int)((j / G.nx) % G.ny), iz = G.zo0 + (int)(j / sz);
+    const unsigned q = (unsigned)j / (unsigned)G.nx;
+    const int ix = (int)((unsigned)j - q * (unsigned)G.nx), iy = (int)(q % (unsigned)G.ny),
+              iz = G.zo0 + (int)(q / (unsigned)G.ny);
     const int64_t i = j + (int64_t)(G.zo0 - G.zu0) * sz;  // index into u
     const float* ux = u;
     const float* uy = u + M;
