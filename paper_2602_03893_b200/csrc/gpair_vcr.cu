@@ -36,7 +36,7 @@ struct Grid {
     int zo0, zo1;    // own planes (values and gradients)
 };
 
-__device__ __forceinline__ float xval(const float* __restrict__ src, int npc, float eps_npc, int64_t i) {
+__device__ __forceinline__ float xval(const float* __restrict__ src, int npc, float eps_npc, int i) {
     const float v = src[i];
     return npc ? (v + eps_npc) * (v + eps_npc) : v;  // x = (z + eps)^2 (Eq. 18) when the state is z
 }
@@ -51,8 +51,10 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
         const unsigned q = (unsigned)i / (unsigned)G.nx;
         const int ix = (int)((unsigned)i - q * (unsigned)G.nx), iy = (int)(q % (unsigned)G.ny),
                   iz = G.zu0 + (int)(q / (unsigned)G.ny);
-        const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
-        auto at = [&](int a, int b, int c) { return xval(src, npc, eps_npc, a * sx + b * sy + (c - G.zb) * sz); };
+        // neighbours by 32-bit offsets from this voxel's x (|offset| < M)
+        const int sy = G.nx, sz = G.nx * G.ny;
+        const float* xc = src + ((int64_t)(iz - G.zb) * sz + (int64_t)iy * sy + ix);
+        auto at = [&](int a, int b, int c) { return xval(xc, npc, eps_npc, (a - ix) + (b - iy) * sy + (c - iz) * sz); };
         const float x0 = at(ix, iy, iz);
         // forward differences (V1)
         const int xp = min(ix + 1, G.nx - 1), yp = min(iy + 1, G.ny - 1), zp = min(iz + 1, G.nz - 1);
@@ -103,12 +105,13 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
 }
 
 // U(m) of a pure second difference along one axis: the sum of u over the
-// voxels whose clamped centre is m (m in [1, n-2]).
-__device__ __forceinline__ float fold_pp(const float* __restrict__ up, int64_t i, int64_t stride, int c, int n) {
+// voxels whose clamped centre is m (m in [1, n-2]); up points at this voxel
+// (coordinate a on the axis), offsets are 32-bit.
+__device__ __forceinline__ float fold_pp(const float* __restrict__ up, int a, int stride, int c, int n) {
     if (c < 1 || c > n - 2) return 0.f;
-    float s = up[i + (int64_t)(c)*stride];
-    if (c == 1) s += up[i];                                 // voxel 0 uses centre 1
-    if (c == n - 2) s += up[i + (int64_t)(n - 1) * stride];  // voxel n-1 uses centre n-2
+    float s = up[(c - a) * stride];
+    if (c == 1) s += up[-a * stride];                      // voxel 0 uses centre 1
+    if (c == n - 2) s += up[(n - 1 - a) * stride];         // voxel n-1 uses centre n-2
     return s;
 }
 
@@ -117,50 +120,46 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
                            float* __restrict__ g) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= Mo) return;
-    const int64_t sx = 1, sy = G.nx, sz = (int64_t)G.nx * G.ny;
+    const int sx = 1, sy = G.nx, sz = G.nx * G.ny;
     const unsigned q = (unsigned)j / (unsigned)G.nx;
     const int ix = (int)((unsigned)j - q * (unsigned)G.nx), iy = (int)(q % (unsigned)G.ny),
               iz = G.zo0 + (int)(q / (unsigned)G.ny);
     const int64_t i = j + (int64_t)(G.zo0 - G.zu0) * sz;  // index into u
-    const float* ux = u;
-    const float* uy = u + M;
-    const float* uz = u + 2 * M;
+    const float* ux = u + i;  // fields at this voxel; neighbours by 32-bit offsets
+    const float* uy = u + M + i;
+    const float* uz = u + 2 * M + i;
     // TV: (D_d^T u)(k) = u(k - e_d) [k_d >= 1] - u(k)   (u = 0 on the last index)
-    float gtv = -(ux[i] + uy[i] + uz[i]);
-    if (ix >= 1) gtv += ux[i - sx];
-    if (iy >= 1) gtv += uy[i - sy];
-    if (iz >= 1) gtv += uz[i - sz];
+    float gtv = -(ux[0] + uy[0] + uz[0]);
+    if (ix >= 1) gtv += ux[-sx];
+    if (iy >= 1) gtv += uy[-sy];
+    if (iz >= 1) gtv += uz[-sz];
     // pure second differences: g(k) = U(k-1) - 2 U(k) + U(k+1) along each axis
+    // (the z fold may reach global plane 0 / NZ-1; those lie inside u when read)
     float gh = 0.f;
     {
-        const int64_t r0 = i - (int64_t)ix * sx;  // start of the x line
-        const float* up = u + 3 * M;
-        if (G.nx >= 3) gh += fold_pp(up, r0, sx, ix - 1, G.nx) - 2.f * fold_pp(up, r0, sx, ix, G.nx) + fold_pp(up, r0, sx, ix + 1, G.nx);
+        const float* up = u + 3 * M + i;
+        if (G.nx >= 3) gh += fold_pp(up, ix, sx, ix - 1, G.nx) - 2.f * fold_pp(up, ix, sx, ix, G.nx) + fold_pp(up, ix, sx, ix + 1, G.nx);
     }
     {
-        const int64_t r0 = i - (int64_t)iy * sy;
-        const float* up = u + 4 * M;
-        if (G.ny >= 3) gh += fold_pp(up, r0, sy, iy - 1, G.ny) - 2.f * fold_pp(up, r0, sy, iy, G.ny) + fold_pp(up, r0, sy, iy + 1, G.ny);
+        const float* up = u + 4 * M + i;
+        if (G.ny >= 3) gh += fold_pp(up, iy, sy, iy - 1, G.ny) - 2.f * fold_pp(up, iy, sy, iy, G.ny) + fold_pp(up, iy, sy, iy + 1, G.ny);
     }
     {
-        const int64_t r0 = i - (int64_t)iz * sz;  // global plane 0 (may precede u's first plane;
-        const float* up = u + 5 * M;                // fold_pp only reads planes inside u)
-        if (G.nz >= 3) gh += fold_pp(up, r0, sz, iz - 1, G.nz) - 2.f * fold_pp(up, r0, sz, iz, G.nz) + fold_pp(up, r0, sz, iz + 1, G.nz);
+        const float* up = u + 5 * M + i;
+        if (G.nz >= 3) gh += fold_pp(up, iz, sz, iz - 1, G.nz) - 2.f * fold_pp(up, iz, sz, iz, G.nz) + fold_pp(up, iz, sz, iz + 1, G.nz);
     }
     // mixed: taps (+1 at (a+1,b+1), -1 at (a+1,b), -1 at (a,b+1), +1 at (a,b)),
     // u = 0 where the forward operator is 0, so only existence checks remain
-    auto mixed_T = [&](const float* um, int a, int na, int64_t sa, int b, int nb, int64_t sb) {
-        float s = um[i];
-        if (a >= 1 && b >= 1) s += um[i - sa - sb];
-        if (a >= 1) s -= um[i - sa];
-        if (b >= 1) s -= um[i - sb];
-        (void)na;
-        (void)nb;
+    auto mixed_T = [&](const float* um, int a, int sa, int b, int sb) {
+        float s = um[0];
+        if (a >= 1 && b >= 1) s += um[-sa - sb];
+        if (a >= 1) s -= um[-sa];
+        if (b >= 1) s -= um[-sb];
         return s;
     };
-    gh += mixed_T(u + 6 * M, ix, G.nx, sx, iy, G.ny, sy);
-    gh += mixed_T(u + 7 * M, ix, G.nx, sx, iz, G.nz, sz);
-    gh += mixed_T(u + 8 * M, iy, G.ny, sy, iz, G.nz, sz);
+    gh += mixed_T(u + 6 * M + i, ix, sx, iy, sy);
+    gh += mixed_T(u + 7 * M + i, ix, sx, iz, sz);
+    gh += mixed_T(u + 8 * M + i, iy, sy, iz, sz);
     g[j] = gh + beta * gtv;
 }
 
