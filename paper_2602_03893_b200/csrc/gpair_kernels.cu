@@ -860,8 +860,11 @@ __device__ __forceinline__ f2_t exp2_acc2(f2_t x) {
     return pk2(p0, p1);
 }
 
+#ifndef GPAIR_LCF_MINB
+#define GPAIR_LCF_MINB 3
+#endif
 template <int W, int SDEG>
-__global__ void __launch_bounds__(256, 3) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
+__global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                        const float* __restrict__ orig, const float* __restrict__ sens,
                                                        const int32_t* __restrict__ wlo, const float* __restrict__ resid,
                                                        const float* __restrict__ gtab, float* __restrict__ gpart,
