@@ -214,6 +214,8 @@ def main():
     ctx = gpair.Context(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), sigma=cfg.sig, v=cfg.v,
                         fs=cfg.fs, n_samples=cfg.n_samples, t0=cfg.t0, k=cfg.k, rank=rank, world=world,
                         nccl_comm=comm, assa=(args.op == "assa"))
+    if vcr_kw:  # agree on the slab layout once, before any timed collective (every rank)
+        ctx.vcr_prepare(vcr_kw["grid"], vcr_kw["z0"])
     info = ctx.info()
     pair_samples_local = ctx.count_pair_samples()
     # measured data b: forward of the vessel phantom (a workload input only)

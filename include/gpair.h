@@ -76,6 +76,11 @@ enum {
                                    + dp e^{-dp^2/2s^2} 1(|dp|<ks)] / (2 r),  dm = r - v t_n,
                                    dp = r + v t_n.  Pairs need only r > 0 (GEOMETRY if some
                                    r = 0).  Exact operator only (not with GPAIR_TOF_ASSA). */
+    GPAIR_COLLECTIVE = 1 << 2,  /* take the kernel-sharded (collective) path even at world = 1:
+                                   the NCCL all-reduce of y, the separate residual kernel, the
+                                   per-group all-reduces of the pipeline and the R_VCR exchange
+                                   run as at world > 1 (with a 1-rank communicator they are
+                                   identities).  Implied by world > 1.  Needs nccl_comm. */
     GPAIR_CHECK_FINITE = 1 << 9 /* gpair_iterate syncs and checks the loss is finite */
 };
 
@@ -96,7 +101,9 @@ typedef struct {
     int32_t n_sensors;     /* N_d >= 1                                                    */
     const float* sensors;  /* DEVICE [3][N_d] SoA point-detector positions [m]   */
     int32_t rank, world;   /* kernel-shard index / count; world >= 1                      */
-    void* nccl_comm;       /* ncclComm_t over `world` ranks (borrowed) or NULL if world=1 */
+    void* nccl_comm;       /* ncclComm_t over `world` ranks (borrowed), or NULL at world = 1
+                              without GPAIR_COLLECTIVE.  Its size and rank must equal
+                              world and rank (INVALID_ARGUMENT otherwise)               */
     int32_t flags;         /* GPAIR_TOF_EXACT or GPAIR_TOF_ASSA, | GPAIR_CHECK_FINITE      */
     int32_t assa_nmin;     /* ASSA N_min ("set to 25"); <= 0 -> 25; ignored unless ASSA */
 } gpair_desc;
@@ -118,7 +125,8 @@ typedef struct {
      * differences use): at world == 1 grid[0] grid[1] grid[2] == M; at
      * world > 1 grid is the GLOBAL grid and each rank's M_local kernels are
      * the z planes [z0, z0 + M_local / (nx ny)) (>= 2 planes), ranks in z
-     * order (rank 0 from z0 = 0, the last rank up to n_z).  The library then
+     * order (rank 0 from z0 = 0, the last rank up to n_z), and every rank must
+     * first call gpair_vcr_prepare(grid, z0) (INVALID_ARGUMENT otherwise).  The library then
      * exchanges 2 halo planes of z with ranks r-1 and r+1 (ncclSend/ncclRecv)
      * and all-reduces the fp64 value of R_VCR (8 bytes); the gradient stays
      * rank-local. */
@@ -177,6 +185,9 @@ typedef struct {
                                    1 = sensor lanes + TAB (k_adjoint_t),
                                    2 = sensor lanes + lane-centred factorisation (k_adjoint_lcf),
                                    3 = sensor lanes + per-sample exponential (k_adjoint_sl) */
+    int32_t collective;         /* 1: kernel-sharded path (NCCL all-reduce of y, separate
+                                   residual kernel): world > 1 or GPAIR_COLLECTIVE          */
+    int32_t reserved;           /* 0                                                    */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial
@@ -229,6 +240,20 @@ gpair_status gpair_vcr(gpair_ctx* ctx, const int32_t* grid, const float* x, floa
 gpair_status gpair_vcr_slab(gpair_ctx* ctx, const int32_t* grid, int32_t z0, int32_t nz_own,
                             const float* x_ext, int32_t ext_z0, int32_t ext_nz, float beta,
                             float eps, float* grad, float* value, void* stream);
+
+/* Validate and set up the slab layout of R_VCR for gpair_iterate with lam > 0
+ * (row f2).  Required on the collective path (world > 1
+ * or GPAIR_COLLECTIVE), optional at world = 1 (it then only pre-allocates, so
+ * the first iterate allocates nothing and stays CUDA-graph capturable).
+ * grid: HOST int32[3] GLOBAL (n_x, n_y, n_z); z0: first global z plane of this
+ * rank's kernels (M_local / (n_x n_y) whole planes, >= 2 at world > 1).
+ * Collective on the collective path: every rank must call it; the ranks
+ * exchange (z0, n_z,own, ok) in one all-reduce and all return the same
+ * verdict, so a bad layout on one rank never leaves the others blocked in
+ * the halo exchange.  Synchronises `stream`.  Allocates the halo buffer and
+ * the R_VCR workspace.  Errors: INVALID_ARGUMENT (slabs not whole planes,
+ * not contiguous in rank order, not covering n_z; bad grid), CUDA, NCCL. */
+gpair_status gpair_vcr_prepare(gpair_ctx* ctx, const int32_t* grid, int32_t z0, void* stream);
 
 /* One iteration of Algorithm 2:
  *   x = (z + eps)^2 (mode 0) or x = z (mode 1);  y = A x  [+ allreduce];

@@ -79,9 +79,11 @@ struct NcclApi {
     nccl_res_t (*Recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     nccl_res_t (*GroupStart)() = nullptr;
     nccl_res_t (*GroupEnd)() = nullptr;
+    nccl_res_t (*CommCount)(void*, int*) = nullptr;
+    nccl_res_t (*CommUserRank)(void*, int*) = nullptr;
 };
 NcclApi g_nccl;
-constexpr int NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
+constexpr int NCCL_INT32 = 2, NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 bool nccl_load() {
     if (g_nccl.tried) return g_nccl.ok;
@@ -98,8 +100,10 @@ bool nccl_load() {
     g_nccl.Recv = (nccl_res_t(*)(void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclRecv");
     g_nccl.GroupStart = (nccl_res_t(*)())dlsym(h, "ncclGroupStart");
     g_nccl.GroupEnd = (nccl_res_t(*)())dlsym(h, "ncclGroupEnd");
+    g_nccl.CommCount = (nccl_res_t(*)(void*, int*))dlsym(h, "ncclCommCount");
+    g_nccl.CommUserRank = (nccl_res_t(*)(void*, int*))dlsym(h, "ncclCommUserRank");
     g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy && g_nccl.Send &&
-                g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd;
+                g_nccl.Recv && g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.CommCount && g_nccl.CommUserRank;
     return g_nccl.ok;
 }
 
@@ -255,7 +259,7 @@ gpair_status sticky_check(gpair_ctx* c) {
 }
 
 gpair_status allreduce(gpair_ctx* c, float* y, cudaStream_t st) {
-    if (c->world <= 1) return GPAIR_OK;
+    if (!c->coll) return GPAIR_OK;
     ProfScope ps(c, GPAIR_PROF_ALLREDUCE, st);
     nccl_res_t r = g_nccl.AllReduce(y, y, (size_t)c->Nd * c->Nt, NCCL_FLOAT32, NCCL_SUM, c->nccl, st);
     if (r != 0)
@@ -276,22 +280,24 @@ gpair_status nccl_check(gpair_ctx* c, nccl_res_t r, const char* what) {
 // boundary go to and come from ranks r - 1 and r + 1), then the slab kernels
 // give the own planes' gradient and the slab's value, which one 8-byte
 // all-reduce sums into the global R_VCR (d_vcr_part[vcr_nb]).
-gpair_status vcr_sharded(gpair_ctx* c, const gpair_step* s, const float* z, int npc, cudaStream_t st) {
-    constexpr int HALO = 2;  // the stencils' reach (gpair_vcr.cu)
-    const int64_t P = (int64_t)s->grid[0] * s->grid[1];
-    const int nzo = (int)(c->M / P), z0 = s->z0;
+constexpr int VCR_HALO = 2;  // the stencils' reach (gpair_vcr.cu)
+
+// The halo buffer [lower halo | own planes | upper halo] of this rank's slab.
+int64_t vcr_halo_elems(const gpair_ctx* c, const int32_t* grid) {
+    const int64_t P = (int64_t)grid[0] * grid[1];
+    const int lo = c->rank > 0 ? VCR_HALO : 0, hi = c->rank < c->world - 1 ? VCR_HALO : 0;
+    return P * (lo + c->M / P + hi);
+}
+
+// Buffers and layout come from gpair_vcr_prepare (validated on every rank, allocated
+// before the first iteration: no allocation or early return between collectives).
+gpair_status vcr_sharded(gpair_ctx* c, const float* z, int npc, const gpair_step* s, cudaStream_t st) {
+    constexpr int HALO = VCR_HALO;
+    const int32_t* grid = c->vcr_grid;
+    const int64_t P = (int64_t)grid[0] * grid[1];
+    const int nzo = (int)(c->M / P), z0 = c->vcr_z0;
     const int lo = c->rank > 0 ? HALO : 0, hi = c->rank < c->world - 1 ? HALO : 0;
-    const int64_t n = P * (lo + nzo + hi);
-    if (c->vcr_x_n != n) {
-        cudaFree(c->d_vcr_x);
-        c->d_vcr_x = nullptr;
-        c->vcr_x_n = 0;
-        API_CUDA(c, cudaMalloc(&c->d_vcr_x, sizeof(float) * (size_t)n), "vcr halo buffer");
-        c->vcr_x_n = n;
-        c->workspace_bytes += (int64_t)sizeof(float) * n;
-    }
     float* xb = c->d_vcr_x;
-    API_CUDA(c, gpair::vcr_slab_ensure(c, s->grid, z0, nzo), "vcr workspace");  // d_vcr_g exists
     API_CUDA(c, cudaMemcpyAsync(xb + P * lo, z, sizeof(float) * (size_t)c->M, cudaMemcpyDeviceToDevice, st),
              "vcr own planes");
     gpair_status gs = nccl_check(c, g_nccl.GroupStart(), "ncclGroupStart");
@@ -310,7 +316,7 @@ gpair_status vcr_sharded(gpair_ctx* c, const gpair_step* s, const float* z, int 
     gpair_status ge = nccl_check(c, g_nccl.GroupEnd(), "ncclGroupEnd");
     if (gs) return gs;
     if (ge) return ge;
-    API_CUDA(c, gpair::launch_vcr_slab(c, s->grid, z0, nzo, xb, z0 - lo, npc, s->eps_npc, s->beta, s->eps_reg,
+    API_CUDA(c, gpair::launch_vcr_slab(c, grid, z0, nzo, xb, z0 - lo, npc, s->eps_npc, s->beta, s->eps_reg,
                                        c->d_vcr_g, nullptr, st),
              "vcr (slab)");
     API_CUDA(c, gpair::launch_vcr_total(c, st), "vcr total");
@@ -393,11 +399,20 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     }
     if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
         return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "rank/world invalid");
-    if (d->world > 1 && !d->nccl_comm) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "world > 1 needs nccl_comm");
+    const bool coll = d->world > 1 || (d->flags & GPAIR_COLLECTIVE);
+    if (coll && !d->nccl_comm)
+        return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "world > 1 (or GPAIR_COLLECTIVE) needs nccl_comm");
     if ((int64_t)d->n_sensors * d->n_samples >= (1LL << 31))
         return fail(nullptr, GPAIR_ERR_RESOURCE, "N_d * N_t must be < 2^31");
     if (d->n_kernels >= (1LL << 31) - 64) return fail(nullptr, GPAIR_ERR_RESOURCE, "n_kernels must be < 2^31 - 64");
-    if (d->world > 1 && !nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    if (coll) {
+        if (!nccl_load()) return fail(nullptr, GPAIR_ERR_NCCL, "cannot dlopen libnccl.so.2");
+        int cn = 0, cr = -1;
+        if (g_nccl.CommCount(d->nccl_comm, &cn) != 0 || g_nccl.CommUserRank(d->nccl_comm, &cr) != 0)
+            return fail(nullptr, GPAIR_ERR_NCCL, "ncclCommCount / ncclCommUserRank failed on nccl_comm");
+        if (cn != d->world || cr != d->rank)
+            return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "nccl_comm size / rank differ from world / rank");
+    }
 
     // operator constants (fp64 on the host)
     const double v = d->sound_speed, fs = d->sampling_rate, s = d->sigma, kk = d->window_k;
@@ -482,6 +497,7 @@ gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
     c->Nt = d->n_samples;
     c->rank = d->rank;
     c->world = d->world;
+    c->coll = (d->world > 1 || (d->flags & GPAIR_COLLECTIVE)) ? 1 : 0;
     c->nccl = d->nccl_comm;
     c->flags = d->flags;
     c->assa = assa ? 1 : 0;
@@ -563,6 +579,8 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->near_pairs = c->n_near;
     o->tab = ((c->ser == 0 || c->ser == gpair::SER_FAST5) && c->tab.on) ? 1 : 0;
     o->adj_kernel = c->assa ? 0 : gpair::adjoint_kernel(c);
+    o->collective = c->coll;
+    o->reserved = 0;
     return GPAIR_OK;
 }
 
@@ -577,7 +595,7 @@ static gpair_status do_forward_core(gpair_ctx* c, const float* src, int npc, flo
         API_CUDA(c, c->assa ? gpair::launch_assa_forward(c, st) : gpair::launch_forward(c, st), "forward");
         if (c->n_near) API_CUDA(c, gpair::launch_near_forward(c, st), "near-field forward");
     }
-    if (c->world == 1) {
+    if (!c->coll) {
         ProfScope ps(c, GPAIR_PROF_REDUCE, st);
         API_CUDA(c, gpair::launch_reduce(c, y, b, b ? c->d_delta : nullptr, st), "reduce");
     } else {
@@ -670,6 +688,62 @@ gpair_status gpair_vcr_slab(gpair_ctx* c, const int32_t* grid, int32_t z0, int32
     return GPAIR_OK;
 }
 
+gpair_status gpair_vcr_prepare(gpair_ctx* c, const int32_t* grid, int32_t z0, void* stream) {
+    if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
+    gpair_status gs = check_vcr_args(c, grid, 0.f, 1.f);
+    if (gs) return gs;
+    gs = sticky_check(c);
+    if (gs) return gs;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t P = (int64_t)grid[0] * grid[1];
+    const int64_t nzo = c->M % P ? 0 : c->M / P;
+    std::string why;
+    if (!nzo) why = "n_kernels is not whole z planes of grid";
+    else if (!c->coll && (nzo != grid[2] || z0 != 0)) why = "world 1: grid must be the kernels' own grid, z0 = 0";
+    else if (c->world > 1 && nzo < 2) why = "world > 1 needs >= 2 z planes per rank";
+    else if (z0 < 0 || z0 + nzo > grid[2]) why = "slab [z0, z0 + M / (nx ny)) outside the grid";
+    if (c->coll) {
+        // every rank contributes (z0, nz, error) in its own slot; one summing all-reduce
+        // gives every rank the whole table, so every rank takes the same decision
+        const int W = c->world;
+        std::vector<int32_t> h((size_t)3 * W, 0);
+        h[3 * c->rank] = z0;
+        h[3 * c->rank + 1] = (int32_t)nzo;
+        h[3 * c->rank + 2] = why.empty() ? 0 : 1;
+        int32_t* d = nullptr;
+        API_CUDA(c, cudaMalloc(&d, sizeof(int32_t) * h.size()), "vcr prepare table");
+        cudaError_t e = cudaMemcpyAsync(d, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, st);
+        nccl_res_t r = e == cudaSuccess ? g_nccl.AllReduce(d, d, h.size(), NCCL_INT32, NCCL_SUM, c->nccl, st) : 0;
+        if (e == cudaSuccess && r == 0) e = cudaMemcpyAsync(h.data(), d, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && r == 0) e = cudaStreamSynchronize(st);
+        cudaFree(d);
+        if (e != cudaSuccess) return cuda_fail(c, e, "vcr prepare exchange");
+        if (r != 0) return nccl_check(c, r, "ncclAllReduce (vcr prepare)");
+        int32_t expect = 0;
+        for (int q = 0; q < W && why.empty(); ++q) {
+            if (h[3 * q + 2]) why = "rank " + std::to_string(q) + " rejected its slab";
+            else if (h[3 * q] != expect) why = "slabs are not contiguous whole z planes in rank order";
+            expect = h[3 * q] + h[3 * q + 1];
+        }
+        if (why.empty() && expect != grid[2]) why = "slabs do not cover the grid's n_z planes";
+    }
+    if (!why.empty()) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "gpair_vcr_prepare: " + why);
+    const int64_t n = c->coll ? vcr_halo_elems(c, grid) : 0;
+    if (c->coll && c->vcr_x_n != n) {
+        cudaFree(c->d_vcr_x);
+        c->d_vcr_x = nullptr;
+        c->vcr_x_n = 0;
+        API_CUDA(c, cudaMalloc(&c->d_vcr_x, sizeof(float) * (size_t)n), "vcr halo buffer");
+        c->vcr_x_n = n;
+        c->workspace_bytes += (int64_t)sizeof(float) * n;
+    }
+    API_CUDA(c, gpair::vcr_slab_ensure(c, grid, z0, (int)nzo), "vcr workspace");
+    for (int d = 0; d < 3; ++d) c->vcr_grid[d] = grid[d];
+    c->vcr_z0 = z0;
+    c->vcr_prepared = 1;
+    return GPAIR_OK;
+}
+
 gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const float* b, const gpair_step* s,
                            float* signals_out, float* x_out, float* loss_out, void* stream) {
     if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
@@ -686,15 +760,14 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
         gpair_status gs = check_vcr_args(c, s->grid, s->beta, s->eps_reg);
         if (gs) return gs;
         const int64_t P = (int64_t)s->grid[0] * s->grid[1];
-        if (c->world == 1) {
+        if (!c->coll) {
             if (P * s->grid[2] != c->M) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "grid[0] grid[1] grid[2] != n_kernels");
-        } else {  // z slab of the global grid (ranks in z order)
-            if (c->M % P) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "n_kernels is not whole z planes of grid");
-            const int64_t nzo = c->M / P;
-            if (nzo < 2) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "lam > 0 at world > 1 needs >= 2 z planes per rank");
-            if (s->z0 < 0 || s->z0 + nzo > s->grid[2] || (c->rank == 0 && s->z0 != 0) ||
-                (c->rank == c->world - 1 && s->z0 + nzo != s->grid[2]))
-                return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "z0 / slab does not fit the global grid in rank order");
+        } else if (!c->vcr_prepared || s->z0 != c->vcr_z0 || s->grid[0] != c->vcr_grid[0] ||
+                   s->grid[1] != c->vcr_grid[1] || s->grid[2] != c->vcr_grid[2]) {
+            // the slab layout was agreed by every rank in gpair_vcr_prepare, so this is
+            // the same decision on every rank that prepared the same layout
+            return fail(c, GPAIR_ERR_INVALID_ARGUMENT,
+                        "lam > 0 on the collective path needs gpair_vcr_prepare(grid, z0) with the same grid / z0");
         }
     }
     cudaStream_t st = (cudaStream_t)stream;
@@ -702,18 +775,18 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     float* y = signals_out ? signals_out : c->d_y;
     if (reg) {  // R_VCR and its gradient at the pre-update x (Alg. 2)
         ProfScope ps(c, GPAIR_PROF_VCR, st);
-        if (c->world == 1) {
+        if (!c->coll) {
             API_CUDA(c, gpair::vcr_slab_ensure(c, s->grid, 0, s->grid[2]), "vcr workspace");  // d_vcr_g exists
             API_CUDA(c, gpair::launch_vcr(c, s->grid, z, npc, s->eps_npc, s->beta, s->eps_reg, c->d_vcr_g, nullptr, st),
                      "vcr");
         } else {
-            gpair_status gs = vcr_sharded(c, s, z, npc, st);
+            gpair_status gs = vcr_sharded(c, z, npc, s, st);
             if (gs) return gs;
         }
     }
     // fp64 R_VCR for the loss: the per-block partials (world 1) or the all-reduced total
-    const double* reg_part = reg ? (c->world == 1 ? c->d_vcr_part : c->d_vcr_part + c->vcr_nb) : nullptr;
-    const int32_t reg_n = reg ? (c->world == 1 ? c->vcr_nb : 1) : 0;
+    const double* reg_part = reg ? (!c->coll ? c->d_vcr_part : c->d_vcr_part + c->vcr_nb) : nullptr;
+    const int32_t reg_n = reg ? (!c->coll ? c->vcr_nb : 1) : 0;
     EpiParams ep{};
     const double N = (double)c->Nd * (double)c->Nt;
     ep.scale = s->grad_scale > 0.f ? s->grad_scale : (float)(2.0 / N);
@@ -736,7 +809,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
     if (c->st2 && pipeline_eligible(c)) {
         WindowReset wr{c};
         cudaStream_t s2 = c->st2;
-        float* yy = (c->world == 1 && !signals_out) ? nullptr : y;
+        float* yy = (!c->coll && !signals_out) ? nullptr : y;
         {
             ProfScope ps(c, GPAIR_PROF_GATHER, st);
             API_CUDA(c, gpair::launch_gather(c, z, npc, s->eps_npc, st), "gather");
@@ -753,7 +826,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
             API_CUDA(c, cudaStreamWaitEvent(s2, c->ev_f[g], 0), "event wait");
             c->lj0 = g * 256;
             c->lnj = std::min(256, c->Nd - g * 256);
-            if (c->world == 1) {
+            if (!c->coll) {
                 ProfScope ps(c, GPAIR_PROF_REDUCE, s2);
                 API_CUDA(c, gpair::launch_reduce(c, yy, b, c->d_delta, s2), "reduce (group)");
             } else {
@@ -807,7 +880,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
         }
         return GPAIR_OK;
     }
-    gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (c->world == 1 && !signals_out) ? nullptr : y, b, st);
+    gpair_status r = do_forward_core(c, z, npc, s->eps_npc, (!c->coll && !signals_out) ? nullptr : y, b, st);
     if (r) return r;
     if (loss_out || (c->flags & GPAIR_CHECK_FINITE)) {
         ProfScope ps(c, GPAIR_PROF_LOSS, st);

@@ -21,6 +21,7 @@ struct gpair_ctx_s {
     int64_t M = 0, Mpad = 0;
     int32_t ncells = 0, Nd = 0, Nt = 0;
     int32_t rank = 0, world = 1;
+    int coll = 0;           // collective path (world > 1, or GPAIR_COLLECTIVE at world 1)
     void* nccl = nullptr;
     int32_t flags = 0;
     int grid_detected = 0;
@@ -50,7 +51,7 @@ struct gpair_ctx_s {
     // adjoint decomposition
     int32_t a_cpr = 0, a_regions = 0, La = 0;
     int32_t* d_wlo_a = nullptr;   // [a_regions][Nd]
-    float* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
+    gpair::gacc_t* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
     float* d_gtab = nullptr;      // [2][La] G(t - La/2) = 2^{K tau^2} and its inverse (k_adjoint_lcf), or NULL
 
     // per-call workspaces
@@ -83,6 +84,8 @@ struct gpair_ctx_s {
     float* d_vcr_g = nullptr;     // [vcr_Mo] dR/dx (caller order)
     float* d_vcr_x = nullptr;     // world > 1: own z planes + halos (NCCL send/recv)
     int64_t vcr_x_n = 0;
+    int vcr_prepared = 0;         // gpair_vcr_prepare: slab layout validated on every rank
+    int32_t vcr_grid[3] = {0, 0, 0}, vcr_z0 = 0;
 
     int64_t workspace_bytes = 0;
     std::string err;
@@ -161,7 +164,7 @@ __device__ __forceinline__ void adjoint_epilogue(float acc, int32_t ic, const Ep
 cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st);
-cudaError_t launch_group_gather(gpair_ctx* c, const float* gpart, int ngroups, int mode, const EpiParams& ep,
+cudaError_t launch_group_gather(gpair_ctx* c, const gacc_t* gpart, int ngroups, int mode, const EpiParams& ep,
                                 cudaStream_t st);
 int adjoint_groups(const gpair_ctx* c);
 int pick_wmax(int w);

@@ -36,6 +36,17 @@ constexpr double MAX_DR_SAMPLES = 4.0; // max group radius [samples] of the seri
 constexpr double EPS_SMALL = 0.006;    // max |eps| for the degree-2 series (SER = 2)
 constexpr float RND_MAGIC = 12582912.f;      // 1.5 * 2^23
 constexpr int RND_MAGIC_BITS = 0x4B400000;   // __float_as_int(RND_MAGIC)
+#ifndef GPAIR_ADJ_ACC64
+#define GPAIR_ADJ_ACC64 1
+#endif
+// Accumulator of the sensor-lane adjoints' cross-sensor sums (warp reduce-scatter,
+// per-warp smem sums, sensor-group partials, k_adj_gather): fp64 keeps these
+// sums' rounding out of the gradient's error budget.
+#if GPAIR_ADJ_ACC64
+typedef double gacc_t;
+#else
+typedef float gacc_t;
+#endif
 
 // Operator constants, computed once on the host in fp64 and passed by value.
 struct OpConst {
@@ -633,21 +644,21 @@ constexpr int STAGE_CELLS = 8;  // cells per staged kernel tile
 // Reduce-scatter of 8 per-lane values (one group of 8 kernels) over the warp's 32
 // sensors: xor 16 / 8 / 4 halve the value set, xor 2 / 1 finish the sums; lane 4k
 // ends with kernel k's sum and writes it to dst[k] (fixed order: deterministic).
-__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, float* dst) {
+__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, gacc_t* dst) {
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-    float h4[4];
+    gacc_t h4[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
+        const gacc_t keep = b4 ? gv[4 + i] : gv[i], send = b4 ? gv[i] : gv[4 + i];
         h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    float h2[2];
+    gacc_t h2[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        const float keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
+        const gacc_t keep = b3 ? h4[2 + i] : h4[i], send = b3 ? h4[i] : h4[2 + i];
         h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
     }
-    float h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
+    gacc_t h1 = (b2 ? h2[1] : h2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? h2[0] : h2[1], 4);
     h1 += __shfl_xor_sync(0xffffffffu, h1, 2);
     h1 += __shfl_xor_sync(0xffffffffu, h1, 1);
     if ((lane & 3) == 0) dst[lane >> 2] = h1;  // lane bits (4, 3, 2) = kernel index
@@ -669,9 +680,9 @@ __device__ __forceinline__ void stage_kernel_tile(const float4* __restrict__ kd,
 }
 
 // Sum of the CTA's per-warp kernel sums in warp order -> this sensor group's partial gradient.
-__device__ __forceinline__ void write_group_partials(const float* s_g, int nw, int nc, float* __restrict__ dst) {
+__device__ __forceinline__ void write_group_partials(const gacc_t* s_g, int nw, int nc, gacc_t* __restrict__ dst) {
     for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-        float sum = 0.f;
+        gacc_t sum = 0;
         for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
         dst[t] = sum;
     }

@@ -658,7 +658,7 @@ template <int W, int SDEG>
 __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                      const float* __restrict__ orig, const float* __restrict__ sens,
                                                      const int32_t* __restrict__ wlo, const float* __restrict__ resid,
-                                                     float* __restrict__ gpart, int32_t cpr, int32_t ncells,
+                                                     gacc_t* __restrict__ gpart, int32_t cpr, int32_t ncells,
                                                      int32_t La, int64_t Mpad, OpConst k, const TabConst tab) {
     constexpr int C = W / 2;
     extern __shared__ float4 smem4[];
@@ -667,9 +667,9 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    gacc_t* s_g = (gacc_t*)(s_grp + STAGE_CELLS * GPC);  // [nw][STAGE_CELLS*CELL] per-warp kernel sums
     // this warp's residual column [La][32] (ADJT_DBL: [La][32] float2 (delta_t, delta_{t+1}))
-    float* s_col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 * (1 + ADJT_DBL);
+    float* s_col = (float*)(s_g + nw * STAGE_CELLS * CELL) + (size_t)warp * La * 32 * (1 + ADJT_DBL);
     float* col = s_col + lane;
     f2_t* col2 = (f2_t*)s_col + lane;
 
@@ -860,6 +860,9 @@ __device__ __forceinline__ f2_t exp2_acc2(f2_t x) {
     return pk2(p0, p1);
 }
 
+#ifndef GPAIR_ADJ_EPOLY
+#define GPAIR_ADJ_EPOLY 0
+#endif
 #ifndef GPAIR_LCF_MINB
 #define GPAIR_LCF_MINB 3
 #endif
@@ -867,7 +870,7 @@ template <int W, int SDEG>
 __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                        const float* __restrict__ orig, const float* __restrict__ sens,
                                                        const int32_t* __restrict__ wlo, const float* __restrict__ resid,
-                                                       const float* __restrict__ gtab, float* __restrict__ gpart,
+                                                       const float* __restrict__ gtab, gacc_t* __restrict__ gpart,
                                                        int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
                                                        float K, float m2K) {
     extern __shared__ float4 smem4[];
@@ -876,8 +879,8 @@ __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
-    float* s_gt = s_g + nw * STAGE_CELLS * CELL;          // [2][La]: G(t - T), 1 / G(t - T)
+    gacc_t* s_g = (gacc_t*)(s_grp + STAGE_CELLS * GPC);  // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    float* s_gt = (float*)(s_g + nw * STAGE_CELLS * CELL);          // [2][La]: G(t - T), 1 / G(t - T)
     float* col = s_gt + 2 * La + (size_t)warp * La * 32 + lane;  // this lane's column dtil_t at col[t * 32]
     for (int t = threadIdx.x; t < 2 * La; t += blockDim.x) s_gt[t] = gtab[t];
     const float* s_ginv = s_gt + La;
@@ -976,10 +979,18 @@ __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float
                         q1 = q1 * fmaf(-r1, q1, 2.f);
                         S2[h] = pk2(q0, q1);
                         UC[h] = add2(ulo[h], pk2(-(float)C, -(float)C));  // u_c, exact
+#if GPAIR_ADJ_EPOLY
+                        // 2^{K u_c^2} by the unbiased polynomial: a per-pair scale error enters g directly
+                        float e0, e1;
+                        upk2(exp2_acc2(mul2(mul2(UC[h], K2), UC[h])), e0, e1);
+                        upk2(mul2(w[h], pk2(e0 * s_ginv[o[2 * h] + C], e1 * s_ginv[o[2 * h + 1] + C])),
+                             sc[2 * h], sc[2 * h + 1]);
+#else
                         float e0, e1;
                         upk2(mul2(mul2(UC[h], K2), UC[h]), e0, e1);
                         upk2(mul2(w[h], pk2(ex2f(e0) * s_ginv[o[2 * h] + C], ex2f(e1) * s_ginv[o[2 * h + 1] + C])),
                              sc[2 * h], sc[2 * h + 1]);
+#endif
                         rp[2 * h] = col + (o[2 * h] + C) * 32;
                         rp[2 * h + 1] = col + (o[2 * h + 1] + C) * 32;
                         U[h] = pk2(rp[2 * h][(W - C - 1) * 32], rp[2 * h + 1][(W - C - 1) * 32]);
@@ -1058,7 +1069,7 @@ template <int W, int SDEG>
 __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict__ kd, const float4* __restrict__ grp,
                                                        const float* __restrict__ orig, const float* __restrict__ sens,
                                                        const int32_t* __restrict__ wlo, const float* __restrict__ resid,
-                                                       float* __restrict__ gpart,
+                                                       gacc_t* __restrict__ gpart,
                                                        int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
                                                        float K) {
     const float m2K = -2.f * K;
@@ -1068,8 +1079,8 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* s_g = (float*)(s_grp + STAGE_CELLS * GPC);   // [nw][STAGE_CELLS*CELL] per-warp kernel sums
-    float* col = s_g + nw * STAGE_CELLS * CELL + (size_t)warp * La * 32 + lane;  // this lane's column delta_t
+    gacc_t* s_g = (gacc_t*)(s_grp + STAGE_CELLS * GPC);  // [nw][STAGE_CELLS*CELL] per-warp kernel sums
+    float* col = (float*)(s_g + nw * STAGE_CELLS * CELL) + (size_t)warp * La * 32 + lane;  // this lane's column delta_t
     const int region = blockIdx.x;
     const int c0 = region * cpr, c1 = min(c0 + cpr, ncells);
     if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(STAGE_CELLS, c1 - c0), s_kxy, s_kzw, s_grp);
@@ -1197,15 +1208,15 @@ __global__ void __launch_bounds__(256, 3) k_adjoint_sl(const float4* __restrict_
 
 // sum of the sensor-group partial gradients (fixed order) + epilogue
 template <int MODE>
-__global__ void k_adj_gather(const float* __restrict__ gpart, int32_t ngroups, const int32_t* __restrict__ perm,
+__global__ void k_adj_gather(const gacc_t* __restrict__ gpart, int32_t ngroups, const int32_t* __restrict__ perm,
                              int64_t Mpad, EpiParams ep) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= Mpad) return;
     const int32_t ic = perm[i];
     if (ic < 0) return;
-    float acc = 0.f;
+    gacc_t acc = 0;
     for (int g = 0; g < ngroups; ++g) acc += gpart[(int64_t)g * Mpad + i];
-    adjoint_epilogue<MODE>(acc, ic, ep);
+    adjoint_epilogue<MODE>((float)acc, ic, ep);
 }
 
 }  // namespace
@@ -1253,7 +1264,7 @@ cudaError_t adj_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cu
 constexpr int ADJT_WARPS = 8;  // sensor warps per CTA of k_adjoint_t
 
 size_t adj_t_smem(const gpair_ctx* c) {
-    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * sizeof(gacc_t) +
            (size_t)ADJT_WARPS * c->La * 32 * 4 * (1 + ADJT_DBL);
 }
 
@@ -1279,7 +1290,7 @@ cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
 }
 
 size_t adj_lcf_smem(const gpair_ctx* c) {
-    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * sizeof(gacc_t) +
            (size_t)2 * c->La * 4 + (size_t)ADJT_WARPS * c->La * 32 * 4;
 }
 
@@ -1306,7 +1317,7 @@ cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep
 }
 
 size_t adj_sl_smem(const gpair_ctx* c) {
-    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * 4 +
+    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * sizeof(gacc_t) +
            (size_t)ADJT_WARPS * c->La * 32 * 4;
 }
 
@@ -1498,7 +1509,7 @@ cudaError_t launch_adjoint(gpair_ctx* c, const float* resid, int mode, const Epi
     return adj_dispatch<EPI_CLAMP>(c, resid, ep, st);
 }
 
-cudaError_t launch_group_gather(gpair_ctx* c, const float* gpart, int ngroups, int mode, const EpiParams& ep,
+cudaError_t launch_group_gather(gpair_ctx* c, const gacc_t* gpart, int ngroups, int mode, const EpiParams& ep,
                                 cudaStream_t st) {
     const unsigned nb = (unsigned)((c->Mpad + 255) / 256);
     ++c->n_launch;

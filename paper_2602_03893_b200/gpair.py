@@ -11,12 +11,13 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpair.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("GPAIR_LIB", "libgpair.so"))
 
 OK, ERR_INVALID_ARGUMENT, ERR_GEOMETRY, ERR_RESOURCE, ERR_NUMERICAL, ERR_CUDA, ERR_NCCL = range(7)
 CHECK_FINITE = 1 << 9
 TOF_ASSA = 1
 NEAR_FIELD = 1 << 1
+COLLECTIVE = 1 << 2
 PROF_NAMES = ["gather", "forward", "reduce", "allreduce", "residual", "adjoint", "loss", "vcr"]
 
 
@@ -95,6 +96,8 @@ class Info(ctypes.Structure):
         ("near_pairs", ctypes.c_int64),
         ("tab", ctypes.c_int32),
         ("adj_kernel", ctypes.c_int32),
+        ("collective", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self):
@@ -122,6 +125,7 @@ def lib():
             "gpair_vcr": (st, [vp, ctypes.POINTER(i32), vp, ctypes.c_float, ctypes.c_float, vp, vp, vp]),
             "gpair_vcr_slab": (st, [vp, ctypes.POINTER(i32), i32, i32, vp, i32, i32, ctypes.c_float, ctypes.c_float,
                                     vp, vp, vp]),
+            "gpair_vcr_prepare": (st, [vp, ctypes.POINTER(i32), i32, vp]),
             "gpair_get_info": (st, [vp, ctypes.POINTER(Info)]),
             "gpair_destroy": (st, [vp]),
             "gpair_profile_enable": (st, [vp, ctypes.c_int]),
@@ -289,6 +293,12 @@ class Context:
         _check(lib().gpair_vcr_slab(self._h, g3, int(z0), int(nz_own), _ptr(x_ext, name="x_ext"), int(ext_z0), ext_nz,
                                     float(beta), float(eps), _ptr(grad, numel=P * int(nz_own), name="grad"),
                                     _ptr(value, numel=1, name="value"), _stream(stream)), self._h)
+
+    def vcr_prepare(self, grid, z0=0, stream=None):
+        """gpair_vcr_prepare: agree on / allocate the R_VCR slab layout (collective
+        on the collective path: every rank calls it)."""
+        g3 = (ctypes.c_int32 * 3)(*(int(d) for d in grid))
+        _check(lib().gpair_vcr_prepare(self._h, g3, int(z0), _stream(stream)), self._h)
 
     def count_pair_samples(self, stream=None):
         out = ctypes.c_int64()

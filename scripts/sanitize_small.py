@@ -34,14 +34,20 @@ def run(c, s, op, **kw):
 c = inputs.grid_centers(8, 8, 8, 1e-4)
 s = inputs.hemisphere(40, 60e-3)
 op = dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=2048, t0=0.0, k=3.0)
-for env in ({}, {"GPAIR_ADJ_NO_LCF": "1"}, {"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, {"GPAIR_NO_TAB": "1"}):
-    for key in ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T"):
+KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE")
+for env in ({}, {"GPAIR_ADJ_NO_LCF": "1"}, {"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, {"GPAIR_NO_TAB": "1"},
+            {"GPAIR_PIPELINE": "1"}, {"GPAIR_PIPELINE": "1", "GPAIR_NO_TAB": "1"}):
+    for key in KEYS:
         os.environ.pop(key, None)
     os.environ.update(env)
     info = run(c, s, op)
     print("path", env, "tab", info["tab"], "adj", info["adj_kernel"], flush=True)
-for key in ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T"):
+for key in KEYS:
     os.environ.pop(key, None)
+# the double-buffered cp.async forward and the LCF adjoint at other window lengths (W = 12, 24, 32)
+for W in (12, 24, 32):
+    sw = W * (1500.0 / 40e6) / 6.0
+    print("W", W, run(inputs.grid_centers(6, 6, 6, sw), s, dict(op, sigma=sw))["adj_kernel"], flush=True)
 cfg1 = inputs.CONFIGS["cfg1"]
 print("cfg1", run(cfg1.centers(), cfg1.sensors(), cfg1.op_kwargs())["adj_kernel"], flush=True)
 print("assa", run(c, s, op, assa=True)["assa"], flush=True)

@@ -15,12 +15,9 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 from oracle import ir  # noqa: E402
 from paper_2602_03893_b200 import gpair, inputs  # noqa: E402
+from tests_common import T, assert_parity, compare, dev, sample_cols, sample_rows  # noqa: E402
 
 pytestmark = pytest.mark.gpu
-
-REL_L2 = 1e-5
-REL_ELEM = 1e-4
-
 
 @pytest.fixture(scope="module", autouse=True)
 def _built():
@@ -29,36 +26,6 @@ def _built():
     from paper_2602_03893_b200 import build
 
     build.build()
-
-
-def dev():
-    return torch.device("cuda:0")
-
-
-def T(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
-
-
-def compare(got, ref):
-    got = np.asarray(got, dtype=np.float64)
-    ref = np.asarray(ref, dtype=np.float64)
-    nref = np.linalg.norm(ref)
-    rel = np.linalg.norm(got - ref) / nref if nref > 0 else np.linalg.norm(got)
-    big = np.abs(ref) >= 1e-3 * np.abs(ref).max() if nref > 0 else np.zeros(ref.shape, bool)
-    elem = float(np.max(np.abs(got[big] - ref[big]) / np.abs(ref[big]))) if big.any() else 0.0
-    return rel, elem
-
-
-def assert_parity(got, ref, what, elementwise=True):
-    """rel L2 gate on everything; the elementwise gate applies to signal
-    samples (north_star: "1e-4 max elementwise relative error on samples
-    above 1e-3 of peak"; reading R19).  For per-kernel vectors it
-    is reported with a 10x looser sanity bound."""
-    rel, elem = compare(got, ref)
-    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e}"
-    bound = REL_ELEM if elementwise else 10 * REL_ELEM
-    assert elem <= bound, f"{what}: max elementwise rel {elem:.3e}"
-    return rel, elem
 
 
 def make_ctx(c, s, op):
@@ -80,7 +47,7 @@ def test_cfg1_forward_adjoint_full():
     assert_parity(y, oracle.forward(c, x, s, **op), "cfg1 forward")
     d = inputs.residual(cfg.n_sensors, cfg.n_samples)
     g = ctx.adjoint(T(d)).cpu().numpy()
-    assert_parity(g, oracle.adjoint(c, d, s, **adj_kw(op)), "cfg1 adjoint", elementwise=False)
+    assert_parity(g, oracle.adjoint(c, d, s, **adj_kw(op)), "cfg1 adjoint")
     assert ctx.count_pair_samples() == oracle.count_pair_samples(c, s, **op)
 
 
@@ -108,7 +75,7 @@ def test_random_suite(seed):
     d = rng.standard_normal((s.shape[1], op["n_samples"])).astype(np.float32)
     g_ref = oracle.adjoint(c, d, s, **adj_kw(op))
     if np.linalg.norm(g_ref) > 0:
-        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_ref, f"seed {seed} adjoint", elementwise=False)
+        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_ref, f"seed {seed} adjoint")
     assert ctx.count_pair_samples() == oracle.count_pair_samples(c, s, **op)
 
 
@@ -123,7 +90,7 @@ def test_ragged_kernel_counts(M):
     x = rng.random(M).astype(np.float32)
     assert_parity(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), "ragged forward")
     d = rng.standard_normal((37, 400)).astype(np.float32)
-    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "ragged adjoint", elementwise=False)
+    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "ragged adjoint")
 
 
 def test_windows_clipped_by_record_and_empty_sensors():
@@ -139,7 +106,7 @@ def test_windows_clipped_by_record_and_empty_sensors():
     assert np.all(y[40:] == 0)
     assert_parity(y, y_ref, "clipped forward")
     d = inputs.residual(s.shape[1], op["n_samples"])
-    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "clipped adjoint", elementwise=False)
+    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "clipped adjoint")
 
 
 def test_geometry_error():
@@ -182,7 +149,7 @@ def test_shard_sum_invariance():
     for sl in (slice(0, half), slice(half, None)):
         ctx = make_ctx(np.ascontiguousarray(c[:, sl]), s, op)
         y_sum += ctx.forward(T(x[sl])).cpu().numpy()
-        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_full[sl], "shard adjoint", elementwise=False)
+        assert_parity(ctx.adjoint(T(d)).cpu().numpy(), g_full[sl], "shard adjoint")
     assert_parity(y_sum, y_full, "shard forward sum")
 
 
@@ -218,13 +185,13 @@ def test_iterate_one_step_teacher_forced(mode):
     if mode == 0:
         z_ref, m_ref, v_ref = ir.adam_update(z0.astype(np.float64), m0.astype(np.float64),
                                              v0.astype(np.float64), gz_ref, lr, t_step, hp)
-        assert_parity(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, "Adam m increment (= 0.1 dL/dz)", elementwise=False)
-        assert_parity(vt.cpu().numpy(), v_ref, "Adam v", elementwise=False)
-        assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "Adam z step", elementwise=False)
-        assert_parity(x_out.cpu().numpy(), ir.npc(z_ref), "x_out", elementwise=False)
+        assert_parity(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, "Adam m increment (= 0.1 dL/dz)")
+        assert_parity(vt.cpu().numpy(), v_ref, "Adam v")
+        assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "Adam z step")
+        assert_parity(x_out.cpu().numpy(), ir.npc(z_ref), "x_out")
     else:
         x_ref = np.maximum(z0 - lr * gz_ref, 0.0)
-        assert_parity(zt.cpu().numpy(), x_ref, "clamp step", elementwise=False)
+        assert_parity(zt.cpu().numpy(), x_ref, "clamp step")
 
 
 def test_iterate_trajectory_cfg1_reports_loss_decrease():
@@ -263,11 +230,11 @@ def test_full_size_sampled_rows(name):
     ctx = make_ctx(c, s, op)
     x = inputs.dense_amplitudes(cfg.M)
     y = ctx.forward(T(x)).cpu().numpy()
-    rows = np.array(sorted({0, 1, cfg.n_sensors // 3, cfg.n_sensors // 2, cfg.n_sensors - 1}), np.int32)
+    rows = sample_rows(cfg.n_sensors)
     assert_parity(y[rows], oracle.forward(c, x, s, rows=rows, **op), f"{name} forward rows")
     d = inputs.residual(cfg.n_sensors, cfg.n_samples)
     g = ctx.adjoint(T(d)).cpu().numpy()
-    cols = np.random.default_rng(4).choice(cfg.M, 2048, replace=False).astype(np.int64)
-    assert_parity(g[cols], oracle.adjoint(c, d, s, cols=cols, **adj_kw(op)), f"{name} adjoint cols", elementwise=False)
+    cols = sample_cols(cfg.M)
+    assert_parity(g[cols], oracle.adjoint(c, d, s, cols=cols, **adj_kw(op)), f"{name} adjoint cols")
     info = ctx.info()
     assert info["grid_detected"] == 1

@@ -18,11 +18,9 @@ torch = pytest.importorskip("torch")
 import oracle  # noqa: E402
 from oracle import ir  # noqa: E402
 from paper_2602_03893_b200 import gpair, inputs  # noqa: E402
+from tests_common import T, assert_parity  # noqa: E402
 
 pytestmark = pytest.mark.gpu
-
-REL_L2 = 1e-5
-REL_ELEM = 1e-4
 
 # switches -> (info.tab, info.adj_kernel)
 PATHS = {
@@ -47,23 +45,7 @@ def _built():
     build.build()
 
 
-def T(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
-
-
-def compare(got, ref):
-    got = np.asarray(got, dtype=np.float64)
-    ref = np.asarray(ref, dtype=np.float64)
-    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
-    big = np.abs(ref) >= 1e-3 * np.abs(ref).max()
-    elem = float(np.max(np.abs(got[big] - ref[big]) / np.abs(ref[big])))
-    return rel, elem
-
-
-def check(got, ref, what, elementwise=True):
-    rel, elem = compare(got, ref)
-    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e}"
-    assert elem <= (REL_ELEM if elementwise else 10 * REL_ELEM), f"{what}: elementwise {elem:.3e}"
+check = assert_parity
 
 
 def small_tab_case():
@@ -95,7 +77,7 @@ def test_forward_adjoint_each_path(path, monkeypatch):
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"{path} forward")
     d = inputs.residual(s.shape[1], op["n_samples"])
     akw = {k: v for k, v in op.items() if k != "n_samples"}
-    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"{path} adjoint", elementwise=False)
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"{path} adjoint")
     ctx.close()
 
 
@@ -128,11 +110,11 @@ def test_iterate_each_path_teacher_forced(path, mode, monkeypatch):
     if mode == 0:
         z_ref, m_ref, v_ref = ir.adam_update(z0.astype(np.float64), m0.astype(np.float64), v0.astype(np.float64),
                                              gz_ref, lr, t_step, hp)
-        check(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, f"{path} Adam m increment", elementwise=False)
-        check(vt.cpu().numpy(), v_ref, f"{path} Adam v", elementwise=False)
-        check(zt.cpu().numpy() - z0, z_ref - z0, f"{path} Adam z step", elementwise=False)
+        check(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, f"{path} Adam m increment")
+        check(vt.cpu().numpy(), v_ref, f"{path} Adam v")
+        check(zt.cpu().numpy() - z0, z_ref - z0, f"{path} Adam z step")
     else:
-        check(zt.cpu().numpy(), np.maximum(z0 - lr * gz_ref, 0.0), f"{path} clamp step", elementwise=False)
+        check(zt.cpu().numpy(), np.maximum(z0 - lr * gz_ref, 0.0), f"{path} clamp step")
     ctx.close()
 
 
@@ -172,8 +154,7 @@ def test_fast_paths_random_geometry(seed, monkeypatch):
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"seed {seed} W {W} forward")
     d = rng.standard_normal((s.shape[1], n_samples)).astype(np.float32)
     akw = {k: v for k, v in op.items() if k != "n_samples"}
-    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
-          elementwise=False)
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint")
     assert info["tab"] == 1, info  # every case is on the fast (TAB) path
     ctx.close()
 
@@ -195,7 +176,7 @@ def test_per_sample_sensor_lane_adjoint(W, monkeypatch):
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"W {W} forward")
     d = rng.standard_normal((s.shape[1], op["n_samples"])).astype(np.float32)
     akw = {k: v for k, v in op.items() if k != "n_samples"}
-    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"W {W} adjoint", elementwise=False)
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"W {W} adjoint")
     ctx.close()
 
 
@@ -219,8 +200,7 @@ def test_random_geometry_any_window(seed, monkeypatch):
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"seed {seed} W {W} forward")
     d = rng.standard_normal((s.shape[1], n_samples)).astype(np.float32)
     akw = {k: v for k, v in op.items() if k != "n_samples"}
-    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint",
-          elementwise=False)
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"seed {seed} W {W} adjoint")
     ctx.close()
 
 

@@ -4,8 +4,8 @@ against oracle/vcr.py and oracle/ir.py (readings V1-V4 of DESIGN.md).
 
 Inputs are fp32 images cast exactly to fp64 for the oracle.  Gate: the
 north_star's rel L2 <= 1e-5 on the gradient, 1e-6 relative on the value (an
-fp64-accumulated sum of positive fp32 terms), elementwise reported with the
-per-kernel-vector sanity bound of reading R19.
+fp64-accumulated sum of positive fp32 terms), and the common elementwise
+gate of tests_common on every gradient / state vector.
 """
 import numpy as np
 import pytest
@@ -60,7 +60,7 @@ def test_vcr_random_image(ctx, dims, beta, eps):
     v, g = _gpu_vcr(ctx, x, dims, beta, eps)
     assert abs(v - v_ref) <= 1e-6 * abs(v_ref), (v, v_ref)
     if M > 1:
-        assert_parity(g, g_ref, f"VCR grad {dims}", elementwise=False)
+        assert_parity(g, g_ref, f"VCR grad {dims}")
     else:
         assert np.abs(g).max() == 0.0
 
@@ -72,7 +72,7 @@ def test_vcr_vessel_phantom(ctx):
     v_ref, g_ref = vcr.r_vcr(x.astype(np.float64), dims, 0.3, 1e-3)
     v, g = _gpu_vcr(ctx, x, dims, 0.3, 1e-3)
     assert abs(v - v_ref) <= 1e-6 * abs(v_ref)
-    assert_parity(g, g_ref, "VCR grad phantom", elementwise=False)
+    assert_parity(g, g_ref, "VCR grad phantom")
 
 
 def test_vcr_constant_image_closed_form(ctx):
@@ -112,7 +112,7 @@ def test_vcr_slabs_match_whole_grid(ctx, dims, cuts, halo):
         total += float(val.item())
         grads.append(g.cpu().numpy())
     assert abs(total - v_ref) <= 1e-6 * abs(v_ref), (total, v_ref)
-    assert_parity(np.concatenate(grads), g_ref, f"VCR slab grad {dims} {cuts}", elementwise=False)
+    assert_parity(np.concatenate(grads), g_ref, f"VCR slab grad {dims} {cuts}")
 
 
 def test_vcr_whole_slab_is_bit_identical_to_gpair_vcr(ctx):
@@ -183,11 +183,11 @@ def test_iterate_with_vcr_teacher_forced(mode):
     if mode == 0:
         z_ref, m_ref, _ = ir.adam_update(z0.astype(np.float64), m0.astype(np.float64), v0.astype(np.float64),
                                          gz_ref, lr, t_step, hp)
-        assert_parity(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, "Adam m increment", elementwise=False)
-        assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "Adam z step", elementwise=False)
+        assert_parity(mt.cpu().numpy() - 0.9 * m0, m_ref - 0.9 * m0, "Adam m increment")
+        assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "Adam z step")
     else:
         x_ref = np.maximum(z0 - lr * gz_ref, 0.0)
-        assert_parity(zt.cpu().numpy() - z0, x_ref - z0, "clamp step", elementwise=False)
+        assert_parity(zt.cpu().numpy() - z0, x_ref - z0, "clamp step")
 
 
 def test_iterate_vcr_rejects_bad_grid(ctx):

@@ -1,9 +1,22 @@
-"""Helpers shared by the GPU parity tests (tolerances: north_star / DESIGN.md R19)."""
+"""The ONE parity gate shared by every GPU test (north_star).
+
+For fp32 GPU results against the fp64 oracle -- signals y, gradients g, dL/dz,
+Adam state and the one-step update alike:
+  * relative L2 error <= 1e-5, and
+  * max elementwise relative error <= 1e-4 over the entries with
+    |oracle| >= 1e-3 max|oracle|.
+There is no looser per-kernel-vector bound.  At the bench sizes the oracle runs
+on exact operator rows / columns (32 sampled sensors for forward
+rows, 65,536 sampled kernels for adjoint columns).
+"""
 import numpy as np
 import torch
 
 REL_L2 = 1e-5
 REL_ELEM = 1e-4
+ELEM_FLOOR = 1e-3  # entries gated elementwise: |oracle| >= ELEM_FLOOR * max|oracle|
+N_ROWS = 32        # sampled forward rows (sensors) at full size
+N_COLS = 65536     # sampled adjoint columns (kernels) at full size
 
 
 def dev():
@@ -15,27 +28,37 @@ def T(a):
 
 
 def compare(got, ref):
+    """(rel L2, max elementwise relative error over |ref| >= ELEM_FLOOR max|ref|)."""
     got = np.asarray(got, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
     nref = np.linalg.norm(ref)
     rel = np.linalg.norm(got - ref) / nref if nref > 0 else np.linalg.norm(got)
-    big = np.abs(ref) >= 1e-3 * np.abs(ref).max() if nref > 0 else np.zeros(ref.shape, bool)
+    big = np.abs(ref) >= ELEM_FLOOR * np.abs(ref).max() if nref > 0 else np.zeros(ref.shape, bool)
     elem = float(np.max(np.abs(got[big] - ref[big]) / np.abs(ref[big]))) if big.any() else 0.0
     return rel, elem
 
 
-def assert_parity(got, ref, what, elementwise=True):
-    """rel L2 gate on everything; the elementwise gate applies to signal
-    samples (north_star: "1e-4 max elementwise relative error on samples
-    above 1e-3 of peak"; reading R19).  For per-kernel vectors it
-    is reported with a 10x looser sanity bound."""
+def assert_parity(got, ref, what):
     rel, elem = compare(got, ref)
-    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e}"
-    bound = REL_ELEM if elementwise else 10 * REL_ELEM
-    assert elem <= bound, f"{what}: max elementwise rel {elem:.3e}"
+    print(f"{what}: rel L2 {rel:.2e} elementwise {elem:.2e}")
+    assert rel <= REL_L2, f"{what}: rel L2 {rel:.3e} > {REL_L2}"
+    assert elem <= REL_ELEM, f"{what}: max elementwise rel {elem:.3e} > {REL_ELEM}"
     return rel, elem
 
 
+def sample_rows(n_sensors, n=N_ROWS, seed=5):
+    """Sorted sensor subset for full-size forward parity (first, last and random rows)."""
+    if n_sensors <= n:
+        return np.arange(n_sensors, dtype=np.int32)
+    rest = np.random.default_rng(seed).choice(np.arange(1, n_sensors - 1), n - 2, replace=False)
+    return np.sort(np.concatenate([[0, n_sensors - 1], rest])).astype(np.int32)
+
+
+def sample_cols(M, n=N_COLS, seed=4):
+    """Sorted kernel subset for full-size adjoint parity."""
+    if M <= n:
+        return np.arange(M, dtype=np.int64)
+    return np.sort(np.random.default_rng(seed).choice(M, n, replace=False)).astype(np.int64)
 
 
 def psnr(a, ref):
