@@ -193,8 +193,10 @@ typedef struct {
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial
  * cells, builds per-(region, sensor) sample windows and allocates
  * workspaces.  Runs on `stream` and synchronises it before returning.
- * Errors: INVALID_ARGUMENT, GEOMETRY (r_ij <= k sigma for some pair, checked
- * conservatively per cell), RESOURCE, CUDA.  *out is NULL on error. */
+ * Errors: INVALID_ARGUMENT, GEOMETRY (r_ij <= k sigma_i for some pair: cells
+ * whose bounding sphere comes within k sigma of a sensor are tested pair by
+ * pair in fp64 with the oracle's operations, so exactly the geometries the
+ * oracle rejects are rejected), RESOURCE, CUDA.  *out is NULL on error. */
 gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream);
 
 /* Forward operator (Eq. 7 summed over kernels).

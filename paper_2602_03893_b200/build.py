@@ -26,6 +26,8 @@ def build(force=False, verbose=False):
              and os.path.getmtime(LIB) >= max(os.path.getmtime(d) for d in deps))
     if not force and fresh:
         return LIB
+    if not force and os.environ.get("GPAIR_LIB") and os.path.exists(LIB) and not extra:
+        return LIB  # a named variant is used as built (its -D flags live in its stamp, not in this env)
     objdir = os.path.join(HERE, "build", os.path.basename(LIB)[:-3])
     os.makedirs(objdir, exist_ok=True)
     objs = []

@@ -12,6 +12,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "gpair_ctx.h"
 
 using gpair::EpiParams;
@@ -130,12 +132,34 @@ gpair_status cuda_fail(gpair_ctx* c, cudaError_t e, const char* where) {
 bool finite_pos(double x) { return std::isfinite(x) && x > 0.0; }
 
 // Event-timed launch wrapper.
+// NVTX ranges (domain "gpair", one per stage; header-only nvtx3, no-ops unless a
+// tool such as nsys or ncu --nvtx is attached): they bracket the enqueue of each
+// stage's kernels, so a timeline attributes every launch to its stage.
+nvtxDomainHandle_t nvtx_domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("gpair");
+    return d;
+}
+const char* const kStageName[GPAIR_PROF_N] = {"gather", "forward", "reduce", "allreduce",
+                                              "residual", "adjoint", "loss", "vcr"};
+struct NvtxRange {
+    explicit NvtxRange(const char* name) {
+        nvtxEventAttributes_t a{};
+        a.version = NVTX_VERSION;
+        a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+        a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+        a.message.ascii = name;
+        nvtxDomainRangePushEx(nvtx_domain(), &a);
+    }
+    ~NvtxRange() { nvtxDomainRangePop(nvtx_domain()); }
+};
+
 struct ProfScope {
     gpair_ctx* c;
     int id;
     cudaStream_t st;
     cudaEvent_t a = nullptr, b = nullptr;
-    ProfScope(gpair_ctx* c_, int id_, cudaStream_t st_) : c(c_), id(id_), st(st_) {
+    NvtxRange nv;
+    ProfScope(gpair_ctx* c_, int id_, cudaStream_t st_) : c(c_), id(id_), st(st_), nv(kStageName[id_]) {
         if (!c->prof_on) return;
         a = take();
         b = take();
@@ -367,6 +391,7 @@ double gpair_cawr_lr(int64_t t, double eta_min, double eta_max, int64_t T0, int6
 }
 
 gpair_status gpair_create(gpair_ctx** out, const gpair_desc* d, void* stream) {
+    NvtxRange nvtx_call("create");
     if (!out) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     if (!d) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "desc is NULL");
@@ -746,6 +771,7 @@ gpair_status gpair_vcr_prepare(gpair_ctx* c, const int32_t* grid, int32_t z0, vo
 
 gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const float* b, const gpair_step* s,
                            float* signals_out, float* x_out, float* loss_out, void* stream) {
+    NvtxRange nvtx_call("iterate");
     if (!c) return fail(nullptr, GPAIR_ERR_INVALID_ARGUMENT, "ctx is NULL");
     if (!z || !b || !s) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "z/b/step NULL");
     if (s->mode != 0 && s->mode != 1) return fail(c, GPAIR_ERR_INVALID_ARGUMENT, "mode must be 0 (NPC) or 1 (clamp)");

@@ -52,7 +52,7 @@ struct gpair_ctx_s {
     int32_t a_cpr = 0, a_regions = 0, La = 0;
     int32_t* d_wlo_a = nullptr;   // [a_regions][Nd]
     gpair::gacc_t* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
-    float* d_gtab = nullptr;      // [2][La] G(t - La/2) = 2^{K tau^2} and its inverse (k_adjoint_lcf), or NULL
+    double* d_gtab = nullptr;     // [La][4] fp64 Q = 2^{-2K tau}, 1/Q, 1/G, G = 2^{K tau^2}, tau = t - La/2 (k_adjoint_lcf), or NULL
 
     // per-call workspaces
     float* d_amp = nullptr;       // [Mpad] amplitudes in sorted order

@@ -114,13 +114,15 @@ struct __align__(16) Anchor {
 
 constexpr int32_t NA_EXACT = -2147483647 - 1;
 
-__device__ __forceinline__ Anchor make_anchor(float4 C, float sx, float sy, float sz, const OpConst& k) {
+__device__ __forceinline__ Anchor make_anchor(float4 C, float sx, float sy, float sz, const OpConst& k,
+                                              double* invR_out = nullptr) {
     const double dx = (double)C.x - (double)sx;
     const double dy = (double)C.y - (double)sy;
     const double dz = (double)C.z - (double)sz;
     const double R2 = fma(dx, dx, fma(dy, dy, dz * dz));
     const double invR = rsqrt(R2);
     const double R = R2 * invR;
+    if (invR_out) *invR_out = invR;
     const double tf = fma(R, k.inv_h, -k.t0fs);  // (R/v - t0) f_s in samples
     const double na = floor(tf);
     Anchor a;
@@ -644,7 +646,8 @@ constexpr int STAGE_CELLS = 8;  // cells per staged kernel tile
 // Reduce-scatter of 8 per-lane values (one group of 8 kernels) over the warp's 32
 // sensors: xor 16 / 8 / 4 halve the value set, xor 2 / 1 finish the sums; lane 4k
 // ends with kernel k's sum and writes it to dst[k] (fixed order: deterministic).
-__device__ __forceinline__ void warp_reduce_scatter8(const float (&gv)[GROUP], int lane, gacc_t* dst) {
+template <typename VT>
+__device__ __forceinline__ void warp_reduce_scatter8(const VT (&gv)[GROUP], int lane, gacc_t* dst) {
     const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
     gacc_t h4[4];
 #pragma unroll
@@ -680,10 +683,11 @@ __device__ __forceinline__ void stage_kernel_tile(const float4* __restrict__ kd,
 }
 
 // Sum of the CTA's per-warp kernel sums in warp order -> this sensor group's partial gradient.
-__device__ __forceinline__ void write_group_partials(const gacc_t* s_g, int nw, int nc, gacc_t* __restrict__ dst) {
+__device__ __forceinline__ void write_group_partials(const gacc_t* s_g, int nw, int nc, gacc_t* __restrict__ dst,
+                                                     int stride = STAGE_CELLS * CELL) {
     for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
         gacc_t sum = 0;
-        for (int w = 0; w < nw; ++w) sum += s_g[w * (STAGE_CELLS * CELL) + t];
+        for (int w = 0; w < nw; ++w) sum += s_g[w * stride + t];
         dst[t] = sum;
     }
 }

@@ -46,6 +46,9 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 }
 
 // ------------------------------------------------------------------ forward
+#ifndef GPAIR_FWD_EXP
+#define GPAIR_FWD_EXP 0
+#endif
 #ifndef GPAIR_FWD_MINB
 #define GPAIR_FWD_MINB 3
 #endif
@@ -254,6 +257,39 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                         const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
                         const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
                         if (!(bad0 || bad1)) {
+#if GPAIR_FWD_EXP
+                            if (true) {  // numerics experiment (see GPAIR_LCF_EXP): exact fp64 pair values
+                                const float4 Cg = s_grp[gq];
+                                const double dxa = (double)Cg.x - sx, dya = (double)Cg.y - sy, dza = (double)Cg.z - sz;
+                                const double Ra = sqrt(dxa * dxa + dya * dya + dza * dza);
+                                const double tfa = fma(Ra, k.inv_h, -k.t0fs);
+                                const double K64 = -1.4426950408889634 * k.h * k.h / (2.0 * k.sigma * k.sigma);
+                                float Aa, Ab;
+                                upk2(A2, Aa, Ab);
+#pragma unroll
+                                for (int hh = 0; hh < 2; ++hh) {
+                                    const int lk = li + hh;
+                                    const int pb = (lk >> 1) * 4 + (lk & 1);
+                                    const double ex = s_kxy[pb], ey = s_kxy[pb + 2], ez = s_kzw[pb];
+                                    float e32a, e32b, u32a, u32b;
+                                    upk2(eu, e32a, e32b);
+                                    upk2(ulo, u32a, u32b);
+                                    const float e32 = hh ? e32b : e32a, u32 = hh ? u32b : u32a;
+                                    const double flp1 = (double)(e32 - u32);
+                                    const double q = 2.0 * (dxa * ex + dya * ey + dza * ez) + (ex * ex + ey * ey + ez * ez);
+                                    const double off = q / (Ra + sqrt(Ra * Ra + q));
+                                    const double r = Ra + off;
+                                    const double u0 = GPAIR_FWD_EXP == 2 ? (tfa - (double)a.na) + off * k.inv_h - flp1
+                                                                         : (double)u32;
+                                    const double wA = (double)(hh ? Ab : Aa) * 0.5 * k.h / r;
+                                    float* ap = s_acc_lane + (hh ? n1 : n0) * 32;
+                                    for (int mm = 0; mm < WMAX; ++mm) {
+                                        const double u = u0 - mm;
+                                        ap[mm * 32] += (float)(wA * u * exp2(K64 * u * u));
+                                    }
+                                }
+                            } else
+#endif
                             if (TABW && tab.on) {
                                 // u_c = u_lo - C (exact), E = exp2(K u_c^2), r = exp2(-2K u_c), s = 1/r
                                 const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
@@ -818,74 +854,115 @@ __global__ void __launch_bounds__(256, GPAIR_ADJT_MINB) k_adjoint_t(const float4
     }
 }
 
-// ------------------------------------------------------------------ adjoint, lane-centred factorisation
-// k_adjoint_t's decomposition with the Gaussian factorised about the CENTRE of
-// the lane's residual column instead of each pair's centre.  Column index t,
-// tau = t - T (T = La / 2), G(tau) = 2^{K tau^2} (fp64 table).
-// For a pair with window start o and u = u_lo - i at t = o + i (u_lo in
-// (ku - 1, ku)), a = u_lo + o - T is its centre in column coordinates and
-//   u 2^{K u^2} = 2^{K u_lo^2} G(o - T)^{-1} * R^i G(o + i - T) (u_lo - i),
-//   R = 2^{-2 K a}.
-// The column is staged once per region as dtil_t = delta_t G(t - T), so
-//   g_ij = w 2^{K u_lo^2} / G(o - T) * (u_lo P - R P'),
-//   P = sum_i dtil_{o+i} R^i,  P' = dP/dR,
-// one simultaneous Horner step (two FFMA) per sample and no table in the loop.
-// R comes from an exact range reduction 2^n * poly(f), |f| <= 1/2, degree 7
-// (unbiased to fp32 rounding).  Valid while |K| max(T, La - T)^2 <= LCF_KMAX
-// (every factor stays a normal fp32); else k_adjoint_t is used.
-constexpr float LCF_KMAX = 90.f;
-
-__device__ __forceinline__ float rcpf(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// 2^x for |x| < 64: 2^rint(x) * e^{f ln2}, f = x - rint(x) in [-1/2, 1/2]
-__device__ __forceinline__ f2_t exp2_acc2(f2_t x) {
-    const f2_t t = add2(x, pk2(RND_MAGIC, RND_MAGIC));
-    const f2_t f = sub2(x, add2(t, pk2(-RND_MAGIC, -RND_MAGIC)));
-    f2_t p = fma2(f, pk2(1.5252733804059840e-5f, 1.5252733804059840e-5f), pk2(1.5403530393381609e-4f, 1.5403530393381609e-4f));
-    p = fma2(f, p, pk2(1.3333558146428443e-3f, 1.3333558146428443e-3f));
-    p = fma2(f, p, pk2(9.6181291076284772e-3f, 9.6181291076284772e-3f));
-    p = fma2(f, p, pk2(5.5504108664821580e-2f, 5.5504108664821580e-2f));
-    p = fma2(f, p, pk2(2.4022650695910071e-1f, 2.4022650695910071e-1f));
-    p = fma2(f, p, pk2(6.9314718055994531e-1f, 6.9314718055994531e-1f));
-    p = fma2(f, p, pk2(1.f, 1.f));
-    float p0, p1, t0, t1;
-    upk2(p, p0, p1);
-    upk2(t, t0, t1);
-    p0 = __int_as_float(__float_as_int(p0) + ((__float_as_int(t0) - RND_MAGIC_BITS) << 23));
-    p1 = __int_as_float(__float_as_int(p1) + ((__float_as_int(t1) - RND_MAGIC_BITS) << 23));
-    return pk2(p0, p1);
-}
-
-#ifndef GPAIR_ADJ_EPOLY
-#define GPAIR_ADJ_EPOLY 0
+// ------------------------------------------------------------------ adjoint, lane-centred factorisation (fp64 chains)
+// k_adjoint_t's decomposition (lane = sensor, the lane's residual window in a private
+// smem column, fp64 anchor per 8-kernel group) with the Gaussian factorised about the
+// CENTRE of the lane's column.  Column index t, T = La / 2, G(t) = 2^{K (t - T)^2}.
+// A pair's window is t_c + m, m in [-C, W - C) (t_c = o + C, C = W / 2) with
+// u = u_c - m, u_c = u_lo - C in (-1, 0], and
+//   (u_c - m) 2^{K (u_c - m)^2} = E Ginv(t_c) G(t_c + m) R^m (u_c - m),
+//   E = 2^{K u_c^2},   R = 2^{-2K (u_c + t_c - T)} = r Q(t_c),   r = 2^{-2K u_c},
+//   Q(t) = 2^{-2K (t - T)},  Ginv = 1 / G.
+// The column is staged once per region as dtil_t = delta_t G(t) (fp64), so
+//   g_ij = w E Ginv(t_c) [u_c (U + L) - R U' + L#],
+//   U = sum_{m=0}^{W-C-1} dtil_{t_c+m} R^m,  U' = dU/dR,
+//   L = sum_{k=1}^{C} dtil_{t_c-k} S^k,  S = 1 / R,  L# = S dL/dS,
+// two simultaneous Horner chains per half, one DFMA per chain and sample.  The chains,
+// R, S, E and the weight are fp64: in fp32 the rounding of R enters every power R^m and
+// made the gradient's error 2e-7 (rel L2); the fp64 pipe (64 DFMA / clk / SM)
+// carries two DFMA per pair-sample plus ~30 per pair.  r, 1 / r and E are short fp64
+// polynomials of |z| <= 0.3 (truncation < 4e-10); G, Ginv, Q, 1 / Q are fp64 tables
+// (host exp2).  Valid while G stays a normal fp32 (GPAIR_LCF_COL32): |K| max(T, La - T)^2 <= 100.
+#ifndef GPAIR_LCF_WARPS
+#define GPAIR_LCF_WARPS 4
 #endif
 #ifndef GPAIR_LCF_MINB
-#define GPAIR_LCF_MINB 3
+#define GPAIR_LCF_MINB 4
 #endif
+constexpr int LCF_WARPS = GPAIR_LCF_WARPS;  // sensor warps per CTA (the fp64 column costs La * 256 B per warp)
+constexpr int LCF_STAGE = 4;                // cells per staged kernel tile (4 CTAs of 4 warps per SM at La = 48)
+#ifndef GPAIR_LCF_PACKS
+#define GPAIR_LCF_PACKS 2
+#endif
+constexpr int LCF_PACKS = GPAIR_LCF_PACKS;  // f32x2 time-of-flight packs per step
+constexpr int LCF_PPS = 2 * LCF_PACKS;      // pairs (kernels) per step: independent fp64 chains
+#ifndef GPAIR_LCF_COL32
+#define GPAIR_LCF_COL32 0
+#endif
+#if GPAIR_LCF_COL32
+typedef float lcol_t;
+#else
+typedef double lcol_t;
+#endif
+
+// fp64 polynomial coefficients in the constant bank (DFMA takes them as c[][] operands
+// instead of two register moves per use): 1/720, 1/24, 1/2, 1/5040, 1/120, 1/6, 1
+__constant__ double kLcfPoly[7] = {1.0 / 720.0, 1.0 / 24.0, 0.5, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0, 1.0};
+// e^{+z} and e^{-z} for |z| <= 0.3: C(z^2) +- z S(z^2), degree 3 in z^2 (truncation < 4e-10,
+// and < 4e-12 at the W = 16 bench constants, |z| <= 0.14)
+__device__ __forceinline__ void exp_pm64(double z, double& ep, double& em) {
+    const double y = z * z;
+    double Cc = fma(y, kLcfPoly[0], kLcfPoly[1]);
+    Cc = fma(y, Cc, kLcfPoly[2]);
+    Cc = fma(y, Cc, kLcfPoly[6]);
+    double Sc = fma(y, kLcfPoly[3], kLcfPoly[4]);
+    Sc = fma(y, Sc, kLcfPoly[5]);
+    Sc = fma(y, Sc, kLcfPoly[6]);
+    const double zs = z * Sc;
+    ep = Cc + zs;
+    em = Cc - zs;
+}
+// e^{z} for -0.13 <= z <= 0: Taylor degree 6 (truncation < 1e-11)
+__device__ __forceinline__ double exp_small64(double z) {
+    double p = fma(z, kLcfPoly[0], kLcfPoly[4]);
+    p = fma(z, p, kLcfPoly[1]);
+    p = fma(z, p, kLcfPoly[5]);
+    p = fma(z, p, kLcfPoly[2]);
+    p = fma(z, p, kLcfPoly[6]);
+    return fma(z, p, kLcfPoly[6]);
+}
+// 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
+__device__ __forceinline__ double exp2_64(double x) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x to an integer
+    const double tn = x + magic;
+    const double n = tn - magic;
+    const double z = (x - n) * 0.6931471805599453;
+    double p = fma(z, 1.0 / 3628800.0, 1.0 / 362880.0);
+    p = fma(z, p, 1.0 / 40320.0);
+    p = fma(z, p, 1.0 / 5040.0);
+    p = fma(z, p, 1.0 / 720.0);
+    p = fma(z, p, 1.0 / 120.0);
+    p = fma(z, p, 1.0 / 24.0);
+    p = fma(z, p, 1.0 / 6.0);
+    p = fma(z, p, 0.5);
+    p = fma(z, p, 1.0);
+    p = fma(z, p, 1.0);
+    const int ni = __double2loint(tn);  // low word of x + magic = n (two's complement)
+    return p * __hiloint2double((ni + 1023) << 20, 0);
+}
+
 template <int W, int SDEG>
-__global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp,
-                                                       const float* __restrict__ orig, const float* __restrict__ sens,
-                                                       const int32_t* __restrict__ wlo, const float* __restrict__ resid,
-                                                       const float* __restrict__ gtab, gacc_t* __restrict__ gpart,
-                                                       int32_t cpr, int32_t ncells, int32_t La, int64_t Mpad, OpConst k,
-                                                       float K, float m2K) {
-    extern __shared__ float4 smem4[];
-    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
-    float* s_kxy = (float*)smem4;
-    float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
-    float4* s_grp = (float4*)(s_kzw + STAGE_CELLS * CELL * 2);  // [STAGE_CELLS*GPC]
+__global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
+    k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
+                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const float* __restrict__ resid,
+                  const double* __restrict__ gtab, gacc_t* __restrict__ gpart, int32_t cpr, int32_t ncells,
+                  int32_t La, int64_t Mpad, OpConst k, double Kln2) {
+    constexpr int C = W / 2;
+    extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    gacc_t* s_g = (gacc_t*)(s_grp + STAGE_CELLS * GPC);  // [nw][STAGE_CELLS*CELL] per-warp kernel sums
-    float* s_gt = (float*)(s_g + nw * STAGE_CELLS * CELL);          // [2][La]: G(t - T), 1 / G(t - T)
-    float* col = s_gt + 2 * La + (size_t)warp * La * 32 + lane;  // this lane's column dtil_t at col[t * 32]
-    for (int t = threadIdx.x; t < 2 * La; t += blockDim.x) s_gt[t] = gtab[t];
-    const float* s_ginv = s_gt + La;
+    double* s_tab = smem8;                                  // [La][4]: Q, 1/Q, Ginv, G (fp64)
+    gacc_t* s_g = (gacc_t*)(s_tab + 4 * La);                // [nw][LCF_STAGE*CELL] per-warp kernel sums
+    // this lane's column dtil_t = delta_t G(t) at col[t*32] (lcol_t: fp64, or fp32 widened by F2F
+    // per sample -- half the shared-memory bytes, but F2F issues on the 16 / clk / SM XU pipe)
+    lcol_t* col = (lcol_t*)(s_g + nw * LCF_STAGE * CELL) + (size_t)warp * La * 32 + lane;
+    float4* s_grp = (float4*)((lcol_t*)(s_g + nw * LCF_STAGE * CELL) + (size_t)nw * La * 32);  // [LCF_STAGE*GPC]
+    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
+    float* s_kxy = (float*)(s_grp + LCF_STAGE * GPC);
+    float* s_kzw = s_kxy + LCF_STAGE * CELL * 2;
+    for (int t = threadIdx.x; t < 4 * La; t += blockDim.x) s_tab[t] = gtab[t];
+
     const int c0 = blockIdx.x * cpr, c1 = min(c0 + cpr, ncells);
-    if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(STAGE_CELLS, c1 - c0), s_kxy, s_kzw, s_grp);
+    if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(LCF_STAGE, c1 - c0), s_kxy, s_kzw, s_grp);
 
     const int region = blockIdx.x;
     const int j = ((blockIdx.y + k.grp0) * nw + warp) * 32 + lane;
@@ -901,42 +978,39 @@ __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float
         const float* src = resid + (int64_t)j * k.Nt;
         for (int t = 0; t < La; ++t) {
             const int n = lo_j + t;
-            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? src[n] * __ldg(gtab + t) : 0.f;
+            col[t * 32] = (lo_j >= 0 && n < k.Nt) ? (lcol_t)((double)src[n] * __ldg(gtab + 4 * t + 3)) : (lcol_t)0;
         }
     }
-    const int Tc = La >> 1;
-    const f2_t c8 = pk2(1.f / 8.f, 1.f / 8.f), c4 = pk2(-0.25f, -0.25f), one = pk2(1.f, 1.f);
-    const f2_t c38 = pk2(3.f / 8.f, 3.f / 8.f), c2 = pk2(-0.5f, -0.5f);
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
-    const f2_t K2 = pk2(K, K), M2K = pk2(m2K, m2K);
+    const f2_t one = pk2(1.f, 1.f);
     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-    for (int cb = c0; cb < c1; cb += STAGE_CELLS) {
-        const int nc = min(STAGE_CELLS, c1 - cb);
+    const double K64 = Kln2 * 1.4426950408889634;  // log2-based K (exact enough: only the rare path uses it)
+    for (int cb = c0; cb < c1; cb += LCF_STAGE) {
+        const int nc = min(LCF_STAGE, c1 - cb);
         if (cb != c0) {  // the first tile was staged with the residual columns
             __syncthreads();  // every warp is done with the previous tile and its s_g sums
             stage_kernel_tile(kd, grp, cb, nc, s_kxy, s_kzw, s_grp);
         }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
-            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
-            float gv[GROUP];
+            double invR64;
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k, &invR64);
+            const double h2R64 = 0.5 * k.h * invR64;
+            double gv[GROUP];
             const bool exact_grp = __any_sync(0xffffffffu, a.na == NA_EXACT);
             const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
-            const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
-            const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R);
+            const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh), Eu = pk2(a.Eu, a.Eu);
             const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // o = n_lo - lo_j = bits(tt) + nrel
-            const float cg = (float)(a.na - lo_j - Tc);            // a_pair = eu + cg (exact integer shift)
-            const f2_t CG = pk2(cg, cg);
-            // four kernels per step: two f32x2 packs whose Horner chains interleave (ILP)
+            // LCF_PPS kernels per step: LCF_PACKS f32x2 packs for the (fp32) time of flight
 #pragma unroll
-            for (int t = 0; t < GROUP; t += 4) {
+            for (int t = 0; t < GROUP; t += LCF_PPS) {
                 const int li = gq * GROUP + t;
                 bool rare = exact_grp;
-                f2_t eu[2], w[2], ulo[2];
-                int o[4];
+                f2_t ulo[LCF_PACKS], twm1[LCF_PACKS];
+                int o[LCF_PPS];
                 if (!exact_grp) {
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
+                    for (int h = 0; h < LCF_PACKS; ++h) {
                         const float4 pxy = *(const float4*)(s_kxy + 2 * (li + 2 * h));
                         const float4 pzw = *(const float4*)(s_kzw + 2 * (li + 2 * h));
                         const f2_t kx = pk2(pxy.x, pxy.y), ky = pk2(pxy.z, pxy.w);
@@ -945,13 +1019,13 @@ __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float
                         const f2_t eps = mul2(q, iR2);
                         f2_t S, Tw;
                         series2<SDEG>(eps, S, Tw);
-                        eu[h] = fma2(mul2(q, i2Rh), S, Eu);
-                        w[h] = mul2(h2R, Tw);
-                        const f2_t x = add2(eu[h], clo);
+                        twm1[h] = sub2(Tw, one);  // T(eps) - 1, exact (Sterbenz): w = h / 2R (1 + twm1) in fp64
+                        const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
+                        const f2_t x = add2(eu, clo);
                         const f2_t tt = add2(x, mag);
                         const f2_t fl = add2(tt, nmag);
                         const f2_t d = sub2(x, fl);
-                        ulo[h] = sub2(eu[h], add2(fl, one));
+                        ulo[h] = sub2(eu, add2(fl, one));
                         float d0, d1, t0, t1;
                         upk2(d, d0, d1);
                         upk2(tt, t0, t1);
@@ -962,100 +1036,92 @@ __global__ void __launch_bounds__(256, GPAIR_LCF_MINB) k_adjoint_lcf(const float
                     }
                 }
                 if (!rare && lo_j >= 0) {
-                    // centred form: value = w 2^{K u_c^2} / G(o + C - T) * [u_c (U + L) - R U' + L#],
-                    // U = sum_{m>=0} at_m R^m, L = sum_{k>=1} at_{-k} S^k (S = 1/R), at_m = dtil_{o+C+m};
-                    // the two halves are independent Horner chains (ILP) with weights |m| <= C
-                    constexpr int C = W / 2;
-                    f2_t R2[2], S2[2], U[2], Ud[2], La_[2], Ld[2], UC[2];
-                    float sc[4];
-                    const float* rp[4];
+                    double U[LCF_PPS], Ud[LCF_PPS], Lc[LCF_PPS], Ld[LCF_PPS], R[LCF_PPS], S[LCF_PPS], uc[LCF_PPS];
+                    const lcol_t* rp[LCF_PPS];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        R2[h] = exp2_acc2(mul2(add2(eu[h], CG), M2K));  // R = 2^{-2 K a}, a = eu + cg
-                        float r0, r1;
-                        upk2(R2[h], r0, r1);
-                        float q0 = rcpf(r0), q1 = rcpf(r1);
-                        q0 = q0 * fmaf(-r0, q0, 2.f);  // one Newton step: S to fp32 rounding
-                        q1 = q1 * fmaf(-r1, q1, 2.f);
-                        S2[h] = pk2(q0, q1);
-                        UC[h] = add2(ulo[h], pk2(-(float)C, -(float)C));  // u_c, exact
-#if GPAIR_ADJ_EPOLY
-                        // 2^{K u_c^2} by the unbiased polynomial: a per-pair scale error enters g directly
-                        float e0, e1;
-                        upk2(exp2_acc2(mul2(mul2(UC[h], K2), UC[h])), e0, e1);
-                        upk2(mul2(w[h], pk2(e0 * s_ginv[o[2 * h] + C], e1 * s_ginv[o[2 * h + 1] + C])),
-                             sc[2 * h], sc[2 * h + 1]);
-#else
-                        float e0, e1;
-                        upk2(mul2(mul2(UC[h], K2), UC[h]), e0, e1);
-                        upk2(mul2(w[h], pk2(ex2f(e0) * s_ginv[o[2 * h] + C], ex2f(e1) * s_ginv[o[2 * h + 1] + C])),
-                             sc[2 * h], sc[2 * h + 1]);
-#endif
-                        rp[2 * h] = col + (o[2 * h] + C) * 32;
-                        rp[2 * h + 1] = col + (o[2 * h + 1] + C) * 32;
-                        U[h] = pk2(rp[2 * h][(W - C - 1) * 32], rp[2 * h + 1][(W - C - 1) * 32]);
-                        Ud[h] = pk2(0.f, 0.f);
-                        La_[h] = pk2(rp[2 * h][-C * 32], rp[2 * h + 1][-C * 32]);
-                        Ld[h] = pk2(0.f, 0.f);
+                    for (int h = 0; h < LCF_PPS; ++h) {
+                        float u32a, u32b, w32a, w32b;
+                        upk2(ulo[h >> 1], u32a, u32b);
+                        upk2(twm1[h >> 1], w32a, w32b);
+                        uc[h] = (double)((h & 1) ? u32b : u32a) - (double)C;  // exact
+                        const int tc = o[h] + C;
+                        double rr, ri;
+                        exp_pm64(-2.0 * Kln2 * uc[h], rr, ri);  // r = 2^{-2K u_c}, 1/r
+                        const double2 qq = *(const double2*)(s_tab + 4 * tc);  // Q(t_c), 1/Q(t_c)
+                        R[h] = rr * qq.x;
+                        S[h] = ri * qq.y;
+                        rp[h] = col + tc * 32;
+                        U[h] = (double)rp[h][(W - C - 1) * 32];
+                        Ud[h] = 0.0;
+                        Lc[h] = (double)rp[h][-C * 32];
+                        Ld[h] = 0.0;
+                        // scale w E Ginv(t_c), E = e^{K ln2 u_c^2}
+                        const double w64 = fma(h2R64, (double)((h & 1) ? w32b : w32a), h2R64);
+                        gv[t + h] = w64 * exp_small64(Kln2 * uc[h] * uc[h]) * s_tab[4 * tc + 2];
                     }
 #pragma unroll
                     for (int i = 1; i < C; ++i) {
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < LCF_PPS; ++h) {
                             const int mu = W - C - 1 - i;  // upper: m = W-C-2 .. 0
-                            Ud[h] = fma2(Ud[h], R2[h], U[h]);
-                            U[h] = fma2(U[h], R2[h], pk2(rp[2 * h][mu * 32], rp[2 * h + 1][mu * 32]));
+                            Ud[h] = fma(Ud[h], R[h], U[h]);
+                            U[h] = fma(U[h], R[h], (double)rp[h][mu * 32]);
                             const int ml = -C + i;  // lower: m = -C+1 .. -1
-                            Ld[h] = fma2(Ld[h], S2[h], La_[h]);
-                            La_[h] = fma2(La_[h], S2[h], pk2(rp[2 * h][ml * 32], rp[2 * h + 1][ml * 32]));
+                            Ld[h] = fma(Ld[h], S[h], Lc[h]);
+                            Lc[h] = fma(Lc[h], S[h], (double)rp[h][ml * 32]);
                         }
                     }
 #pragma unroll
-                    for (int i = C; i < W - C; ++i) {  // upper chain longer than the lower one (W odd: never, W % 4 == 0)
+                    for (int i = C; i < W - C; ++i) {  // upper chain longer than the lower one (never for W % 4 == 0)
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
+                        for (int h = 0; h < LCF_PPS; ++h) {
                             const int mu = W - C - 1 - i;
-                            Ud[h] = fma2(Ud[h], R2[h], U[h]);
-                            U[h] = fma2(U[h], R2[h], pk2(rp[2 * h][mu * 32], rp[2 * h + 1][mu * 32]));
+                            Ud[h] = fma(Ud[h], R[h], U[h]);
+                            U[h] = fma(U[h], R[h], (double)rp[h][mu * 32]);
                         }
                     }
 #pragma unroll
-                    for (int h = 0; h < 2; ++h) {
-                        // L = S Lacc, L# = S Lacc + S^2 Lacc'
-                        const f2_t Lv = mul2(S2[h], La_[h]);
-                        const f2_t Ls = fma2(mul2(S2[h], S2[h]), Ld[h], Lv);
-                        // u_c (U + L) - R U' + L#
-                        const f2_t v = add2(fma2(UC[h], add2(U[h], Lv), mul2(mul2(R2[h], Ud[h]), pk2(-1.f, -1.f))), Ls);
-                        float v0, v1;
-                        upk2(v, v0, v1);
-                        gv[t + 2 * h] = sc[2 * h] * v0;
-                        gv[t + 2 * h + 1] = sc[2 * h + 1] * v1;
+                    for (int h = 0; h < LCF_PPS; ++h) {
+                        // L = S Lc, L# = S Lc + S^2 Ld;  u_c (U + L) - R U' + L#
+                        const double Lv = S[h] * Lc[h];
+                        const double Ls = fma(S[h] * S[h], Ld[h], Lv);
+                        gv[t + h] *= fma(uc[h], U[h] + Lv, -R[h] * Ud[h]) + Ls;
                     }
                 } else {
-#pragma unroll
-                    for (int h = 0; h < 4; ++h) {  // exact window edges / record clipping / exact-ToF groups
-                        float g = 0.f;
+#pragma unroll 1
+                    for (int h = 0; h < LCF_PPS; ++h) {  // exact window edges / record clipping / exact-ToF groups
+                        double g = 0.0;
                         if (lo_j >= 0) {
                             const int64_t gi = (int64_t)cb * CELL + li + h;
                             const int pb = ((li + h) >> 1) * 4 + ((li + h) & 1);
                             const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
                             const PairWin pw = pair_setup<SDEG>(a, kdt, 1.f, orig, gi, Mpad, sx, sy, sz, k);
-                            float part = 0.f;
-                            const int oo = pw.n_lo - lo_j;
-                            for (int m = 0; m < pw.cnt; ++m) {
-                                const float um = pw.u_lo - (float)m;
-                                part = fmaf(um * ex2f((um * k.K1u) * um), col[(oo + m) * 32] * s_ginv[oo + m], part);
+                            // the exact window [n_lo, n_lo + cnt) from its start t0 = n_lo - lo_j:
+                            // (u - m) 2^{K (u - m)^2} = 2^{K u^2} Ginv(t0) G(t0 + m) R0^m (u - m),
+                            // R0 = 2^{-2K (u + t0 - T)}: one fp64 Horner pair over the column
+                            const int t0 = pw.n_lo - lo_j;
+                            if (pw.cnt > 0) {
+                                const double u = (double)pw.u_lo;
+                                const double R0 = exp2_64(-2.0 * K64 * (u + (double)(t0 - (La >> 1))));
+                                double P = col[(t0 + pw.cnt - 1) * 32], Pd = 0.0;
+                                for (int m = pw.cnt - 2; m >= 0; --m) {
+                                    Pd = fma(Pd, R0, P);
+                                    P = fma(P, R0, (double)col[(t0 + m) * 32]);
+                                }
+                                g = (double)pw.w * exp2_64(K64 * u * u) * s_tab[4 * t0 + 2] * fma(u, P, -R0 * Pd);
                             }
-                            g = pw.w * part;
                         }
-                        gv[t + h] = g;
+#pragma unroll
+                        for (int hh = 0; hh < LCF_PPS; ++hh)  // static register index (h is a rolled loop)
+                            if (hh == h) gv[t + hh] = g;
                     }
                 }
             }
-            warp_reduce_scatter8(gv, lane, s_g + warp * (STAGE_CELLS * CELL) + gq * GROUP);
+            warp_reduce_scatter8(gv, lane, s_g + warp * (LCF_STAGE * CELL) + gq * GROUP);
         }
         __syncthreads();
-        write_group_partials(s_g, nw, nc, gpart + (int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL);
+        write_group_partials(s_g, nw, nc, gpart + (int64_t)(blockIdx.y + k.grp0) * Mpad + (int64_t)cb * CELL,
+                             LCF_STAGE * CELL);
     }
 }
 
@@ -1290,24 +1356,26 @@ cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
 }
 
 size_t adj_lcf_smem(const gpair_ctx* c) {
-    return (size_t)STAGE_CELLS * CELL * 16 + STAGE_CELLS * GPC * 16 + (size_t)ADJT_WARPS * STAGE_CELLS * CELL * sizeof(gacc_t) +
-           (size_t)2 * c->La * 4 + (size_t)ADJT_WARPS * c->La * 32 * 4;
+    return (size_t)LCF_STAGE * CELL * 16 + LCF_STAGE * GPC * 16 + (size_t)LCF_WARPS * LCF_STAGE * CELL * sizeof(gacc_t) +
+           (size_t)4 * c->La * 8 + (size_t)LCF_WARPS * c->La * 32 * sizeof(lcol_t);
 }
 
 template <int W, int MODE, int SDEG>
 cudaError_t adj_lcf_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, cudaStream_t st) {
-    const int nw = ADJT_WARPS;
+    const int nw = LCF_WARPS;
     const size_t smem = adj_lcf_smem(c);
     cudaError_t e = cudaFuncSetAttribute(k_adjoint_lcf<W, SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int ngroups = (c->Nd + 32 * nw - 1) / (32 * nw);
-    dim3 grid(c->a_regions, c->lng > 0 ? c->lng : ngroups);
+    constexpr int per256 = 256 / (32 * LCF_WARPS);  // adjoint sensor groups per pipeline (256-sensor) group
+    dim3 grid(c->a_regions, c->lng > 0 ? std::min(c->lng * per256, ngroups - c->lg0 * per256) : ngroups);
     OpConst kk = c->k;
-    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
+    kk.grp0 = c->lng > 0 ? c->lg0 * per256 : 0;
+    const double Kln2 = -0.5 * c->k.h * c->k.h / (c->k.sigma * c->k.sigma);  // K ln 2 = -h^2 / (2 sigma^2)
     ++c->n_launch;
-    k_adjoint_lcf<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid, c->d_gtab,
-                                                  c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, kk, c->tab.K,
-                                                  c->tab.m2K);
+    k_adjoint_lcf<W, SDEG><<<grid, 32 * nw, smem, st>>>(c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_a, resid,
+                                                         c->d_gtab, c->d_gpart, c->a_cpr, c->ncells, c->La, c->Mpad, kk,
+                                                         Kln2);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (c->lskip_gather) return cudaSuccess;  // pipelined iterate: launched once after all groups
@@ -1523,10 +1591,13 @@ cudaError_t launch_group_gather(gpair_ctx* c, const gacc_t* gpart, int ngroups, 
 }
 
 cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, cudaStream_t st) {
-    return launch_group_gather(c, c->d_gpart, (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS), mode, ep, st);
+    return launch_group_gather(c, c->d_gpart, adjoint_groups(c), mode, ep, st);
 }
 
-int adjoint_groups(const gpair_ctx* c) { return (c->Nd + 32 * ADJT_WARPS - 1) / (32 * ADJT_WARPS); }
+int adjoint_groups(const gpair_ctx* c) {
+    const int nw = adjoint_kernel(c) == ADJ_LCF ? LCF_WARPS : ADJT_WARPS;
+    return (c->Nd + 32 * nw - 1) / (32 * nw);
+}
 
 cudaError_t launch_count(gpair_ctx* c, cudaStream_t st) {
     cudaError_t e = cudaMemsetAsync(c->d_count, 0, sizeof(unsigned long long), st);

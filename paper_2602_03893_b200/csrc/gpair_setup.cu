@@ -144,13 +144,36 @@ __device__ __forceinline__ bool cell_window(float4 C, float sx, float sy, float 
     return true;
 }
 
+// Exact far-field geometry test of one cell (reading R2): some pair of the cell has
+// r_ij <= k sigma_i, decided with the oracle's fp64 operations (pair_distance:
+// differences of the fp32 inputs, sqrt of the sum of squares, no contraction).
+__device__ bool cell_pairs_too_close(int cc, const float* __restrict__ orig, const int32_t* __restrict__ perm,
+                                     const float4* __restrict__ ksig, int64_t Mpad, float sx, float sy, float sz,
+                                     const OpConst& k) {
+    for (int t = 0; t < CELL; ++t) {
+        const int64_t i = (int64_t)cc * CELL + t;
+        if (perm[i] < 0) continue;  // padding
+        const double dx = __dsub_rn((double)orig[i], (double)sx);
+        const double dy = __dsub_rn((double)orig[Mpad + i], (double)sy);
+        const double dz = __dsub_rn((double)orig[2 * Mpad + i], (double)sz);
+        const double r = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+        const double ks = ksig ? kernel_ks(ksig[i].z, k) : k.ks;
+        if (!(r > ks)) return true;
+    }
+    return false;
+}
+
 // Thread per (region, sensor): union window over the region's cells.
 // check != 0 also performs the geometry check and the anchor-expansion bound.
+// The geometry check is exact: a cell whose bounding sphere comes within k sigma_max
+// of the sensor has its pairs tested one by one (cell_pairs_too_close).
 __global__ void k_region_windows(const float4* __restrict__ cell, const float4* __restrict__ grp, int32_t ncells,
                                  const float* __restrict__ sens, int32_t cpr, int32_t nregions,
                                  OpConst k, int32_t* wlo, int* maxlen, int check, int* geom_bad,
                                  unsigned int* max_eps_bits, unsigned int* rmin_bits = nullptr,
-                                 unsigned int* rmax_bits = nullptr) {
+                                 unsigned int* rmax_bits = nullptr, const float* __restrict__ orig = nullptr,
+                                 const int32_t* __restrict__ perm = nullptr, const float4* __restrict__ ksig = nullptr,
+                                 int64_t Mpad = 0) {
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= (int64_t)nregions * k.Nd) return;
     int j = (int)(t % k.Nd);
@@ -180,7 +203,9 @@ __global__ void k_region_windows(const float4* __restrict__ cell, const float4* 
         if (check) {
             rmin = fminf(rmin, (float)fmax(R - (double)C.w, 0.0));
             rmax = fmaxf(rmax, (float)(R + (double)C.w));
-            if (!k.nf && !(R - (double)C.w > k.ks)) bad = 1;  // near field: any r > 0 (row f4)
+            if (!k.nf && !bad && !(R - (double)C.w > k.ks) &&  // near field: any r > 0 (row f4)
+                cell_pairs_too_close(cc, orig, perm, ksig, Mpad, sx, sy, sz, k))
+                bad = 1;
             for (int gq = 0; gq < GPC; ++gq) {  // anchor-expansion bound per 8-kernel group
                 const float4 G = grp[(int64_t)cc * GPC + gq];
                 double gx = (double)G.x - sx, gy = (double)G.y - sy, gz = (double)G.z - sz;
@@ -385,14 +410,14 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         int64_t nt = (int64_t)nreg * Nd;
         k_region_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(
             c->d_cell, c->d_grp, c->ncells, c->d_sens, cpr, nreg, c->k, wlo, c->d_flags + 2, 1, c->d_flags + 3,
-            (unsigned int*)(c->d_flags + 4), (unsigned int*)(c->d_flags + 8), (unsigned int*)(c->d_flags + 9));
+            (unsigned int*)(c->d_flags + 4), (unsigned int*)(c->d_flags + 8), (unsigned int*)(c->d_flags + 9),
+            c->d_orig, c->d_perm, c->gen ? c->d_ksig : nullptr, c->Mpad);
         SETUP_CHECK(cudaGetLastError());
         SETUP_CHECK(cudaMemcpyAsync(h_flags, c->d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, st));
         SETUP_CHECK(cudaStreamSynchronize(st));
         if (h_flags[3]) {
             cudaFree(wlo);
-            why = "some kernel-sensor distance r_ij <= k*sigma (checked per 32-kernel cell): the far-field "
-                  "Eq. 7 model does not apply";
+            why = "some kernel-sensor distance r_ij <= k*sigma_i: the far-field Eq. 7 model does not apply";
             geom_err = GPAIR_ERR_GEOMETRY;
             return cudaSuccess;
         }
@@ -506,22 +531,25 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
 
     // ---- workspaces
     if (c->ser == 0 || c->ser == SER_FAST5) {  // sensor-lane adjoints (k_adjoint_lcf / _t / _sl) group partials
-        SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 255) / 256) * c->Mpad));
+        SETUP_CHECK(dmalloc(c, &c->d_gpart, (size_t)((Nd + 127) / 128) * c->Mpad));  // 128-sensor groups (LCF)
     }
     if ((c->ser == 0 || c->ser == SER_FAST5) && c->tab.on) {
-        // lane-centred factorisation table G(tau) = 2^{K tau^2}, tau = t - La/2, in fp64
+        // lane-centred factorisation tables (k_adjoint_lcf), fp64, tau = t - La/2:
+        // Q = 2^{-2K tau}, 1/Q, 1/G, G = 2^{K tau^2}
         const double Kd = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
         const int La = c->La, T = La / 2;
         const double tmax = (double)std::max(T, La - T);
-        if (std::fabs(Kd) * tmax * tmax <= 90.0) {
-            std::vector<float> g(2 * (size_t)La);
-            for (int t = 0; t < La; ++t) {
+        if (std::fabs(Kd) * tmax * tmax <= 100.0) {  // column values delta G stay normal fp32
+            std::vector<double> g(4 * (size_t)La);
+            for (int t = 0; t < La; ++t) {  // [t][4] = Q, 1/Q, 1/G, G
                 const double tau = (double)(t - T);
-                g[t] = (float)std::exp2(Kd * tau * tau);
-                g[La + t] = (float)std::exp2(-Kd * tau * tau);
+                g[4 * t] = std::exp2(-2.0 * Kd * tau);
+                g[4 * t + 1] = std::exp2(2.0 * Kd * tau);
+                g[4 * t + 2] = std::exp2(-Kd * tau * tau);
+                g[4 * t + 3] = std::exp2(Kd * tau * tau);
             }
             SETUP_CHECK(dmalloc(c, &c->d_gtab, g.size()));
-            SETUP_CHECK(cudaMemcpyAsync(c->d_gtab, g.data(), g.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+            SETUP_CHECK(cudaMemcpyAsync(c->d_gtab, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice, st));
             SETUP_CHECK(cudaStreamSynchronize(st));
         }
     }

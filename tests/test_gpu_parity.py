@@ -117,6 +117,29 @@ def test_geometry_error():
     assert ei.value.status == gpair.ERR_GEOMETRY
 
 
+@pytest.mark.parametrize("gap", [0.31e-3, 0.305e-3])
+def test_geometry_check_is_exact_per_pair(gap):
+    """A sensor below a 4x4x2 block whose bounding sphere comes within k sigma but whose
+    nearest kernel is at r > k sigma: the oracle accepts it (R2: GEOMETRY only if some
+    r_ij <= k sigma), so the GPU must accept it too and match the oracle; one step
+    closer than k sigma it is rejected."""
+    c = inputs.grid_centers(4, 4, 2, 1e-4)
+    op = dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=64, t0=0.0, k=3.0)
+    s = np.array([[0.0], [0.0], [-0.5e-4 - gap]], np.float32)
+    r = np.sqrt(((c.astype(np.float64) - s.astype(np.float64)) ** 2).sum(0))
+    assert r.min() > 3e-4  # every pair is far (the oracle's test)
+    ctx = make_ctx(c, s, op)
+    x = inputs.dense_amplitudes(c.shape[1])
+    assert_parity(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), "near-cell forward")
+    d = inputs.residual(1, op["n_samples"])
+    assert_parity(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **adj_kw(op)), "near-cell adjoint")
+    ctx.close()
+    s_bad = np.array([[0.05e-3], [0.05e-3], [-0.05e-3 - 0.299e-3]], np.float32)  # r = 0.299 mm to one kernel
+    with pytest.raises(gpair.GpairError) as ei:
+        make_ctx(c, s_bad, op)
+    assert ei.value.status == gpair.ERR_GEOMETRY
+
+
 # ----------------------------------------------------------------- self-consistency
 def test_gpu_dot_test_and_determinism():
     cfg = inputs.CONFIGS["cfg1"]
