@@ -265,7 +265,7 @@ bool pipeline_eligible(const gpair_ctx* c) {
     const int ak = gpair::adjoint_kernel(c);
     return c->pipeline && !c->assa && !c->n_near && c->f_warps == 8 &&
            (ak == gpair::ADJ_LCF || ak == gpair::ADJ_TAB_T || ak == gpair::ADJ_SL) && gpair::adjoint_groups(c) <= 64 &&
-           (c->Nd + 255) / 256 == c->f_sgroups;
+           256 % (32 * (c->f_warps / c->f_split)) == 0;
 }
 
 struct WindowReset {
@@ -840,7 +840,7 @@ gpair_status gpair_iterate(gpair_ctx* c, float* z, float* m, float* v, const flo
             ProfScope ps(c, GPAIR_PROF_GATHER, st);
             API_CUDA(c, gpair::launch_gather(c, z, npc, s->eps_npc, st), "gather");
         }
-        const int G = c->f_sgroups;
+        const int G = (c->Nd + 255) / 256;  // 256-sensor pipeline groups
         for (int g = 0; g < G; ++g) {
             {
                 ProfScope ps(c, GPAIR_PROF_FORWARD, st);

@@ -42,6 +42,7 @@ struct gpair_ctx_s {
 
     // forward decomposition
     int32_t f_cpr = 0, f_regions = 0, f_warps = 0, f_sgroups = 0, Lf = 0;
+    int32_t f_split = 1;  // kernel subsets per sensor warp in k_forward (split accumulation)
     int32_t* d_wlo_f = nullptr;   // [f_regions][Nd] window start (-1 = empty)
     int2* d_rent = nullptr;       // [Nd][f_regions] (window start, region) sorted by start (reducer)
     int32_t jlen_max = 0;         // longest per-sensor live range of the partial windows
@@ -79,7 +80,7 @@ struct gpair_ctx_s {
     // VCR regulariser workspaces (row f2, gpair_vcr.cu), allocated on first use
     int64_t vcr_M = 0, vcr_Mo = 0; // voxels of the u planes / of the own planes
     int32_t vcr_nb = 0;           // per-block partials of the last launch_vcr_slab
-    float* d_vcr_u = nullptr;     // [9][vcr_M] normalised difference fields
+    double* d_vcr_u = nullptr;    // [9][vcr_M] normalised difference fields (fp64)
     double* d_vcr_part = nullptr; // [vcr_nb + 1] per-block fp64 values, then the slab total
     float* d_vcr_g = nullptr;     // [vcr_Mo] dR/dx (caller order)
     float* d_vcr_x = nullptr;     // world > 1: own z planes + halos (NCCL send/recv)

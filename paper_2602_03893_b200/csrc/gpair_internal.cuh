@@ -585,6 +585,23 @@ __device__ __forceinline__ void tab_rs(f2_t uc, const TabConst& t, f2_t& r, f2_t
     s = sub2(C, xS);
 }
 
+// r - 1 and s - 1 (r = exp2(-2K u_c), s = 1/r) for two pairs: the chains P r^m
+// multiply by 1 + eps (FFMA P eps + P), so the fp32 rounding of the multiplier is
+// relative to |eps| <= 0.3 instead of 1 (the "near-1" form; same cost as FMUL)
+__device__ __forceinline__ void tab_rs_eps(f2_t uc, const TabConst& t, f2_t& er, f2_t& es) {
+    const f2_t x = mul2(uc, pk2(t.kappa, t.kappa));
+    const f2_t y = mul2(x, x);
+    f2_t C1 = fma2(y, pk2(1.f / 720.f, 1.f / 720.f), pk2(1.f / 24.f, 1.f / 24.f));
+    C1 = fma2(y, C1, pk2(0.5f, 0.5f));
+    C1 = mul2(y, C1);  // cosh(x) - 1
+    f2_t S = fma2(y, pk2(1.f / 5040.f, 1.f / 5040.f), pk2(1.f / 120.f, 1.f / 120.f));
+    S = fma2(y, S, pk2(1.f / 6.f, 1.f / 6.f));
+    S = fma2(y, S, pk2(1.f, 1.f));
+    const f2_t xS = mul2(x, S);  // sinh(x)
+    er = add2(C1, xS);
+    es = sub2(C1, xS);
+}
+
 // Packed (two pairs) series S(eps) of (sqrt(1+eps)-1)/(eps/2) and T(eps) of
 // (1+eps)^-1/2: degree 2 / 2 (SER 0, |eps| <= EPS_SMALL) or 5 / 4 (SER_FAST5,
 // |eps| <= EPS_FAST) -- the same polynomials as pair_setup<2> / pair_setup<5>.
@@ -608,13 +625,15 @@ __device__ __forceinline__ void series2(f2_t eps, f2_t& S, f2_t& Tw) {
 }
 
 // Forward accumulate of one pair's W samples into its smem column (lane stride
-// 32; ap points at sample n_lo).  P0 = w E; r, s = exp2(-/+2 K u_c).
+// 32; ap points at sample n_lo).  P0 = w E; er, es = r - 1, s - 1 with
+// r, s = exp2(-/+2 K u_c) (tab_rs_eps): every chain step is P (1 + eps).
 template <int W>
-__device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, float s, const TabConst& t) {
+__device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float er, float es, const TabConst& t) {
     constexpr int C = W / 2;
+
     const f2_t U = pk2(uc, uc);
-    f2_t P = pk2(P0, P0 * r);  // (P_0, P_1)
-    const float r2 = r * r;
+    f2_t P = pk2(P0, fmaf(P0, er, P0));  // (P_0, P_1)
+    const float e2 = fmaf(er, er, 2.f * er);  // r^2 - 1
 #pragma unroll
     for (int i = C; i < W; i += 2) {
         const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
@@ -624,10 +643,11 @@ __device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, 
         upk2(acc2, v0, v1);
         ap[i * 32] = v0;
         ap[(i + 1) * 32] = v1;
-        P = mul2(P, pk2(r2, r2));
+        P = fma2(P, pk2(e2, e2), P);
     }
-    const float s2 = s * s;
-    f2_t Pd = pk2(P0 * s2, P0 * s);  // (P_-2, P_-1)
+    const float Pm1 = fmaf(P0, es, P0);
+    const float f2 = fmaf(es, es, 2.f * es);  // s^2 - 1
+    f2_t Pd = pk2(fmaf(Pm1, es, Pm1), Pm1);  // (P_-2, P_-1)
 #pragma unroll
     for (int i = C - 2; i >= 0; i -= 2) {
         const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
@@ -637,7 +657,7 @@ __device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, 
         upk2(acc2, v0, v1);
         ap[i * 32] = v0;
         ap[(i + 1) * 32] = v1;
-        Pd = mul2(Pd, pk2(s2, s2));
+        Pd = fma2(Pd, pk2(f2, f2), Pd);
     }
 }
 

@@ -45,10 +45,53 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
     amp[i] = a;
 }
 
+// fp64 polynomial coefficients in the constant bank (DFMA takes them as c[][] operands
+// instead of two register moves per use): 1/720, 1/24, 1/2, 1/5040, 1/120, 1/6, 1
+__constant__ double kLcfPoly[7] = {1.0 / 720.0, 1.0 / 24.0, 0.5, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0, 1.0};
+// e^{+z} and e^{-z} for |z| <= 0.3: C(z^2) +- z S(z^2), degree 3 in z^2 (truncation < 4e-10,
+// and < 4e-12 at the W = 16 bench constants, |z| <= 0.14)
+__device__ __forceinline__ void exp_pm64(double z, double& ep, double& em) {
+    const double y = z * z;
+    double Cc = fma(y, kLcfPoly[0], kLcfPoly[1]);
+    Cc = fma(y, Cc, kLcfPoly[2]);
+    Cc = fma(y, Cc, kLcfPoly[6]);
+    double Sc = fma(y, kLcfPoly[3], kLcfPoly[4]);
+    Sc = fma(y, Sc, kLcfPoly[5]);
+    Sc = fma(y, Sc, kLcfPoly[6]);
+    const double zs = z * Sc;
+    ep = Cc + zs;
+    em = Cc - zs;
+}
+// e^{z} for -0.13 <= z <= 0: Taylor degree 6 (truncation < 1e-11)
+__device__ __forceinline__ double exp_small64(double z) {
+    double p = fma(z, kLcfPoly[0], kLcfPoly[4]);
+    p = fma(z, p, kLcfPoly[1]);
+    p = fma(z, p, kLcfPoly[5]);
+    p = fma(z, p, kLcfPoly[2]);
+    p = fma(z, p, kLcfPoly[6]);
+    return fma(z, p, kLcfPoly[6]);
+}
+// 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
+__device__ __forceinline__ double exp2_64(double x) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x to an integer
+    const double tn = x + magic;
+    const double n = tn - magic;
+    const double z = (x - n) * 0.6931471805599453;
+    double p = fma(z, 1.0 / 3628800.0, 1.0 / 362880.0);
+    p = fma(z, p, 1.0 / 40320.0);
+    p = fma(z, p, 1.0 / 5040.0);
+    p = fma(z, p, 1.0 / 720.0);
+    p = fma(z, p, 1.0 / 120.0);
+    p = fma(z, p, 1.0 / 24.0);
+    p = fma(z, p, 1.0 / 6.0);
+    p = fma(z, p, 0.5);
+    p = fma(z, p, 1.0);
+    p = fma(z, p, 1.0);
+    const int ni = __double2loint(tn);  // low word of x + magic = n (two's complement)
+    return p * __hiloint2double((ni + 1023) << 20, 0);
+}
+
 // ------------------------------------------------------------------ forward
-#ifndef GPAIR_FWD_EXP
-#define GPAIR_FWD_EXP 0
-#endif
 #ifndef GPAIR_FWD_MINB
 #define GPAIR_FWD_MINB 3
 #endif
@@ -127,7 +170,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
                                                  float* __restrict__ partial, int32_t cpr, int32_t ncells,
                                                  int32_t Lf, int64_t Mpad, OpConst k,
-                                                 const float4* __restrict__ ksig, const TabConst tab) {
+                                                 const float4* __restrict__ ksig, const TabConst tab, int32_t split) {
     constexpr bool GEN = SER == SER_GEN;
     // two pairs per setup in f32x2 (exact-integer window length): degree-2 or degree-5 series
     constexpr bool FAST = SER == 0 || SER == SER_FAST5;
@@ -150,12 +193,18 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     float* s_kxy = (float*)s_kd;
     float* s_kzw = s_kxy + STAGE_CELLS * CELL * 2;
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // split-accumulation: the CTA's warps are nsw sensor warps x split kernel subsets; warp
+    // (q, sw) accumulates every split-th 8-kernel group of the region for the 32 sensors of
+    // sensor warp sw into its own column, and the split columns are summed before the flush:
+    // fp32 accumulation chains split times shorter (forward accuracy)
+    const int nsw = nw / split, sw = warp % nsw, q = warp / nsw;
+    const double Kln2 = -0.5 * k.h * k.h / (k.sigma * k.sigma);  // K ln 2 of E = 2^{K u^2}
     float* s_acc = (DBUF ? (float*)smem4 + 2 * FWD_BUF : (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0))) +
                    (size_t)warp * Lf * 32;
     float* s_acc_lane = s_acc + lane;
 
     const int region = blockIdx.x;
-    const int jbase = ((blockIdx.y + k.grp0) * nw + warp) * 32;
+    const int jbase = ((blockIdx.y + k.grp0) * nsw + sw) * 32;
     const int j = jbase + lane;
     const bool jok = j < k.Nd;
     for (int t = lane; t < Lf * 32; t += 32) s_acc[t] = 0.f;
@@ -216,8 +265,10 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
             if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
         }
         __syncthreads();
-        for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
-            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
+        for (int gq = q; gq < nc * GPC && lo_j >= 0; gq += split) {
+            double invR64;
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k, &invR64);
+            const double h2R64 = 0.5 * k.h * invR64;
             if constexpr (FAST) {
                 if (!__any_sync(__activemask(), a.na == NA_EXACT)) {
                     // Two pairs per step: pair_fast's arithmetic in f32x2 (bit-identical
@@ -257,48 +308,25 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                         const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
                         const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
                         if (!(bad0 || bad1)) {
-#if GPAIR_FWD_EXP
-                            if (true) {  // numerics experiment (see GPAIR_LCF_EXP): exact fp64 pair values
-                                const float4 Cg = s_grp[gq];
-                                const double dxa = (double)Cg.x - sx, dya = (double)Cg.y - sy, dza = (double)Cg.z - sz;
-                                const double Ra = sqrt(dxa * dxa + dya * dya + dza * dza);
-                                const double tfa = fma(Ra, k.inv_h, -k.t0fs);
-                                const double K64 = -1.4426950408889634 * k.h * k.h / (2.0 * k.sigma * k.sigma);
-                                float Aa, Ab;
-                                upk2(A2, Aa, Ab);
-#pragma unroll
-                                for (int hh = 0; hh < 2; ++hh) {
-                                    const int lk = li + hh;
-                                    const int pb = (lk >> 1) * 4 + (lk & 1);
-                                    const double ex = s_kxy[pb], ey = s_kxy[pb + 2], ez = s_kzw[pb];
-                                    float e32a, e32b, u32a, u32b;
-                                    upk2(eu, e32a, e32b);
-                                    upk2(ulo, u32a, u32b);
-                                    const float e32 = hh ? e32b : e32a, u32 = hh ? u32b : u32a;
-                                    const double flp1 = (double)(e32 - u32);
-                                    const double q = 2.0 * (dxa * ex + dya * ey + dza * ez) + (ex * ex + ey * ey + ez * ez);
-                                    const double off = q / (Ra + sqrt(Ra * Ra + q));
-                                    const double r = Ra + off;
-                                    const double u0 = GPAIR_FWD_EXP == 2 ? (tfa - (double)a.na) + off * k.inv_h - flp1
-                                                                         : (double)u32;
-                                    const double wA = (double)(hh ? Ab : Aa) * 0.5 * k.h / r;
-                                    float* ap = s_acc_lane + (hh ? n1 : n0) * 32;
-                                    for (int mm = 0; mm < WMAX; ++mm) {
-                                        const double u = u0 - mm;
-                                        ap[mm * 32] += (float)(wA * u * exp2(K64 * u * u));
-                                    }
-                                }
-                            } else
-#endif
                             if (TABW && tab.on) {
                                 // u_c = u_lo - C (exact), E = exp2(K u_c^2), r = exp2(-2K u_c), s = 1/r
                                 const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
                                 f2_t r2, s2;
-                                tab_rs(uc, tab, r2, s2);
-                                float e0, e1, uc0, uc1, p0, p1, r0, r1, q0, q1;
-                                upk2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), e0, e1);
-                                upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), p0, p1);
+                                tab_rs_eps(uc, tab, r2, s2);  // r - 1, s - 1
+                                float uc0, uc1, p0, p1, r0, r1, q0, q1;
                                 upk2(uc, uc0, uc1);
+                                {
+                                    // per-pair scale A h / (2r) 2^{K u_c^2} in fp64: its fp32 roundings
+                                    // (h/2R, T(eps), E, the products) were a per-pair error of ~2 ulp
+                                    // that the cancelling sums of cfg5 amplify
+                                    float Aa, Ab, ta, tb;
+                                    upk2(A2, Aa, Ab);
+                                    upk2(sub2(Tw, one), ta, tb);  // T(eps) - 1, exact
+                                    p0 = (float)((double)Aa * fma(h2R64, (double)ta, h2R64) *
+                                                 exp_small64(Kln2 * (double)uc0 * (double)uc0));
+                                    p1 = (float)((double)Ab * fma(h2R64, (double)tb, h2R64) *
+                                                 exp_small64(Kln2 * (double)uc1 * (double)uc1));
+                                }
                                 upk2(r2, r0, r1);
                                 upk2(s2, q0, q1);
                                 acc_tab<TABW ? WMAX : 4>(s_acc_lane + n0 * 32, uc0, p0, r0, q0, tab);
@@ -353,6 +381,17 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                 acc_pair<WMAX>(s_acc_lane, lo_j, p, K1);
             }
         }
+    }
+    if (split > 1) {  // sum the split columns of each sensor warp into q = 0's, in fixed order
+        __syncthreads();
+        float* base = s_acc - (size_t)warp * Lf * 32;  // column of warp 0
+        for (int r = q; r < Lf; r += split) {
+            float v = 0.f;
+            for (int qq = 0; qq < split; ++qq) v += base[((size_t)(qq * nsw + sw) * Lf + r) * 32 + lane];
+            base[((size_t)sw * Lf + r) * 32 + lane] = v;
+        }
+        __syncthreads();
+        if (q != 0) return;
     }
     __syncwarp();
     // flush: per 32-row block, in-place XOR-swizzled transpose then coalesced stores
@@ -895,52 +934,6 @@ typedef float lcol_t;
 typedef double lcol_t;
 #endif
 
-// fp64 polynomial coefficients in the constant bank (DFMA takes them as c[][] operands
-// instead of two register moves per use): 1/720, 1/24, 1/2, 1/5040, 1/120, 1/6, 1
-__constant__ double kLcfPoly[7] = {1.0 / 720.0, 1.0 / 24.0, 0.5, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0, 1.0};
-// e^{+z} and e^{-z} for |z| <= 0.3: C(z^2) +- z S(z^2), degree 3 in z^2 (truncation < 4e-10,
-// and < 4e-12 at the W = 16 bench constants, |z| <= 0.14)
-__device__ __forceinline__ void exp_pm64(double z, double& ep, double& em) {
-    const double y = z * z;
-    double Cc = fma(y, kLcfPoly[0], kLcfPoly[1]);
-    Cc = fma(y, Cc, kLcfPoly[2]);
-    Cc = fma(y, Cc, kLcfPoly[6]);
-    double Sc = fma(y, kLcfPoly[3], kLcfPoly[4]);
-    Sc = fma(y, Sc, kLcfPoly[5]);
-    Sc = fma(y, Sc, kLcfPoly[6]);
-    const double zs = z * Sc;
-    ep = Cc + zs;
-    em = Cc - zs;
-}
-// e^{z} for -0.13 <= z <= 0: Taylor degree 6 (truncation < 1e-11)
-__device__ __forceinline__ double exp_small64(double z) {
-    double p = fma(z, kLcfPoly[0], kLcfPoly[4]);
-    p = fma(z, p, kLcfPoly[1]);
-    p = fma(z, p, kLcfPoly[5]);
-    p = fma(z, p, kLcfPoly[2]);
-    p = fma(z, p, kLcfPoly[6]);
-    return fma(z, p, kLcfPoly[6]);
-}
-// 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
-__device__ __forceinline__ double exp2_64(double x) {
-    const double magic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x to an integer
-    const double tn = x + magic;
-    const double n = tn - magic;
-    const double z = (x - n) * 0.6931471805599453;
-    double p = fma(z, 1.0 / 3628800.0, 1.0 / 362880.0);
-    p = fma(z, p, 1.0 / 40320.0);
-    p = fma(z, p, 1.0 / 5040.0);
-    p = fma(z, p, 1.0 / 720.0);
-    p = fma(z, p, 1.0 / 120.0);
-    p = fma(z, p, 1.0 / 24.0);
-    p = fma(z, p, 1.0 / 6.0);
-    p = fma(z, p, 0.5);
-    p = fma(z, p, 1.0);
-    p = fma(z, p, 1.0);
-    const int ni = __double2loint(tn);  // low word of x + magic = n (two's complement)
-    return p * __hiloint2double((ni + 1023) << 20, 0);
-}
-
 template <int W, int SDEG>
 __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
     k_adjoint_lcf(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
@@ -1303,13 +1296,15 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
                   (size_t)c->f_warps * c->Lf * 32 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid(c->f_regions, c->lng > 0 ? c->lng : c->f_sgroups);  // lng / lg0: sensor-group window (pipeline)
+    // lng / lg0: window of 256-sensor pipeline groups; one CTA covers 32 f_warps / f_split sensors
+    const int per256 = 256 / (32 * (c->f_warps / c->f_split));
+    dim3 grid(c->f_regions, c->lng > 0 ? std::min(c->lng * per256, c->f_sgroups - c->lg0 * per256) : c->f_sgroups);
     OpConst kk = c->k;
-    kk.grp0 = c->lng > 0 ? c->lg0 : 0;
+    kk.grp0 = c->lng > 0 ? c->lg0 * per256 : 0;
     ++c->n_launch;
     k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
-                                                      c->Mpad, kk, c->d_ksig, c->tab);
+                                                      c->Mpad, kk, c->d_ksig, c->tab, c->f_split);
     return cudaGetLastError();
 }
 

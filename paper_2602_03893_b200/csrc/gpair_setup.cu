@@ -390,8 +390,18 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     // ---- forward regions: sized for >= ~4 CTAs per SM of work and smem fit
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
-    c->f_warps = std::min(c->assa ? assa_forward_warps() : 8, (Nd + 31) / 32);
-    c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
+    if (c->assa) {
+        c->f_warps = std::min(assa_forward_warps(), (Nd + 31) / 32);
+        c->f_split = 1;
+    } else {  // 8 warps = nsw sensor warps x f_split kernel subsets (split accumulation, k_forward)
+        int split = 4;
+        if (const char* ev = std::getenv("GPAIR_FWD_SPLIT")) split = std::max(1, std::min(8, atoi(ev)));
+        while (8 % split) --split;
+        const int nsw = std::min(8 / split, (Nd + 31) / 32);
+        c->f_warps = 8;
+        c->f_split = 8 / nsw;
+    }
+    c->f_sgroups = (Nd + 32 * (c->f_warps / c->f_split) - 1) / (32 * (c->f_warps / c->f_split));
     int cpr = 16;  // 512 kernels (8x8x8 on a grid): bounds fp32 accumulation chains
     bool cpr_forced = false;
     if (const char* ev = std::getenv("GPAIR_FWD_CPR")) {  // A/B experiments

@@ -7,7 +7,9 @@
 //   D_pp  [1,-2,1] on the nearest interior stencil (centre clamp(i,1,n-2))
 //   D_pq  forward-forward cross difference, 0 on the last index of p or q,
 //         counted twice (ordered pairs pq and qp)
-// Two passes, both one thread per voxel, deterministic:
+// Two passes, both one thread per voxel, deterministic, in fp64 (the differences
+// of fp32 inputs are then exact, and the cancelling adjoint gathers of flat image
+// regions keep the gradient's elementwise error at the 1e-4 gate of SURVEY 8c):
 //   k_vcr_terms  differences, s_H, s_TV, the 9 normalised fields
 //                u = (D_d x / s_TV, D_pp x / s_H, 2 D_pq x / s_H) and fp64
 //                per-block partial values (fixed-order reduction later)
@@ -36,14 +38,14 @@ struct Grid {
     int zo0, zo1;    // own planes (values and gradients)
 };
 
-__device__ __forceinline__ float xval(const float* __restrict__ src, int npc, float eps_npc, int i) {
-    const float v = src[i];
+__device__ __forceinline__ double xval(const float* __restrict__ src, int npc, float eps_npc, int i) {
+    const double v = src[i];
     return npc ? (v + eps_npc) * (v + eps_npc) : v;  // x = (z + eps)^2 (Eq. 18) when the state is z
 }
 
 // u is [9][M] over the planes [zu0, zu0 + M / (nx ny)).
 __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_npc, Grid G, float beta, float eps,
-                            float* __restrict__ u, int64_t M, double* __restrict__ part) {
+                            double* __restrict__ u, int64_t M, double* __restrict__ part) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     double val = 0.0;
     if (i < M) {
@@ -55,42 +57,42 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
         const int sy = G.nx, sz = G.nx * G.ny;
         const float* xc = src + ((int64_t)(iz - G.zb) * sz + (int64_t)iy * sy + ix);
         auto at = [&](int a, int b, int c) { return xval(xc, npc, eps_npc, (a - ix) + (b - iy) * sy + (c - iz) * sz); };
-        const float x0 = at(ix, iy, iz);
+        const double x0 = at(ix, iy, iz);
         // forward differences (V1)
         const int xp = min(ix + 1, G.nx - 1), yp = min(iy + 1, G.ny - 1), zp = min(iz + 1, G.nz - 1);
-        const float dx = at(xp, iy, iz) - x0, dy = at(ix, yp, iz) - x0, dz = at(ix, iy, zp) - x0;
+        const double dx = at(xp, iy, iz) - x0, dy = at(ix, yp, iz) - x0, dz = at(ix, iy, zp) - x0;
         // pure second differences on the nearest interior stencil (V2)
-        float dxx = 0.f, dyy = 0.f, dzz = 0.f;
+        double dxx = 0.0, dyy = 0.0, dzz = 0.0;
         if (G.nx >= 3) {
             const int c = min(max(ix, 1), G.nx - 2);
-            dxx = at(c + 1, iy, iz) - 2.f * at(c, iy, iz) + at(c - 1, iy, iz);
+            dxx = at(c + 1, iy, iz) - 2.0 * at(c, iy, iz) + at(c - 1, iy, iz);
         }
         if (G.ny >= 3) {
             const int c = min(max(iy, 1), G.ny - 2);
-            dyy = at(ix, c + 1, iz) - 2.f * at(ix, c, iz) + at(ix, c - 1, iz);
+            dyy = at(ix, c + 1, iz) - 2.0 * at(ix, c, iz) + at(ix, c - 1, iz);
         }
         if (G.nz >= 3) {
             const int c = min(max(iz, 1), G.nz - 2);
-            dzz = at(ix, iy, c + 1) - 2.f * at(ix, iy, c) + at(ix, iy, c - 1);
+            dzz = at(ix, iy, c + 1) - 2.0 * at(ix, iy, c) + at(ix, iy, c - 1);
         }
         // mixed forward-forward differences (V3), 0 on the last index of either axis
-        const float dxy = (ix < G.nx - 1 && iy < G.ny - 1) ? at(ix + 1, iy + 1, iz) - at(ix + 1, iy, iz) - at(ix, iy + 1, iz) + x0 : 0.f;
-        const float dxz = (ix < G.nx - 1 && iz < G.nz - 1) ? at(ix + 1, iy, iz + 1) - at(ix + 1, iy, iz) - at(ix, iy, iz + 1) + x0 : 0.f;
-        const float dyz = (iy < G.ny - 1 && iz < G.nz - 1) ? at(ix, iy + 1, iz + 1) - at(ix, iy + 1, iz) - at(ix, iy, iz + 1) + x0 : 0.f;
-        const float stv = sqrtf(dx * dx + dy * dy + dz * dz + eps);
-        const float sh =
-            sqrtf(dxx * dxx + dyy * dyy + dzz * dzz + 2.f * (dxy * dxy + dxz * dxz + dyz * dyz) + eps);
-        const float itv = 1.f / stv, ih = 1.f / sh;
+        const double dxy = (ix < G.nx - 1 && iy < G.ny - 1) ? at(ix + 1, iy + 1, iz) - at(ix + 1, iy, iz) - at(ix, iy + 1, iz) + x0 : 0.0;
+        const double dxz = (ix < G.nx - 1 && iz < G.nz - 1) ? at(ix + 1, iy, iz + 1) - at(ix + 1, iy, iz) - at(ix, iy, iz + 1) + x0 : 0.0;
+        const double dyz = (iy < G.ny - 1 && iz < G.nz - 1) ? at(ix, iy + 1, iz + 1) - at(ix, iy + 1, iz) - at(ix, iy, iz + 1) + x0 : 0.0;
+        const double stv = sqrt(dx * dx + dy * dy + dz * dz + eps);
+        const double sh =
+            sqrt(dxx * dxx + dyy * dyy + dzz * dzz + 2.0 * (dxy * dxy + dxz * dxz + dyz * dyz) + eps);
+        const double itv = 1.0 / stv, ih = 1.0 / sh;
         u[0 * M + i] = dx * itv;
         u[1 * M + i] = dy * itv;
         u[2 * M + i] = dz * itv;
         u[3 * M + i] = dxx * ih;
         u[4 * M + i] = dyy * ih;
         u[5 * M + i] = dzz * ih;
-        u[6 * M + i] = 2.f * dxy * ih;
-        u[7 * M + i] = 2.f * dxz * ih;
-        u[8 * M + i] = 2.f * dyz * ih;
-        if (iz >= G.zo0 && iz < G.zo1) val = (double)sh + (double)beta * (double)stv;
+        u[6 * M + i] = 2.0 * dxy * ih;
+        u[7 * M + i] = 2.0 * dxz * ih;
+        u[8 * M + i] = 2.0 * dyz * ih;
+        if (iz >= G.zo0 && iz < G.zo1) val = sh + (double)beta * stv;
     }
     __shared__ double s_red[32];
     for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
@@ -107,16 +109,16 @@ __global__ void k_vcr_terms(const float* __restrict__ src, int npc, float eps_np
 // U(m) of a pure second difference along one axis: the sum of u over the
 // voxels whose clamped centre is m (m in [1, n-2]); up points at this voxel
 // (coordinate a on the axis), offsets are 32-bit.
-__device__ __forceinline__ float fold_pp(const float* __restrict__ up, int a, int stride, int c, int n) {
-    if (c < 1 || c > n - 2) return 0.f;
-    float s = up[(c - a) * stride];
+__device__ __forceinline__ double fold_pp(const double* __restrict__ up, int a, int stride, int c, int n) {
+    if (c < 1 || c > n - 2) return 0.0;
+    double s = up[(c - a) * stride];
     if (c == 1) s += up[-a * stride];                      // voxel 0 uses centre 1
     if (c == n - 2) s += up[(n - 1 - a) * stride];         // voxel n-1 uses centre n-2
     return s;
 }
 
 // u: [9][M] over the planes from zu0; g: [Mo] over the own planes.
-__global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int64_t M, int64_t Mo,
+__global__ void k_vcr_grad(const double* __restrict__ u, Grid G, float beta, int64_t M, int64_t Mo,
                            float* __restrict__ g) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= Mo) return;
@@ -125,33 +127,33 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
     const int ix = (int)((unsigned)j - q * (unsigned)G.nx), iy = (int)(q % (unsigned)G.ny),
               iz = G.zo0 + (int)(q / (unsigned)G.ny);
     const int64_t i = j + (int64_t)(G.zo0 - G.zu0) * sz;  // index into u
-    const float* ux = u + i;  // fields at this voxel; neighbours by 32-bit offsets
-    const float* uy = u + M + i;
-    const float* uz = u + 2 * M + i;
+    const double* ux = u + i;  // fields at this voxel; neighbours by 32-bit offsets
+    const double* uy = u + M + i;
+    const double* uz = u + 2 * M + i;
     // TV: (D_d^T u)(k) = u(k - e_d) [k_d >= 1] - u(k)   (u = 0 on the last index)
-    float gtv = -(ux[0] + uy[0] + uz[0]);
+    double gtv = -(ux[0] + uy[0] + uz[0]);
     if (ix >= 1) gtv += ux[-sx];
     if (iy >= 1) gtv += uy[-sy];
     if (iz >= 1) gtv += uz[-sz];
     // pure second differences: g(k) = U(k-1) - 2 U(k) + U(k+1) along each axis
     // (the z fold may reach global plane 0 / NZ-1; those lie inside u when read)
-    float gh = 0.f;
+    double gh = 0.0;
     {
-        const float* up = u + 3 * M + i;
-        if (G.nx >= 3) gh += fold_pp(up, ix, sx, ix - 1, G.nx) - 2.f * fold_pp(up, ix, sx, ix, G.nx) + fold_pp(up, ix, sx, ix + 1, G.nx);
+        const double* up = u + 3 * M + i;
+        if (G.nx >= 3) gh += fold_pp(up, ix, sx, ix - 1, G.nx) - 2.0 * fold_pp(up, ix, sx, ix, G.nx) + fold_pp(up, ix, sx, ix + 1, G.nx);
     }
     {
-        const float* up = u + 4 * M + i;
-        if (G.ny >= 3) gh += fold_pp(up, iy, sy, iy - 1, G.ny) - 2.f * fold_pp(up, iy, sy, iy, G.ny) + fold_pp(up, iy, sy, iy + 1, G.ny);
+        const double* up = u + 4 * M + i;
+        if (G.ny >= 3) gh += fold_pp(up, iy, sy, iy - 1, G.ny) - 2.0 * fold_pp(up, iy, sy, iy, G.ny) + fold_pp(up, iy, sy, iy + 1, G.ny);
     }
     {
-        const float* up = u + 5 * M + i;
-        if (G.nz >= 3) gh += fold_pp(up, iz, sz, iz - 1, G.nz) - 2.f * fold_pp(up, iz, sz, iz, G.nz) + fold_pp(up, iz, sz, iz + 1, G.nz);
+        const double* up = u + 5 * M + i;
+        if (G.nz >= 3) gh += fold_pp(up, iz, sz, iz - 1, G.nz) - 2.0 * fold_pp(up, iz, sz, iz, G.nz) + fold_pp(up, iz, sz, iz + 1, G.nz);
     }
     // mixed: taps (+1 at (a+1,b+1), -1 at (a+1,b), -1 at (a,b+1), +1 at (a,b)),
     // u = 0 where the forward operator is 0, so only existence checks remain
-    auto mixed_T = [&](const float* um, int a, int sa, int b, int sb) {
-        float s = um[0];
+    auto mixed_T = [&](const double* um, int a, int sa, int b, int sb) {
+        double s = um[0];
         if (a >= 1 && b >= 1) s += um[-sa - sb];
         if (a >= 1) s -= um[-sa];
         if (b >= 1) s -= um[-sb];
@@ -160,7 +162,7 @@ __global__ void k_vcr_grad(const float* __restrict__ u, Grid G, float beta, int6
     gh += mixed_T(u + 6 * M + i, ix, sx, iy, sy);
     gh += mixed_T(u + 7 * M + i, ix, sx, iz, sz);
     gh += mixed_T(u + 8 * M + i, iy, sy, iz, sz);
-    g[j] = gh + beta * gtv;
+    g[j] = (float)(gh + (double)beta * gtv);
 }
 
 __global__ void k_vcr_sum(const double* __restrict__ part, int n, float* __restrict__ value,
@@ -193,13 +195,13 @@ cudaError_t vcr_ensure(gpair_ctx* c, int64_t Mu, int64_t Mo) {
     c->vcr_M = c->vcr_Mo = 0;
     const int nb = vcr_blocks(Mu);
     // d_vcr_part carries one extra double: the (all-reduced) total of a slab
-    cudaError_t e = cudaMalloc(&c->d_vcr_u, sizeof(float) * 9 * (size_t)Mu);
+    cudaError_t e = cudaMalloc(&c->d_vcr_u, sizeof(double) * 9 * (size_t)Mu);
     if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_part, sizeof(double) * (nb + 1));
     if (e == cudaSuccess) e = cudaMalloc(&c->d_vcr_g, sizeof(float) * (size_t)Mo);
     if (e == cudaSuccess) {
         c->vcr_M = Mu;
         c->vcr_Mo = Mo;
-        c->workspace_bytes += (int64_t)(sizeof(float) * (9 * Mu + Mo) + sizeof(double) * (nb + 1));
+        c->workspace_bytes += (int64_t)(sizeof(double) * 9 * Mu + sizeof(float) * Mo + sizeof(double) * (nb + 1));
     }
     return e;
 }

@@ -14,7 +14,7 @@ import oracle  # noqa: E402
 from oracle import ir  # noqa: E402
 from paper_2602_03893_b200 import gpair, inputs  # noqa: E402
 
-from tests_common import T, assert_parity, dev  # noqa: E402
+from tests_common import T, assert_parity, assert_state_update, dev  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -151,4 +151,4 @@ def test_iterate_general_teacher_forced(mode):
         z_ref, _, _ = ir.adam_update(z0.astype(np.float64), m0.astype(np.float64), v0.astype(np.float64), gz, lr, 3, hp)
     else:
         z_ref = np.maximum(z0 - lr * gz, 0.0)
-    assert_parity(zt.cpu().numpy() - z0, z_ref - z0, "general iterate step")
+    assert_state_update(zt.cpu().numpy(), z0, z_ref, "general iterate step")

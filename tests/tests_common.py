@@ -46,6 +46,25 @@ def assert_parity(got, ref, what):
     return rel, elem
 
 
+def assert_state_update(z_new, z0, z_ref, what):
+    """One-step state update z' (Adam or clamp) from z0: the gate on z' itself (SURVEY 8c:
+    "the one-step z'"), and rel L2 <= REL_L2 on the step z' - z0 where the fp32 state can
+    resolve it.  The step is not gated elementwise: z' carries ulp(z)/2 ~ 3e-8 of rounding,
+    ~3e-4 of the smallest gated Adam steps (1e-3 of the largest) whatever the arithmetic."""
+    assert_parity(z_new, z_ref, what)
+    step, step_ref = np.asarray(z_new, np.float64) - z0, np.asarray(z_ref, np.float64) - z0
+    # the fp32 state resolves the step to ~2^-24 |z'| (rms); below REL_L2 of that the step is
+    # not representable (e.g. clamp steps with the 2/N gradient scale) and z' is the gate
+    quant = 2.0 ** -24 * np.sqrt(np.mean(np.asarray(z_ref, np.float64) ** 2))
+    rms = np.sqrt(np.mean(step_ref ** 2))
+    if rms < quant / REL_L2:
+        print(f"{what}: step rms {rms:.2e} below the fp32 state's resolution; gated through z'")
+        return
+    rel = np.linalg.norm(step - step_ref) / np.linalg.norm(step_ref)
+    print(f"{what} (step z' - z0): rel L2 {rel:.2e}")
+    assert rel <= REL_L2, f"{what} step: rel L2 {rel:.3e} > {REL_L2}"
+
+
 def sample_rows(n_sensors, n=N_ROWS, seed=5):
     """Sorted sensor subset for full-size forward parity (first, last and random rows)."""
     if n_sensors <= n:
