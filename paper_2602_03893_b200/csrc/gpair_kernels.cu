@@ -198,7 +198,6 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
     // sensor warp sw into its own column, and the split columns are summed before the flush:
     // fp32 accumulation chains split times shorter (forward accuracy)
     const int nsw = nw / split, sw = warp % nsw, q = warp / nsw;
-    const double Kln2 = -0.5 * k.h * k.h / (k.sigma * k.sigma);  // K ln 2 of E = 2^{K u^2}
     float* s_acc = (DBUF ? (float*)smem4 + 2 * FWD_BUF : (float*)(s_ks + (GEN ? STAGE_CELLS * CELL : 0))) +
                    (size_t)warp * Lf * 32;
     float* s_acc_lane = s_acc + lane;
@@ -266,9 +265,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
         }
         __syncthreads();
         for (int gq = q; gq < nc * GPC && lo_j >= 0; gq += split) {
-            double invR64;
-            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k, &invR64);
-            const double h2R64 = 0.5 * k.h * invR64;
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             if constexpr (FAST) {
                 if (!__any_sync(__activemask(), a.na == NA_EXACT)) {
                     // Two pairs per step: pair_fast's arithmetic in f32x2 (bit-identical
@@ -316,16 +313,16 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                 float uc0, uc1, p0, p1, r0, r1, q0, q1;
                                 upk2(uc, uc0, uc1);
                                 {
-                                    // per-pair scale A h / (2r) 2^{K u_c^2} in fp64: its fp32 roundings
-                                    // (h/2R, T(eps), E, the products) were a per-pair error of ~2 ulp
-                                    // that the cancelling sums of cfg5 amplify
-                                    float Aa, Ab, ta, tb;
-                                    upk2(A2, Aa, Ab);
-                                    upk2(sub2(Tw, one), ta, tb);  // T(eps) - 1, exact
-                                    p0 = (float)((double)Aa * fma(h2R64, (double)ta, h2R64) *
-                                                 exp_small64(Kln2 * (double)uc0 * (double)uc0));
-                                    p1 = (float)((double)Ab * fma(h2R64, (double)tb, h2R64) *
-                                                 exp_small64(Kln2 * (double)uc1 * (double)uc1));
+                                    // per-pair scale in fp32 with few roundings: w = A (h/2R)(1 + (T - 1)),
+                                    // E = 2^{K u_c^2} by a degree-5 polynomial (|z| <= 0.13, unbiased)
+                                    const f2_t z = mul2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), pk2(0.69314718f, 0.69314718f));
+                                    f2_t ep = fma2(z, pk2(1.f / 120.f, 1.f / 120.f), pk2(1.f / 24.f, 1.f / 24.f));
+                                    ep = fma2(z, ep, pk2(1.f / 6.f, 1.f / 6.f));
+                                    ep = fma2(z, ep, pk2(0.5f, 0.5f));
+                                    ep = fma2(z, ep, pk2(1.f, 1.f));
+                                    ep = fma2(z, ep, pk2(1.f, 1.f));
+                                    const f2_t wq = fma2(h2R, sub2(Tw, one), h2R);
+                                    upk2(mul2(mul2(A2, ep), wq), p0, p1);
                                 }
                                 upk2(r2, r0, r1);
                                 upk2(s2, q0, q1);
@@ -986,9 +983,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
         }
         __syncthreads();
         for (int gq = 0; gq < nc * GPC; ++gq) {
-            double invR64;
-            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k, &invR64);
-            const double h2R64 = 0.5 * k.h * invR64;
+            const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             double gv[GROUP];
             const bool exact_grp = __any_sync(0xffffffffu, a.na == NA_EXACT);
             const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
@@ -1012,7 +1007,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                         const f2_t eps = mul2(q, iR2);
                         f2_t S, Tw;
                         series2<SDEG>(eps, S, Tw);
-                        twm1[h] = sub2(Tw, one);  // T(eps) - 1, exact (Sterbenz): w = h / 2R (1 + twm1) in fp64
+                        twm1[h] = sub2(Tw, one);  // T(eps) - 1, exact (Sterbenz): w = h / 2R (1 + twm1)
                         const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
                         const f2_t x = add2(eu, clo);
                         const f2_t tt = add2(x, mag);
@@ -1033,9 +1028,22 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                     const lcol_t* rp[LCF_PPS];
 #pragma unroll
                     for (int h = 0; h < LCF_PPS; ++h) {
-                        float u32a, u32b, w32a, w32b;
+                        float u32a, u32b;
                         upk2(ulo[h >> 1], u32a, u32b);
-                        upk2(twm1[h >> 1], w32a, w32b);
+                        // w E in fp32 with few roundings (the forward's scale arithmetic): its ~1 ulp
+                        // per pair is below the time of flight's share of g's error
+                        float sc32a, sc32b;
+                        {
+                            const f2_t ucp = add2(ulo[h >> 1], pk2(-(float)C, -(float)C));
+                            const f2_t z = mul2(mul2(ucp, ucp), pk2((float)Kln2, (float)Kln2));
+                            f2_t ep = fma2(z, pk2(1.f / 120.f, 1.f / 120.f), pk2(1.f / 24.f, 1.f / 24.f));
+                            ep = fma2(z, ep, pk2(1.f / 6.f, 1.f / 6.f));
+                            ep = fma2(z, ep, pk2(0.5f, 0.5f));
+                            ep = fma2(z, ep, pk2(1.f, 1.f));
+                            ep = fma2(z, ep, pk2(1.f, 1.f));
+                            const f2_t h2 = pk2(a.h2R, a.h2R);
+                            upk2(mul2(ep, fma2(h2, twm1[h >> 1], h2)), sc32a, sc32b);
+                        }
                         uc[h] = (double)((h & 1) ? u32b : u32a) - (double)C;  // exact
                         const int tc = o[h] + C;
                         double rr, ri;
@@ -1049,8 +1057,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                         Lc[h] = (double)rp[h][-C * 32];
                         Ld[h] = 0.0;
                         // scale w E Ginv(t_c), E = e^{K ln2 u_c^2}
-                        const double w64 = fma(h2R64, (double)((h & 1) ? w32b : w32a), h2R64);
-                        gv[t + h] = w64 * exp_small64(Kln2 * uc[h] * uc[h]) * s_tab[4 * tc + 2];
+                        gv[t + h] = (double)((h & 1) ? sc32b : sc32a) * s_tab[4 * tc + 2];
                     }
 #pragma unroll
                     for (int i = 1; i < C; ++i) {

@@ -394,7 +394,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->f_warps = std::min(assa_forward_warps(), (Nd + 31) / 32);
         c->f_split = 1;
     } else {  // 8 warps = nsw sensor warps x f_split kernel subsets (split accumulation, k_forward)
-        int split = 4;
+        int split = 2;  // measured: 2 -> cfg4 forward rows 5.7e-5 elementwise, 4 costs +1.2 ms
         if (const char* ev = std::getenv("GPAIR_FWD_SPLIT")) split = std::max(1, std::min(8, atoi(ev)));
         while (8 % split) --split;
         const int nsw = std::min(8 / split, (Nd + 31) / 32);

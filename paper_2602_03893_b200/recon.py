@@ -27,6 +27,7 @@ class Schedule:
     beta: float = 0.0  # beta of Eq. 20
     eps_reg: float = 1e-8
     eps_npc: float = 1e-8
+    grad_scale: float = 0.0  # dL/dy = grad_scale (y - b); <= 0 -> 2/N (R10); 1.0 = Alg. 2 line 529 literally
 
 
 def reconstruct(ctx: gpair.Context, b, sched: Schedule, grid=None, stream=None):
@@ -48,7 +49,8 @@ def reconstruct(ctx: gpair.Context, b, sched: Schedule, grid=None, stream=None):
     losses = torch.empty(sched.iters, device=dev)
     for t in range(sched.iters):
         lr = gpair.cawr_lr(t, sched.eta_min, sched.eta_max, sched.T0, sched.Tmult, sched.printed_formula)
-        ctx.iterate(z, m, v, b, lr=lr, step=t + 1, mode=sched.mode, eps_npc=sched.eps_npc, lam=sched.lam,
+        ctx.iterate(z, m, v, b, lr=lr, step=t + 1, mode=sched.mode, eps_npc=sched.eps_npc, grad_scale=sched.grad_scale,
+                    lam=sched.lam,
                     beta=sched.beta, eps_reg=sched.eps_reg, grid=grid,
                     x_out=x if t == sched.iters - 1 else None, loss_out=losses[t:t + 1], stream=stream)
     return x, losses
