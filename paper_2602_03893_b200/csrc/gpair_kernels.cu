@@ -46,8 +46,9 @@ __global__ void k_gather(const float* __restrict__ src, const int32_t* __restric
 }
 
 // fp64 polynomial coefficients in the constant bank (DFMA takes them as c[][] operands
-// instead of two register moves per use): 1/720, 1/24, 1/2, 1/5040, 1/120, 1/6, 1
-__constant__ double kLcfPoly[7] = {1.0 / 720.0, 1.0 / 24.0, 0.5, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0, 1.0};
+// instead of two register moves per use): 1/720, 1/24, 1/2, 1/5040, 1/120, 1/6, 1, 1/8!, 1/9!
+__constant__ double kLcfPoly[9] = {1.0 / 720.0, 1.0 / 24.0, 0.5, 1.0 / 5040.0, 1.0 / 120.0, 1.0 / 6.0, 1.0,
+                                   1.0 / 40320.0, 1.0 / 362880.0};
 // e^{+z} and e^{-z} for |z| <= 0.3: C(z^2) +- z S(z^2), degree 3 in z^2 (truncation < 4e-10,
 // and < 4e-12 at the W = 16 bench constants, |z| <= 0.14)
 __device__ __forceinline__ void exp_pm64(double z, double& ep, double& em) {
@@ -70,6 +71,27 @@ __device__ __forceinline__ double exp_small64(double z) {
     p = fma(z, p, kLcfPoly[2]);
     p = fma(z, p, kLcfPoly[6]);
     return fma(z, p, kLcfPoly[6]);
+}
+// 2^{+x} and 2^{-x} for |x| < 1000: x = n + f, n = rint(x), |f| <= 1/2, e^{+-f ln2} = C(z^2) +- z S(z^2)
+// (z = f ln 2, degree 4 in z^2: truncation < 1e-11), scaled by 2^{+-n} through the exponent
+__device__ __forceinline__ void exp2_pm64(double x, double& ep, double& em) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52
+    const double tn = x + magic;
+    const double n = tn - magic;
+    const double z = (x - n) * 0.6931471805599453;
+    const double y = z * z;
+    double Cc = fma(y, kLcfPoly[7], kLcfPoly[0]);
+    Cc = fma(y, Cc, kLcfPoly[1]);
+    Cc = fma(y, Cc, kLcfPoly[2]);
+    Cc = fma(y, Cc, kLcfPoly[6]);
+    double Sc = fma(y, kLcfPoly[8], kLcfPoly[3]);
+    Sc = fma(y, Sc, kLcfPoly[4]);
+    Sc = fma(y, Sc, kLcfPoly[5]);
+    Sc = fma(y, Sc, kLcfPoly[6]);
+    const double zs = z * Sc;
+    const int ni = __double2loint(tn);
+    ep = (Cc + zs) * __hiloint2double((1023 + ni) << 20, 0);
+    em = (Cc - zs) * __hiloint2double((1023 - ni) << 20, 0);
 }
 // 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
 __device__ __forceinline__ double exp2_64(double x) {
@@ -940,8 +962,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
     constexpr int C = W / 2;
     extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* s_tab = smem8;                                  // [La][4]: Q, 1/Q, Ginv, G (fp64)
-    gacc_t* s_g = (gacc_t*)(s_tab + 4 * La);                // [nw][LCF_STAGE*CELL] per-warp kernel sums
+    gacc_t* s_g = (gacc_t*)smem8;                           // [nw][LCF_STAGE*CELL] per-warp kernel sums
     // this lane's column dtil_t = delta_t G(t) at col[t*32] (lcol_t: fp64, or fp32 widened by F2F
     // per sample -- half the shared-memory bytes, but F2F issues on the 16 / clk / SM XU pipe)
     lcol_t* col = (lcol_t*)(s_g + nw * LCF_STAGE * CELL) + (size_t)warp * La * 32 + lane;
@@ -949,7 +970,8 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
     // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1)
     float* s_kxy = (float*)(s_grp + LCF_STAGE * GPC);
     float* s_kzw = s_kxy + LCF_STAGE * CELL * 2;
-    for (int t = threadIdx.x; t < 4 * La; t += blockDim.x) s_tab[t] = gtab[t];
+    double* s_gi = (double*)(s_kzw + LCF_STAGE * CELL * 2);  // [La] Ginv(t) (fp64 factor of the per-pair scale)
+    for (int t = threadIdx.x; t < La; t += blockDim.x) s_gi[t] = gtab[4 * t + 2];
 
     const int c0 = blockIdx.x * cpr, c1 = min(c0 + cpr, ncells);
     if (c0 < c1) stage_kernel_tile(kd, grp, c0, min(LCF_STAGE, c1 - c0), s_kxy, s_kzw, s_grp);
@@ -974,7 +996,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
     const f2_t one = pk2(1.f, 1.f);
     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-    const double K64 = Kln2 * 1.4426950408889634;  // log2-based K (exact enough: only the rare path uses it)
+    const double K64 = Kln2 * 1.4426950408889634;  // K of 2^{K u^2} (log2 base)
     for (int cb = c0; cb < c1; cb += LCF_STAGE) {
         const int nc = min(LCF_STAGE, c1 - cb);
         if (cb != c0) {  // the first tile was staged with the residual columns
@@ -989,12 +1011,18 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
             const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
             const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh), Eu = pk2(a.Eu, a.Eu);
             const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // o = n_lo - lo_j = bits(tt) + nrel
+            // R = 2^{-2K a} with a = u_c + t_c - T = eu + cg (cg = n_a - lo_j - T, an integer per
+            // group and lane): R = Ag 2^{-2K eu}, S = 1/R = Agi 2^{2K eu}; Ag, Agi once per group
+            // (no per-pair table reads: shared memory is the LCF kernel's binding pipe)
+            const double cgd = (double)(a.na - lo_j - (La >> 1));
+            double Ag, Agi;
+            exp2_pm64(-2.0 * K64 * cgd, Ag, Agi);
             // LCF_PPS kernels per step: LCF_PACKS f32x2 packs for the (fp32) time of flight
 #pragma unroll
             for (int t = 0; t < GROUP; t += LCF_PPS) {
                 const int li = gq * GROUP + t;
                 bool rare = exact_grp;
-                f2_t ulo[LCF_PACKS], twm1[LCF_PACKS];
+                f2_t ulo[LCF_PACKS], twm1[LCF_PACKS], eup[LCF_PACKS];
                 int o[LCF_PPS];
                 if (!exact_grp) {
 #pragma unroll
@@ -1009,6 +1037,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                         series2<SDEG>(eps, S, Tw);
                         twm1[h] = sub2(Tw, one);  // T(eps) - 1, exact (Sterbenz): w = h / 2R (1 + twm1)
                         const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
+                        eup[h] = eu;
                         const f2_t x = add2(eu, clo);
                         const f2_t tt = add2(x, mag);
                         const f2_t fl = add2(tt, nmag);
@@ -1046,18 +1075,19 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                         }
                         uc[h] = (double)((h & 1) ? u32b : u32a) - (double)C;  // exact
                         const int tc = o[h] + C;
-                        double rr, ri;
-                        exp_pm64(-2.0 * Kln2 * uc[h], rr, ri);  // r = 2^{-2K u_c}, 1/r
-                        const double2 qq = *(const double2*)(s_tab + 4 * tc);  // Q(t_c), 1/Q(t_c)
-                        R[h] = rr * qq.x;
-                        S[h] = ri * qq.y;
+                        float e32a, e32b;
+                        upk2(eup[h >> 1], e32a, e32b);
+                        double ep, em;
+                        exp2_pm64(-2.0 * K64 * (double)((h & 1) ? e32b : e32a), ep, em);  // 2^{-2K eu}, 2^{2K eu}
+                        R[h] = Ag * ep;
+                        S[h] = Agi * em;
                         rp[h] = col + tc * 32;
                         U[h] = (double)rp[h][(W - C - 1) * 32];
                         Ud[h] = 0.0;
                         Lc[h] = (double)rp[h][-C * 32];
                         Ld[h] = 0.0;
                         // scale w E Ginv(t_c), E = e^{K ln2 u_c^2}
-                        gv[t + h] = (double)((h & 1) ? sc32b : sc32a) * s_tab[4 * tc + 2];
+                        gv[t + h] = (double)((h & 1) ? sc32b : sc32a) * s_gi[tc];
                     }
 #pragma unroll
                     for (int i = 1; i < C; ++i) {
@@ -1108,7 +1138,7 @@ __global__ void __launch_bounds__(32 * LCF_WARPS, GPAIR_LCF_MINB)
                                     Pd = fma(Pd, R0, P);
                                     P = fma(P, R0, (double)col[(t0 + m) * 32]);
                                 }
-                                g = (double)pw.w * exp2_64(K64 * u * u) * s_tab[4 * t0 + 2] * fma(u, P, -R0 * Pd);
+                                g = (double)pw.w * exp2_64(K64 * u * u) * s_gi[t0] * fma(u, P, -R0 * Pd);
                             }
                         }
 #pragma unroll
@@ -1359,7 +1389,7 @@ cudaError_t adj_t_launch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
 
 size_t adj_lcf_smem(const gpair_ctx* c) {
     return (size_t)LCF_STAGE * CELL * 16 + LCF_STAGE * GPC * 16 + (size_t)LCF_WARPS * LCF_STAGE * CELL * sizeof(gacc_t) +
-           (size_t)4 * c->La * 8 + (size_t)LCF_WARPS * c->La * 32 * sizeof(lcol_t);
+           (size_t)c->La * 8 + (size_t)LCF_WARPS * c->La * 32 * sizeof(lcol_t);
 }
 
 template <int W, int MODE, int SDEG>
