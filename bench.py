@@ -26,7 +26,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "kernel-sensor pair evals/s; ms per fwd+adjoint IR iteration at 8.4M kernels"
 UNIT = "pair-evals/s"
-SFU_PER_CLK_SM = 16  # MUFU ex2 lanes / clk / SM (sm_100)
+# roofline of the exact operator: 16 pair-samples / clk / SM = the
+# shared-memory pipe's 128 B / clk / SM over the 8 B each pair-sample moves in both kernels
+# (forward: 4-B load + 4-B store of the lane's accumulator; adjoint: one 8-B load of the lane's
+# fp64 residual column) = SURVEY 8d's SFU rate of one exp per pair-sample (16 MUFU / clk / SM)
+PAIR_SAMPLES_PER_CLK_SM = 16
+ISSUE_PER_CLK_SM = 4  # warp instructions / clk / SM (4 SMSPs)
 
 
 def parse():
@@ -285,35 +290,61 @@ def main():
     if world > 1:
         e2e_s = max_over_ranks(dist, e2e_s, dev)
 
-    # ---- roofline of the dominant kernel (forward or adjoint) on this rank
+    # ---- roofline of the dominant kernel (forward or adjoint) on this rank, and of both
     # per-step totals: with the sensor-group pipeline the forward is 4 equal launches per step
     fwd_ms, fwd_n = prof["forward"]
     adj_ms, adj_n = prof["adjoint"]
     dom = "forward" if fwd_ms >= adj_ms else "adjoint"
     dom_ms = (fwd_ms if dom == "forward" else adj_ms) / args.steps
     dom_launches = (fwd_n if dom == "forward" else adj_n) / args.steps
-    achieved = pair_samples_local / (dom_ms * 1e-3)
     clocks = clk.summary()
     f_max = (clocks["sm_max_mhz"] or 1965) * 1e6
+    f_meas = (clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = n_sm * SFU_PER_CLK_SM * f_max
-    traffic = None
+    side = {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
+            side = json.load(open(tpath)).get(("assa_" if args.op == "assa" else "") + args.config, {})
         except Exception:
-            traffic = None
-    f_meas = (clocks["sm_mhz"] or clocks["sm_max_mhz"] or 1965) * 1e6
-    roof = {"bound": "alu", "kernel": f"k_{'assa_' if args.op == 'assa' else ''}{dom}", "achieved": achieved / 1e9,
-            "peak": peak / 1e9 if args.op == "exact" else None,
-            "unit": "Gpair-samples/s", "frac": achieved / peak if args.op == "exact" else None, "traffic": traffic,
-            "frac_at_measured_clock": (achieved / (n_sm * SFU_PER_CLK_SM * f_meas)) if args.op == "exact" else None,
-            "peak_def": f"{n_sm} SMs x {SFU_PER_CLK_SM} pair-samples/clk x {f_max / 1e6:.0f} MHz: the SFU ex2 rate of one "
-                        "exp per pair-sample (SURVEY 8d) = the shared-memory accumulator rate of one 4-B load + 4-B "
-                        "store per pair-sample at 128 B/clk/SM (the forward's binding unit on the TAB path); "
-                        "DESIGN.md section 6",
-            "pair_samples_per_step": pair_samples_local, "dominant_launches_per_step": dom_launches,
+            side = {}
+    names = {"forward": "k_assa_forward" if args.op == "assa" else "k_forward",
+             "adjoint": "k_assa_adjoint" if args.op == "assa" else "k_adjoint_lcf"}
+    if args.op == "exact":
+        # units: in-window pair-samples, counted on the GPU for this context
+        units, unit, bound = pair_samples_local, "Gpair-samples/s", "alu"
+        peak_of = lambda f: n_sm * PAIR_SAMPLES_PER_CLK_SM * f  # noqa: E731
+        peak_def = (f"{n_sm} SMs x {PAIR_SAMPLES_PER_CLK_SM} pair-samples/clk x {f_max / 1e6:.0f} MHz: 8 B of shared "
+                    "memory per pair-sample (forward 4-B load + 4-B store of the accumulator column, adjoint one 8-B "
+                    "load of the fp64 residual column) at 128 B/clk/SM = SURVEY 8d's one SFU exp per pair-sample; "
+                    "DESIGN.md section 6")
+    else:
+        # ASSA (row f1): units = impulses (pairs); issue-bound: 4 warp instructions / clk / SM over the
+        # kernel's executed instructions per impulse (ncu, profiles/ncu_traffic.json)
+        units, unit, bound = M * cfg.n_sensors, "Gpairs/s", "issue"
+        ipp = side.get("instr_per_pair", {}).get(dom)
+        peak_of = (lambda f: n_sm * ISSUE_PER_CLK_SM * 32 * f / ipp) if ipp else None  # noqa: E731
+        peak_def = (f"{n_sm} SMs x 4 warp-instr/clk x 32 lanes x {f_max / 1e6:.0f} MHz / {ipp} executed instructions "
+                    "per impulse (ncu, cfg4): the issue bound of the kernel as built; DESIGN.md section 8b")
+    per_kernel = {}
+    for key, (tot_ms, n) in (("forward", prof["forward"]), ("adjoint", prof["adjoint"])):
+        if not n:
+            continue
+        k_ms = tot_ms / args.steps
+        ach = units / (k_ms * 1e-3)
+        if args.op == "exact":
+            kpeak = peak_of(f_max)
+        else:
+            kipp = side.get("instr_per_pair", {}).get(key)
+            kpeak = n_sm * ISSUE_PER_CLK_SM * 32 * f_max / kipp if kipp else None
+        per_kernel[names[key]] = {"ms": k_ms, "achieved": ach / 1e9, "frac": (ach / kpeak) if kpeak else None}
+    achieved = units / (dom_ms * 1e-3)
+    peak = peak_of(f_max) if peak_of else None
+    roof = {"bound": bound, "kernel": names[dom], "achieved": achieved / 1e9,
+            "peak": peak / 1e9 if peak else None, "unit": unit, "frac": achieved / peak if peak else None,
+            "traffic": side.get(dom), "frac_at_measured_clock": (achieved / peak_of(f_meas)) if peak_of else None,
+            "peak_def": peak_def, "units_per_step": units, "dominant_launches_per_step": dom_launches,
+            "per_kernel": per_kernel,
             "kernel_ms": {k: (v[0] / args.steps) for k, v in prof.items() if v[1]},
             "share_of_step": {k: (v[0] / args.steps) / ms for k, v in prof.items() if v[1]}}
 

@@ -568,6 +568,7 @@ struct TabConst {
     float K;               // K1u
     float kappa;           // -2 K1u ln 2
     int32_t on;            // 1: cnt_int == W, W % 4 == 0, TAB_MIN <= W <= TAB_MAX, degree-2 series path
+    int32_t pscale;        // 1: per-pair scale by the unbiased polynomial (wide 1/r spread, set at create)
 };
 
 // r = exp2(-2 K u_c), s = 1 / r for two pairs (f32x2)
@@ -625,10 +626,44 @@ __device__ __forceinline__ void series2(f2_t eps, f2_t& S, f2_t& Tw) {
 }
 
 // Forward accumulate of one pair's W samples into its smem column (lane stride
+// 32; ap points at sample n_lo).  P0 = w E; r, s = exp2(-/+2 K u_c).
+template <int W>
+__device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float r, float s, const TabConst& t) {
+    constexpr int C = W / 2;
+    const f2_t U = pk2(uc, uc);
+    f2_t P = pk2(P0, P0 * r);  // (P_0, P_1)
+    const float r2 = r * r;
+#pragma unroll
+    for (int i = C; i < W; i += 2) {
+        const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
+        f2_t acc2 = pk2(ap[i * 32], ap[(i + 1) * 32]);
+        acc2 = fma2(P, Q, acc2);
+        float v0, v1;
+        upk2(acc2, v0, v1);
+        ap[i * 32] = v0;
+        ap[(i + 1) * 32] = v1;
+        P = mul2(P, pk2(r2, r2));
+    }
+    const float s2 = s * s;
+    f2_t Pd = pk2(P0 * s2, P0 * s);  // (P_-2, P_-1)
+#pragma unroll
+    for (int i = C - 2; i >= 0; i -= 2) {
+        const f2_t Q = fma2(U, t.c2[i / 2], t.d2[i / 2]);
+        f2_t acc2 = pk2(ap[i * 32], ap[(i + 1) * 32]);
+        acc2 = fma2(Pd, Q, acc2);
+        float v0, v1;
+        upk2(acc2, v0, v1);
+        ap[i * 32] = v0;
+        ap[(i + 1) * 32] = v1;
+        Pd = mul2(Pd, pk2(s2, s2));
+    }
+}
+
+// Forward accumulate of one pair's W samples into its smem column (lane stride
 // 32; ap points at sample n_lo).  P0 = w E; er, es = r - 1, s - 1 with
 // r, s = exp2(-/+2 K u_c) (tab_rs_eps): every chain step is P (1 + eps).
 template <int W>
-__device__ __forceinline__ void acc_tab(float* ap, float uc, float P0, float er, float es, const TabConst& t) {
+__device__ __forceinline__ void acc_tab_eps(float* ap, float uc, float P0, float er, float es, const TabConst& t) {
     constexpr int C = W / 2;
 
     const f2_t U = pk2(uc, uc);

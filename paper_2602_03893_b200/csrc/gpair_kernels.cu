@@ -331,10 +331,13 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                 // u_c = u_lo - C (exact), E = exp2(K u_c^2), r = exp2(-2K u_c), s = 1/r
                                 const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
                                 f2_t r2, s2;
-                                tab_rs_eps(uc, tab, r2, s2);  // r - 1, s - 1
+                                if (tab.pscale)
+                                    tab_rs_eps(uc, tab, r2, s2);  // r - 1, s - 1 (near-1 chains)
+                                else
+                                    tab_rs(uc, tab, r2, s2);
                                 float uc0, uc1, p0, p1, r0, r1, q0, q1;
                                 upk2(uc, uc0, uc1);
-                                {
+                                if (tab.pscale) {
                                     // per-pair scale in fp32 with few roundings: w = A (h/2R)(1 + (T - 1)),
                                     // E = 2^{K u_c^2} by a degree-5 polynomial (|z| <= 0.13, unbiased)
                                     const f2_t z = mul2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), pk2(0.69314718f, 0.69314718f));
@@ -345,11 +348,20 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                     ep = fma2(z, ep, pk2(1.f, 1.f));
                                     const f2_t wq = fma2(h2R, sub2(Tw, one), h2R);
                                     upk2(mul2(mul2(A2, ep), wq), p0, p1);
+                                } else {  // E by MUFU.EX2 (the compact geometries of cfg2-4)
+                                    float e0, e1;
+                                    upk2(mul2(mul2(uc, pk2(tab.K, tab.K)), uc), e0, e1);
+                                    upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), p0, p1);
                                 }
                                 upk2(r2, r0, r1);
                                 upk2(s2, q0, q1);
-                                acc_tab<TABW ? WMAX : 4>(s_acc_lane + n0 * 32, uc0, p0, r0, q0, tab);
-                                acc_tab<TABW ? WMAX : 4>(s_acc_lane + n1 * 32, uc1, p1, r1, q1, tab);
+                                if (tab.pscale) {  // wide geometries: the near-1 chains (acc_tab_eps)
+                                    acc_tab_eps<TABW ? WMAX : 4>(s_acc_lane + n0 * 32, uc0, p0, r0, q0, tab);
+                                    acc_tab_eps<TABW ? WMAX : 4>(s_acc_lane + n1 * 32, uc1, p1, r1, q1, tab);
+                                } else {
+                                    acc_tab<TABW ? WMAX : 4>(s_acc_lane + n0 * 32, uc0, p0, r0, q0, tab);
+                                    acc_tab<TABW ? WMAX : 4>(s_acc_lane + n1 * 32, uc1, p1, r1, q1, tab);
+                                }
                             } else {
                                 acc_packed<WMAX>(s_acc_lane + n0 * 32, u0, w0, k.K1u);
                                 acc_packed<WMAX>(s_acc_lane + n1 * 32, u1, w1, k.K1u);

@@ -438,6 +438,9 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
             unsigned b0 = (unsigned)h_flags[8], b1 = (unsigned)h_flags[9];
             memcpy(&rmn, &b0, 4);
             memcpy(&rmx, &b1, 4);
+            // the same spread makes the y samples cancel strongly enough that the forward's
+            // per-pair scale needs its few-rounding form (measured at cfg5)
+            c->tab.pscale = rmx > FWD_WIDE_RATIO * rmn ? 1 : 0;
             if (cpr > FWD_CPR_WIDE && !cpr_forced && rmx > FWD_WIDE_RATIO * rmn) {
                 cudaFree(wlo);
                 cpr = FWD_CPR_WIDE;

@@ -7,7 +7,7 @@ mkdir -p gpurun_out
 CFG=${CFG:-cfg4}; K=${K:-k_adjoint}; TAG=${TAG:-x}
 REP=gpurun_out/prof_${CFG}_${KN:-$K}_${TAG}
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -c 1 \
-    -o $REP -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${KN:-$K}_${TAG}.log 2>&1
+    -o $REP -f python scripts/profile_once.py $CFG $ARGS > gpurun_out/ncu_full_${KN:-$K}_${TAG}.log 2>&1
 echo "full $K rc=$?"
 python scripts/ncu_summary.py $REP.ncu-rep > ${REP}_summary.txt 2>&1
 python scripts/sass_mix.py $REP.ncu-rep ${UNITS:-268435456} > ${REP}_sassmix.txt 2>&1
