@@ -21,7 +21,14 @@ for K in k_forward k_adjoint_lcf "k_reduce\$"; do
       -o gpurun_out/prof_${CFG}_${KN}_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${KN}_${TAG}.log 2>&1
   echo "full $KN rc=$?"
   python scripts/ncu_summary.py gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep > gpurun_out/ncu_summary_${KN}_${TAG}.txt 2>&1
-  ncu -i gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_source_${KN}_${TAG}.csv 2>/dev/null
+  python scripts/sass_mix.py gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep 268435456 > gpurun_out/ncu_sassmix_${KN}_${TAG}.txt 2>&1
   [ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep
 done
+# the other bench lines: the reference arm (fp64 oracle), the ASSA operator, cfg5 / cfg3
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1
+timeout 600 python bench.py --op assa --no-cpu-baseline > gpurun_out/bench_assa_${TAG}.log 2>&1
+for C in cfg5 cfg3; do timeout 600 python bench.py --config $C --no-cpu-baseline > gpurun_out/bench_${C}_${TAG}.log 2>&1; done
+# NVTX: the library's stage ranges (domain "gpair") around each launch of one cfg1 iterate
+timeout 300 ncu --nvtx --print-summary per-nvtx --metrics gpu__time_duration.sum --clock-control none \
+    python scripts/profile_once.py cfg1 > gpurun_out/ncu_nvtx_${TAG}.txt 2>&1
 tail -2 gpurun_out/pytest_gpu_${TAG}.log; tail -2 gpurun_out/smoke_${TAG}.log; tail -c 600 gpurun_out/bench_${TAG}.log
