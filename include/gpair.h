@@ -187,7 +187,7 @@ typedef struct {
                                    3 = sensor lanes + per-sample exponential (k_adjoint_sl) */
     int32_t collective;         /* 1: kernel-sharded path (NCCL all-reduce of y, separate
                                    residual kernel): world > 1 or GPAIR_COLLECTIVE          */
-    int32_t reserved;           /* 0                                                    */
+    int32_t fwd_union;          /* 1: register-window forward (opt-in GPAIR_FWD_UNION=1) */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial

@@ -46,6 +46,7 @@ void build_tab(gpair_ctx* c) {
     t.K = k.K1u;
     t.m2K = -2.0f * k.K1u;
     t.kappa = (float)(-2.0 * (double)k.K1u * 0.6931471805599453);
+    t.inv_h = (float)k.inv_h;
     if (t.on) {
         const int C = W / 2;
         const double Kd = -1.4426950408889634 * k.h * k.h / (2.0 * k.sigma * k.sigma);
@@ -55,6 +56,11 @@ void build_tab(gpair_ctx* c) {
             const double cv = std::exp2(Kd * (double)m * (double)m);
             cf[i] = (float)cv;                 // each entry rounded once from fp64:
             df[i] = (float)(-(double)m * cv);  // the table's error is common to every pair
+        }
+        for (int i = 0; i < 11; ++i) {  // union-window Gaussian G_p = 2^{K (p - 11)^2}, p = 2i, 2i + 1
+            const float g0 = (float)std::exp2(Kd * (2.0 * i - 11) * (2.0 * i - 11));
+            const float g1 = (float)std::exp2(Kd * (2.0 * i - 10) * (2.0 * i - 10));
+            t.g2[i] = ((gpair::f2_t)__builtin_bit_cast(uint32_t, g1) << 32) | __builtin_bit_cast(uint32_t, g0);
         }
         for (int i = 0; i < W; i += 2) {
             t.c2[i / 2] = ((gpair::f2_t)__builtin_bit_cast(uint32_t, cf[i + 1]) << 32) | __builtin_bit_cast(uint32_t, cf[i]);
@@ -605,7 +611,7 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->tab = ((c->ser == 0 || c->ser == gpair::SER_FAST5) && c->tab.on) ? 1 : 0;
     o->adj_kernel = c->assa ? 0 : gpair::adjoint_kernel(c);
     o->collective = c->coll;
-    o->reserved = 0;
+    o->fwd_union = c->f_union;
     return GPAIR_OK;
 }
 

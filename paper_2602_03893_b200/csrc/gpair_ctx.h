@@ -43,6 +43,7 @@ struct gpair_ctx_s {
     // forward decomposition
     int32_t f_cpr = 0, f_regions = 0, f_warps = 0, f_sgroups = 0, Lf = 0;
     int32_t f_split = 1;  // kernel subsets per sensor warp in k_forward (split accumulation)
+    int32_t f_union = 0;  // 1: register-window forward (k_forward<16, 0, true>)
     int32_t* d_wlo_f = nullptr;   // [f_regions][Nd] window start (-1 = empty)
     int2* d_rent = nullptr;       // [Nd][f_regions] (window start, region) sorted by start (reducer)
     int32_t jlen_max = 0;         // longest per-sensor live range of the partial windows

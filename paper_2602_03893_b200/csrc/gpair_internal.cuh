@@ -569,6 +569,8 @@ struct TabConst {
     float kappa;           // -2 K1u ln 2
     int32_t on;            // 1: cnt_int == W, W % 4 == 0, TAB_MIN <= W <= TAB_MAX, degree-2 series path
     int32_t pscale;        // 1: per-pair scale by the unbiased polynomial (wide 1/r spread, set at create)
+    float inv_h;           // f_s / v (group radius in samples, union window)
+    f2_t g2[11];           // union window: (G_2i, G_2i+1), G_p = 2^{K (p - 11)^2} (k_forward<.., UNION>)
 };
 
 // r = exp2(-2 K u_c), s = 1 / r for two pairs (f32x2)

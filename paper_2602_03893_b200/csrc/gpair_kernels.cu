@@ -186,7 +186,19 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 constexpr int FWD_STAGE = 6;                                        // cells per double-buffered tile (FAST)
 constexpr int FWD_BUF = FWD_STAGE * CELL * 5 + FWD_STAGE * GPC * 4;  // floats per tile buffer
 
-template <int WMAX, int SER>
+// Register-window union (UNION, W = 16 compact geometries): the 8 pairs of a group are
+// evaluated at the 22 positions of their union window in registers and the group's sums
+// are added to the lane's column once per position:
+//   value(P0 + p) = w (a - tau_p) 2^{K (a - tau_p)^2},  tau_p = p - 11,  a = u_c + k - 3
+//                 = G_p * alpha rho^tau_p (tau_p - a) * (-1),  alpha = w 2^{K a^2}, rho = 2^{-2K a},
+// with G_p = 2^{K tau_p^2} applied at the group flush (constant per position).  The chains
+// rho^tau run from the window centre (tau = 0) outward; k = window start - P0 in [0, 6] (P0 from
+// the anchor and the group radius); positions 6..15 lie in every window, the 6 + 6 edge
+// positions are masked per pair.  Accumulation: 8 pairs in registers, then one fp32 add per
+// group and position into the column (64 groups per 512-kernel region: no split needed).
+constexpr int UNION_U = 22;
+
+template <int WMAX, int SER, bool UNION = false>
 __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* __restrict__ kd, const float* __restrict__ amp,
                                                  const float4* __restrict__ grp, const float* __restrict__ orig,
                                                  const float* __restrict__ sens, const int32_t* __restrict__ wlo,
@@ -290,6 +302,14 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             if constexpr (FAST) {
                 if (!__any_sync(__activemask(), a.na == NA_EXACT)) {
+                    // union window eligibility: group radius <= 2.5 samples (k in [0, 6]), uniform per group
+                    const float dR = s_grp[gq].w * tab.inv_h * 1.0001f + 1e-3f;
+                    const bool uni = UNION && dR <= 2.5f;
+                    // union start (column index): round(eu + c_lo) + 1 + n_a - lo_j over eu in [Eu - dR, Eu + dR]
+                    const int P0 = (int)floorf(a.Eu + k.c_lo - dR + 0.5f) + 1 + (a.na - lo_j);
+                    f2_t Su[UNION_U / 2];
+#pragma unroll
+                    for (int i = 0; i < UNION_U / 2; ++i) Su[i] = 0ull;
                     // Two pairs per step: pair_fast's arithmetic in f32x2 (bit-identical
                     // results), the anchor's per-lane scalars broadcast to both halves.
                     const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
@@ -326,7 +346,68 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                         const int n0 = __float_as_int(t0) + nrel, n1 = __float_as_int(t1) + nrel;
                         const bool bad0 = fabsf(d0) > 0.5f - GAMMA || (unsigned)(n0 + lo_j) > span;
                         const bool bad1 = fabsf(d1) > 0.5f - GAMMA || (unsigned)(n1 + lo_j) > span;
-                        if (!(bad0 || bad1)) {
+                        const int ku0 = n0 - P0, ku1 = n1 - P0;
+                        if (UNION && uni && !(bad0 || bad1) && (unsigned)ku0 <= 6u && (unsigned)ku1 <= 6u) {
+                            // a = u_c + k - 3 (|a| < 4); alpha = w 2^{K a^2}; rho = 2^{-2K a}, 1/rho
+                            const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
+                            const f2_t av = add2(uc, pk2((float)(ku0 - 3), (float)(ku1 - 3)));
+                            float a0, a1, e0, e1;
+                            upk2(av, a0, a1);
+                            upk2(mul2(mul2(av, pk2(tab.K, tab.K)), av), e0, e1);
+                            float al0, al1;
+                            upk2(mul2(w, pk2(ex2f(e0), ex2f(e1))), al0, al1);
+                            // e^{+-x}, x = -2K ln2 a (|x| <= 0.56): C(x^2) +- x S(x^2), degree 4 in x^2
+                            const f2_t x = mul2(av, pk2(tab.kappa, tab.kappa));
+                            const f2_t y = mul2(x, x);
+                            f2_t Cc = fma2(y, pk2(1.f / 40320.f, 1.f / 40320.f), pk2(1.f / 720.f, 1.f / 720.f));
+                            Cc = fma2(y, Cc, pk2(1.f / 24.f, 1.f / 24.f));
+                            Cc = fma2(y, Cc, pk2(0.5f, 0.5f));
+                            Cc = fma2(y, Cc, pk2(1.f, 1.f));
+                            f2_t Sn = fma2(y, pk2(1.f / 362880.f, 1.f / 362880.f), pk2(1.f / 5040.f, 1.f / 5040.f));
+                            Sn = fma2(y, Sn, pk2(1.f / 120.f, 1.f / 120.f));
+                            Sn = fma2(y, Sn, pk2(1.f / 6.f, 1.f / 6.f));
+                            Sn = fma2(y, Sn, pk2(1.f, 1.f));
+                            const f2_t xS = mul2(x, Sn);
+                            float rho0, rho1, sig0, sig1;
+                            upk2(add2(Cc, xS), rho0, rho1);
+                            upk2(sub2(Cc, xS), sig0, sig1);
+#pragma unroll
+                            for (int h = 0; h < 2; ++h) {
+                                const float al = h ? al1 : al0, rho = h ? rho1 : rho0, sig = h ? sig1 : sig0;
+                                const float aa = h ? a1 : a0;
+                                const int kk = h ? ku1 : ku0;
+                                const f2_t na2 = pk2(-aa, -aa);
+                                const f2_t r2 = pk2(rho * rho, rho * rho), s2 = pk2(sig * sig, sig * sig);
+                                // centre pair i = 5: tau = (-1, 0)
+                                const f2_t Xc = pk2(al * sig, al);
+                                f2_t X = Xc;
+#pragma unroll
+                                for (int i = 5; i < UNION_U / 2; ++i) {  // tau = 2i - 11, 2i - 10 upward
+                                    if (i > 5) X = mul2(X, r2);
+                                    const f2_t D = add2(pk2((float)(2 * i - 11), (float)(2 * i - 10)), na2);
+                                    f2_t Xm = X;
+                                    if (2 * i + 1 >= WMAX) {  // positions 16..21: in-window iff p < k + 16
+                                        float x0, x1;
+                                        upk2(X, x0, x1);
+                                        Xm = pk2(2 * i - WMAX < kk ? x0 : 0.f, 2 * i + 1 - WMAX < kk ? x1 : 0.f);
+                                    }
+                                    Su[i] = fma2(D, Xm, Su[i]);
+                                }
+                                X = Xc;
+#pragma unroll
+                                for (int i = 4; i >= 0; --i) {  // downward
+                                    X = mul2(X, s2);
+                                    const f2_t D = add2(pk2((float)(2 * i - 11), (float)(2 * i - 10)), na2);
+                                    f2_t Xm = X;
+                                    if (2 * i < 6) {  // positions 0..5: in-window iff p >= k
+                                        float x0, x1;
+                                        upk2(X, x0, x1);
+                                        Xm = pk2(2 * i >= kk ? x0 : 0.f, 2 * i + 1 >= kk ? x1 : 0.f);
+                                    }
+                                    Su[i] = fma2(D, Xm, Su[i]);
+                                }
+                            }
+                        } else if (!(bad0 || bad1)) {
                             if (TABW && tab.on) {
                                 // u_c = u_lo - C (exact), E = exp2(K u_c^2), r = exp2(-2K u_c), s = 1/r
                                 const f2_t uc = add2(ulo, pk2(-(float)(WMAX / 2), -(float)(WMAX / 2)));
@@ -387,6 +468,18 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                                 p = pair_fix(p, e1, a.na, fabsf(d1) > 0.5f - GAMMA, orig, gi + 1, Mpad, sx, sy, sz,
                                              k.cnt_int, k);
                             acc_pair<WMAX>(s_acc_lane, lo_j, p, k.K1u);
+                        }
+                    }
+                    if (UNION && uni) {  // the group's union sums -> column (value = -G_p S_p), fixed order
+#pragma unroll
+                        for (int i = 0; i < UNION_U / 2; ++i) {
+                            const int p0 = P0 + 2 * i;
+                            float v0, v1, g0, g1;
+                            upk2(Su[i], v0, v1);
+                            upk2(tab.g2[i], g0, g1);
+                            if ((unsigned)p0 < (unsigned)Lf) s_acc_lane[p0 * 32] = fmaf(-g0, v0, s_acc_lane[p0 * 32]);
+                            if ((unsigned)(p0 + 1) < (unsigned)Lf)
+                                s_acc_lane[(p0 + 1) * 32] = fmaf(-g1, v1, s_acc_lane[(p0 + 1) * 32]);
                         }
                     }
                     continue;
@@ -1336,14 +1429,14 @@ int pick_wmax(int w) {
 }
 namespace {
 
-template <int W, int SER>
+template <int W, int SER, bool UNION = false>
 cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
     constexpr bool DBUFL = (SER == 0 || SER == SER_FAST5) && W >= 12;
     size_t smem = (DBUFL ? (size_t)2 * FWD_BUF * 4
                          : (size_t)STAGE_CELLS * CELL * 20 + STAGE_CELLS * GPC * 16 +
                                (SER == SER_GEN ? (size_t)STAGE_CELLS * CELL * 16 : 0)) +
                   (size_t)c->f_warps * c->Lf * 32 * 4;
-    cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_forward<W, SER, UNION>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // lng / lg0: window of 256-sensor pipeline groups; one CTA covers 32 f_warps / f_split sensors
     const int per256 = 256 / (32 * (c->f_warps / c->f_split));
@@ -1351,7 +1444,7 @@ cudaError_t fwd_launch(gpair_ctx* c, cudaStream_t st) {
     OpConst kk = c->k;
     kk.grp0 = c->lng > 0 ? c->lg0 * per256 : 0;
     ++c->n_launch;
-    k_forward<W, SER><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
+    k_forward<W, SER, UNION><<<grid, 32 * c->f_warps, smem, st>>>(c->d_kd, c->d_amp, c->d_grp, c->d_orig, c->d_sens,
                                                       c->d_wlo_f, c->d_partial, c->f_cpr, c->ncells, c->Lf,
                                                       c->Mpad, kk, c->d_ksig, c->tab, c->f_split);
     return cudaGetLastError();
@@ -1555,7 +1648,10 @@ cudaError_t fwd_dispatch(gpair_ctx* c, cudaStream_t st) {
         case 5: return fwd_launch<5, SER>(c, st);
         case 8: return fwd_launch<8, SER>(c, st);
         case 12: return fwd_launch<12, SER>(c, st);
-        case 16: return fwd_launch<16, SER>(c, st);
+        case 16:
+            if constexpr (SER == 0)
+                if (c->f_union) return fwd_launch<16, 0, true>(c, st);
+            return fwd_launch<16, SER>(c, st);
         case 20: return fwd_launch<20, SER>(c, st);
         case 24: return fwd_launch<24, SER>(c, st);
         case 32: return fwd_launch<32, SER>(c, st);

@@ -480,6 +480,20 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
         c->workspace_bytes += sizeof(int32_t) * (int64_t)nreg * Nd;
         break;
     }
+    {
+        // register-window forward (k_forward<16, 0, true>), opt-in with GPAIR_FWD_UNION=1:
+        // W = 16 on the degree-2 TAB path of a compact geometry, |2K ln2| * 4 <= 0.6 (its rho polynomial);
+        // its register sums keep the fp32 column chains short, so it runs without split accumulation.
+        // Measured at cfg4: 46.2 ms against 42.9 ms for the split TAB forward (more accurate: rows
+        // 3.8e-5 vs 5.5e-5 elementwise), so it is not the default.
+        const char* ev = std::getenv("GPAIR_FWD_UNION");
+        c->f_union = (c->k.cnt_int == 16 && c->ser == 0 && c->tab.on && !c->tab.pscale &&
+                      std::fabs(c->tab.kappa) * 4.f <= 0.6f && (ev && ev[0] == '1') && !c->assa) ? 1 : 0;
+        if (c->f_union) {
+            c->f_split = 1;
+            c->f_sgroups = (Nd + 32 * c->f_warps - 1) / (32 * c->f_warps);
+        }
+    }
     // reducer tables (sorted window starts per sensor, chunk ranges)
     {
         const int64_t nt = (int64_t)c->f_regions * Nd;
@@ -509,6 +523,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
 
     // ---- adjoint regions
     int acpr = 8;
+    if (const char* ev = std::getenv("GPAIR_ADJ_CPR")) acpr = std::max(1, std::min(8, atoi(ev)));  // A/B runs
     while (acpr > 1 && (c->ncells + acpr - 1) / acpr < 4 * dev_sms) acpr /= 2;
     for (;;) {
         int nreg = (c->ncells + acpr - 1) / acpr;

@@ -97,7 +97,7 @@ class Info(ctypes.Structure):
         ("tab", ctypes.c_int32),
         ("adj_kernel", ctypes.c_int32),
         ("collective", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("fwd_union", ctypes.c_int32),
     ]
 
     def as_dict(self):

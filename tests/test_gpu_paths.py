@@ -32,8 +32,10 @@ PATHS = {
     # sensor-group pipeline of gpair_iterate (opt-in): forward / reducer / adjoint per 256-sensor group
     "tab+lcf+pipeline": ({"GPAIR_PIPELINE": "1"}, (1, 2)),
     "per_sample_exp+lane_sl+pipeline": ({"GPAIR_NO_TAB": "1", "GPAIR_PIPELINE": "1"}, (0, 3)),
+    # register-window forward (opt-in)
+    "tab_union+lcf": ({"GPAIR_FWD_UNION": "1"}, (1, 2)),
 }
-ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE")
+ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE", "GPAIR_FWD_UNION")
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -73,6 +75,7 @@ def test_forward_adjoint_each_path(path, monkeypatch):
     ctx = make_ctx(c, s, op, monkeypatch, env)
     info = ctx.info()
     assert (info["tab"], info["adj_kernel"]) == expect, info
+    assert info["fwd_union"] == (1 if env.get("GPAIR_FWD_UNION") == "1" else 0), info
     x = inputs.dense_amplitudes(c.shape[1])
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"{path} forward")
     d = inputs.residual(s.shape[1], op["n_samples"])
