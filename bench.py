@@ -309,7 +309,9 @@ def main():
         except Exception:
             side = {}
     names = {"forward": "k_assa_forward" if args.op == "assa" else "k_forward",
-             "adjoint": "k_assa_adjoint" if args.op == "assa" else "k_adjoint_lcf"}
+             "adjoint": "k_assa_adjoint" if args.op == "assa" else
+             {0: "k_adjoint", 1: "k_adjoint_t", 2: "k_adjoint_lcf", 3: "k_adjoint_sl",
+              4: "k_adjoint_mp"}.get(info["adj_kernel"], "adjoint")}
     if args.op == "exact":
         # units: in-window pair-samples, counted on the GPU for this context
         units, unit, bound = pair_samples_local, "Gpair-samples/s", "alu"

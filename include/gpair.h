@@ -184,7 +184,8 @@ typedef struct {
     int32_t adj_kernel;         /* adjoint kernel: 0 = lane per kernel (k_adjoint),
                                    1 = sensor lanes + TAB (k_adjoint_t),
                                    2 = sensor lanes + lane-centred factorisation (k_adjoint_lcf),
-                                   3 = sensor lanes + per-sample exponential (k_adjoint_sl) */
+                                   3 = sensor lanes + per-sample exponential (k_adjoint_sl),
+                                   4 = lane per kernel + moment polynomial (k_adjoint_mp) */
     int32_t collective;         /* 1: kernel-sharded path (NCCL all-reduce of y, separate
                                    residual kernel): world > 1 or GPAIR_COLLECTIVE          */
     int32_t fwd_union;          /* 1: register-window forward (opt-in GPAIR_FWD_UNION=1) */

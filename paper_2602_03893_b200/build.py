@@ -8,7 +8,7 @@ CSRC = os.path.join(HERE, "csrc")
 # GPAIR_LIB names an alternative output (compile-time variant builds, scripts/variants.sh);
 # gpair.py loads the same name, so a variant never overwrites the default library.
 LIB = os.path.join(HERE, os.environ.get("GPAIR_LIB", "libgpair.so"))
-SOURCES = ["gpair_api.cu", "gpair_setup.cu", "gpair_kernels.cu", "gpair_assa.cu", "gpair_vcr.cu", "gpair_near.cu"]
+SOURCES = ["gpair_api.cu", "gpair_setup.cu", "gpair_kernels.cu", "gpair_assa.cu", "gpair_vcr.cu", "gpair_near.cu", "gpair_mp.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

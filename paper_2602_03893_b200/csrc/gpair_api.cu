@@ -41,7 +41,7 @@ void build_tab(gpair_ctx* c) {
         return v && v[0] == '1';
     };
     c->dbg = (env1("GPAIR_NO_TAB") ? gpair::DBG_NO_TAB : 0) | (env1("GPAIR_ADJ_NO_LCF") ? gpair::DBG_ADJ_NO_LCF : 0) |
-             (env1("GPAIR_ADJ_NO_T") ? gpair::DBG_ADJ_NO_T : 0);
+             (env1("GPAIR_ADJ_NO_T") ? gpair::DBG_ADJ_NO_T : 0) | (env1("GPAIR_ADJ_NO_MP") ? gpair::DBG_ADJ_NO_MP : 0);
     t.on = (W >= gpair::TAB_MIN && W % 4 == 0 && W <= gpair::TAB_MAX && !k.gen && !(c->dbg & gpair::DBG_NO_TAB)) ? 1 : 0;
     t.K = k.K1u;
     t.m2K = -2.0f * k.K1u;
@@ -215,6 +215,9 @@ void free_ctx(gpair_ctx* c) {
     cudaFree(c->d_wlo_a);
     cudaFree(c->d_gpart);
     cudaFree(c->d_gtab);
+    cudaFree(c->d_wlo_m);
+    cudaFree(c->d_mp);
+    cudaFree(c->d_mp_coef);
     cudaFree(c->d_amp);
     cudaFree(c->d_y);
     cudaFree(c->d_delta);
@@ -270,7 +273,7 @@ gpair_status pipeline_init(gpair_ctx* c) {
 bool pipeline_eligible(const gpair_ctx* c) {
     const int ak = gpair::adjoint_kernel(c);
     return c->pipeline && !c->assa && !c->n_near && c->f_warps == 8 &&
-           (ak == gpair::ADJ_LCF || ak == gpair::ADJ_TAB_T || ak == gpair::ADJ_SL) && gpair::adjoint_groups(c) <= 64 &&
+           (ak == gpair::ADJ_MP || ak == gpair::ADJ_LCF || ak == gpair::ADJ_TAB_T || ak == gpair::ADJ_SL) && gpair::adjoint_groups(c) <= 64 &&
            256 % (32 * (c->f_warps / c->f_split)) == 0;
 }
 

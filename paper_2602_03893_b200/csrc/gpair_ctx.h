@@ -54,6 +54,13 @@ struct gpair_ctx_s {
     int32_t a_cpr = 0, a_regions = 0, La = 0;
     int32_t* d_wlo_a = nullptr;   // [a_regions][Nd]
     gpair::gacc_t* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
+    // moment-polynomial adjoint (gpair_mp.cu): regions of mp_cpr cells, start-sample ranges, moments
+    int mp_on = 0;
+    double mp_fit_err = 0.0;      // max error of the degree-7 interpolants / max |f| (create)
+    int32_t mp_cpr = 0, mp_regions = 0, mp_Lr2 = 0, mp_NtP = 0, mp_pad = 0;
+    int32_t* d_wlo_m = nullptr;   // [mp_regions][Nd] lowest n_lo of the region's pairs (INT_MIN: none)
+    double* d_mp = nullptr;       // [Nd][mp_NtP][8] fp64 moments M_k[j][n] at row n + W - 1 + mp_pad (chunk-swizzled)
+    double* d_mp_coef = nullptr;  // [W][8] interpolation coefficients c_mk
     double* d_gtab = nullptr;     // [La][4] fp64 Q = 2^{-2K tau}, 1/Q, 1/G, G = 2^{K tau^2}, tau = t - La/2 (k_adjoint_lcf), or NULL
 
     // per-call workspaces
@@ -172,10 +179,16 @@ int adjoint_groups(const gpair_ctx* c);
 int pick_wmax(int w);
 // adjoint kernel of a context: 0 = k_adjoint (lane = kernel), 1 = k_adjoint_t (TAB, sensor lanes),
 // 2 = k_adjoint_lcf (lane-centred factorisation), 3 = k_adjoint_sl (sensor lanes, per-sample exponential)
-enum { ADJ_LANE_KERNEL = 0, ADJ_TAB_T = 1, ADJ_LCF = 2, ADJ_SL = 3 };
+// 4 = k_adjoint_mp (lane = kernel, moment polynomial; gpair_mp.cu)
+enum { ADJ_LANE_KERNEL = 0, ADJ_TAB_T = 1, ADJ_LCF = 2, ADJ_SL = 3, ADJ_MP = 4 };
 int adjoint_kernel(const gpair_ctx* c);
 // debug / A-B switches read once at create from the environment
-enum { DBG_NO_TAB = 1, DBG_ADJ_NO_LCF = 2, DBG_ADJ_NO_T = 4 };
+enum { DBG_NO_TAB = 1, DBG_ADJ_NO_LCF = 2, DBG_ADJ_NO_T = 4, DBG_ADJ_NO_MP = 8 };
+
+// moment-polynomial adjoint (gpair_mp.cu)
+cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why);
+cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
+int mp_groups(const gpair_ctx* c);
 
 // ASSA operator (gpair_assa.cu)
 size_t assa_forward_smem(const gpair_ctx* c, int Lf);

@@ -497,6 +497,26 @@ __device__ __forceinline__ AssaPair assa_fast(const Anchor& a, float4 kd, float 
     return p;
 }
 
+// 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
+__device__ __forceinline__ double exp2_64(double x) {
+    const double magic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x to an integer
+    const double tn = x + magic;
+    const double n = tn - magic;
+    const double z = (x - n) * 0.6931471805599453;
+    double p = fma(z, 1.0 / 3628800.0, 1.0 / 362880.0);
+    p = fma(z, p, 1.0 / 40320.0);
+    p = fma(z, p, 1.0 / 5040.0);
+    p = fma(z, p, 1.0 / 720.0);
+    p = fma(z, p, 1.0 / 120.0);
+    p = fma(z, p, 1.0 / 24.0);
+    p = fma(z, p, 1.0 / 6.0);
+    p = fma(z, p, 0.5);
+    p = fma(z, p, 1.0);
+    p = fma(z, p, 1.0);
+    const int ni = __double2loint(tn);  // low word of x + magic = n (two's complement)
+    return p * __hiloint2double((ni + 1023) << 20, 0);
+}
+
 // ---- packed fp32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2)
 typedef unsigned long long f2_t;
 __device__ __forceinline__ f2_t pk2(float lo, float hi) {

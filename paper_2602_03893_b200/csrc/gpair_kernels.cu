@@ -93,26 +93,6 @@ __device__ __forceinline__ void exp2_pm64(double x, double& ep, double& em) {
     ep = (Cc + zs) * __hiloint2double((1023 + ni) << 20, 0);
     em = (Cc - zs) * __hiloint2double((1023 - ni) << 20, 0);
 }
-// 2^x for |x| < 1000 (rare paths): 2^n e^{f ln 2}, f = x - n in [-1/2, 1/2], degree 10 (< 1e-13)
-__device__ __forceinline__ double exp2_64(double x) {
-    const double magic = 6755399441055744.0;  // 1.5 * 2^52: x + magic rounds x to an integer
-    const double tn = x + magic;
-    const double n = tn - magic;
-    const double z = (x - n) * 0.6931471805599453;
-    double p = fma(z, 1.0 / 3628800.0, 1.0 / 362880.0);
-    p = fma(z, p, 1.0 / 40320.0);
-    p = fma(z, p, 1.0 / 5040.0);
-    p = fma(z, p, 1.0 / 720.0);
-    p = fma(z, p, 1.0 / 120.0);
-    p = fma(z, p, 1.0 / 24.0);
-    p = fma(z, p, 1.0 / 6.0);
-    p = fma(z, p, 0.5);
-    p = fma(z, p, 1.0);
-    p = fma(z, p, 1.0);
-    const int ni = __double2loint(tn);  // low word of x + magic = n (two's complement)
-    return p * __hiloint2double((ni + 1023) << 20, 0);
-}
-
 // ------------------------------------------------------------------ forward
 #ifndef GPAIR_FWD_MINB
 #define GPAIR_FWD_MINB 3
@@ -1596,6 +1576,7 @@ cudaError_t adj_dispatch_gen(gpair_ctx* c, const float* resid, const EpiParams& 
 // Which adjoint kernel a context uses (gpair_info.adj_kernel).
 int adjoint_kernel(const gpair_ctx* c) {
     if (c->ser == SER_GEN) return ADJ_LANE_KERNEL;
+    if (c->mp_on) return ADJ_MP;
     const bool fast = c->ser == 0 || c->ser == SER_FAST5;
     if (fast && c->tab.on && c->d_gpart) {
         if (c->d_gtab && adj_lcf_smem(c) <= 227 * 1024 && !(c->dbg & DBG_ADJ_NO_LCF)) return ADJ_LCF;
@@ -1613,6 +1594,7 @@ cudaError_t adj_dispatch(gpair_ctx* c, const float* resid, const EpiParams& ep, 
     if constexpr (MODE != MODE_COUNT) {
         if (c->ser == SER_GEN) return adj_dispatch_gen<MODE>(c, resid, ep, st);
         const bool deg5 = c->ser == SER_FAST5;
+        if (adjoint_kernel(c) == ADJ_MP) return launch_mp_adjoint(c, resid, MODE, ep, st);
         if (adjoint_kernel(c) == ADJ_LCF) {
             switch (c->k.cnt_int) {
                 case 12: return deg5 ? adj_lcf_launch<12, MODE, 5>(c, resid, ep, st) : adj_lcf_launch<12, MODE, 2>(c, resid, ep, st);
@@ -1735,6 +1717,7 @@ cudaError_t launch_adjoint_gather(gpair_ctx* c, int mode, const EpiParams& ep, c
 }
 
 int adjoint_groups(const gpair_ctx* c) {
+    if (adjoint_kernel(c) == ADJ_MP) return mp_groups(c);
     const int nw = adjoint_kernel(c) == ADJ_LCF ? LCF_WARPS : ADJT_WARPS;
     return (c->Nd + 32 * nw - 1) / (32 * nw);
 }

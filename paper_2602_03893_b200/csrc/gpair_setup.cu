@@ -586,6 +586,7 @@ cudaError_t build_geometry(gpair_ctx* c, const float* centers, const float* sens
     SETUP_CHECK(dmalloc(c, &c->d_y, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_delta, (size_t)Nd * c->Nt));
     SETUP_CHECK(dmalloc(c, &c->d_loss_part, Nd));
+    SETUP_CHECK(mp_setup(c, st, why));  // moment-polynomial adjoint (gpair_mp.cu), when eligible
     SETUP_CHECK(cudaStreamSynchronize(st));
     return cudaSuccess;
 }

@@ -1,14 +1,15 @@
 """GPU parity of every forward / adjoint kernel path of the common configuration.
 
 The bench configuration (degree-2 series, full windows of W = 16 samples)
-runs the factorised-Gaussian forward (TAB) and the lane-centred adjoint
-(k_adjoint_lcf).  The other kernels of the same configuration -- the TAB
-sensor-lane adjoint (k_adjoint_t), the per-sample sensor-lane adjoint
-(k_adjoint_sl), the lane-per-kernel adjoint (k_adjoint) and the
-per-sample-exponential forward -- are the fallbacks for contexts the fast
-kernels do not cover; the library selects them at create time, and the
-environment switches GPAIR_NO_TAB / GPAIR_ADJ_NO_LCF / GPAIR_ADJ_NO_T force
-them here so each is held to the same oracle gate (DESIGN.md sections 5, 6).
+runs the factorised-Gaussian forward (TAB) and the moment-polynomial adjoint
+(k_adjoint_mp).  The other kernels of the same configuration -- the
+lane-centred sensor-lane adjoint (k_adjoint_lcf), the TAB sensor-lane adjoint
+(k_adjoint_t), the per-sample sensor-lane adjoint (k_adjoint_sl), the
+lane-per-kernel adjoint (k_adjoint) and the per-sample-exponential forward --
+are the fallbacks for contexts the fast kernels do not cover; the library
+selects them at create time, and the environment switches GPAIR_NO_TAB /
+GPAIR_ADJ_NO_MP / GPAIR_ADJ_NO_LCF / GPAIR_ADJ_NO_T force them here so each is
+held to the same oracle gate (DESIGN.md sections 5, 6).
 """
 import numpy as np
 import pytest
@@ -24,18 +25,21 @@ pytestmark = pytest.mark.gpu
 
 # switches -> (info.tab, info.adj_kernel)
 PATHS = {
-    "tab+lcf": ({}, (1, 2)),
-    "tab+lane_t": ({"GPAIR_ADJ_NO_LCF": "1"}, (1, 1)),
-    "tab+lane_kernel": ({"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, (1, 0)),
-    "per_sample_exp+lane_sl": ({"GPAIR_NO_TAB": "1"}, (0, 3)),
-    "per_sample_exp+lane_kernel": ({"GPAIR_NO_TAB": "1", "GPAIR_ADJ_NO_T": "1"}, (0, 0)),
+    "tab+mp": ({}, (1, 4)),
+    "tab+lcf": ({"GPAIR_ADJ_NO_MP": "1"}, (1, 2)),
+    "tab+lane_t": ({"GPAIR_ADJ_NO_MP": "1", "GPAIR_ADJ_NO_LCF": "1"}, (1, 1)),
+    "tab+lane_kernel": ({"GPAIR_ADJ_NO_MP": "1", "GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, (1, 0)),
+    "per_sample_exp+mp": ({"GPAIR_NO_TAB": "1"}, (0, 4)),
+    "per_sample_exp+lane_sl": ({"GPAIR_NO_TAB": "1", "GPAIR_ADJ_NO_MP": "1"}, (0, 3)),
+    "per_sample_exp+lane_kernel": ({"GPAIR_NO_TAB": "1", "GPAIR_ADJ_NO_MP": "1", "GPAIR_ADJ_NO_T": "1"}, (0, 0)),
     # sensor-group pipeline of gpair_iterate (opt-in): forward / reducer / adjoint per 256-sensor group
-    "tab+lcf+pipeline": ({"GPAIR_PIPELINE": "1"}, (1, 2)),
-    "per_sample_exp+lane_sl+pipeline": ({"GPAIR_NO_TAB": "1", "GPAIR_PIPELINE": "1"}, (0, 3)),
+    "tab+mp+pipeline": ({"GPAIR_PIPELINE": "1"}, (1, 4)),
+    "tab+lcf+pipeline": ({"GPAIR_PIPELINE": "1", "GPAIR_ADJ_NO_MP": "1"}, (1, 2)),
+    "per_sample_exp+lane_sl+pipeline": ({"GPAIR_NO_TAB": "1", "GPAIR_PIPELINE": "1", "GPAIR_ADJ_NO_MP": "1"}, (0, 3)),
     # register-window forward (opt-in)
-    "tab_union+lcf": ({"GPAIR_FWD_UNION": "1"}, (1, 2)),
+    "tab_union+mp": ({"GPAIR_FWD_UNION": "1"}, (1, 4)),
 }
-ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE", "GPAIR_FWD_UNION")
+ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_MP", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE", "GPAIR_FWD_UNION")
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -122,14 +126,14 @@ def test_iterate_each_path_teacher_forced(path, mode, monkeypatch):
 
 
 def test_bench_configuration_uses_fast_paths(monkeypatch):
-    """cfg2 / cfg4 geometry (the bench's) selects the TAB forward and the LCF adjoint."""
+    """cfg2 / cfg4 geometry (the bench's) selects the TAB forward and the moment-polynomial adjoint."""
     for key in ENV_KEYS:
         monkeypatch.delenv(key, raising=False)
     cfg = inputs.CONFIGS["cfg2"]
     ctx = gpair.Context(T(cfg.centers()), T(cfg.sensors()), sigma=cfg.sig, v=cfg.v, fs=cfg.fs,
                         n_samples=cfg.n_samples, t0=cfg.t0, k=cfg.k)
     info = ctx.info()
-    assert info["tab"] == 1 and info["adj_kernel"] == 2, info
+    assert info["tab"] == 1 and info["adj_kernel"] == 4, info
     ctx.close()
 
 
@@ -151,8 +155,10 @@ def test_fast_paths_random_geometry(seed, monkeypatch):
     rmax = float(np.max(np.linalg.norm(s[:, :, None] - c[:, None, :].mean(axis=2, keepdims=True), axis=0)))
     n_samples = int((rmax / v - t0) * fs) + int(rng.integers(-8, 24))  # some windows reach past the record
     op = dict(sigma=sigma, v=v, fs=fs, n_samples=n_samples, t0=t0, k=3.0)
-    ctx = make_ctx(c, s, op, monkeypatch, {})
+    # even seeds: the moment-polynomial adjoint; odd seeds: the lane-centred one
+    ctx = make_ctx(c, s, op, monkeypatch, {} if seed % 2 == 0 else {"GPAIR_ADJ_NO_MP": "1"})
     info = ctx.info()
+    assert info["adj_kernel"] == (4 if seed % 2 == 0 else 2), info
     x = rng.random(c.shape[1]).astype(np.float32)
     check(ctx.forward(T(x)).cpu().numpy(), oracle.forward(c, x, s, **op), f"seed {seed} W {W} forward")
     d = rng.standard_normal((s.shape[1], n_samples)).astype(np.float32)
@@ -171,7 +177,7 @@ def test_per_sample_sensor_lane_adjoint(W, monkeypatch):
     c = inputs.grid_centers(10, 9, 8, sigma)
     s = inputs.hemisphere(48, 60e-3)
     op = dict(sigma=sigma, v=v, fs=fs, n_samples=1900 + 2 * W, t0=2e-6, k=3.0)
-    ctx = make_ctx(c, s, op, monkeypatch, {})
+    ctx = make_ctx(c, s, op, monkeypatch, {"GPAIR_ADJ_NO_MP": "1"})
     info = ctx.info()
     assert info["adj_kernel"] == 3 and info["tab"] == 0, info
     rng = np.random.default_rng(W)
