@@ -612,7 +612,7 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->near_rows = c->n_near_rows;
     o->near_pairs = c->n_near;
     o->tab = ((c->ser == 0 || c->ser == gpair::SER_FAST5) && c->tab.on) ? 1 : 0;
-    o->adj_kernel = c->assa ? 0 : gpair::adjoint_kernel(c);
+    o->adj_kernel = c->assa ? (c->mp_on ? gpair::ADJ_MP : 0) : gpair::adjoint_kernel(c);
     o->collective = c->coll;
     o->fwd_union = c->f_union;
     return GPAIR_OK;

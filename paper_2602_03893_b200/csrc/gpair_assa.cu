@@ -191,8 +191,8 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
 
 // zero-fill + correlation (Eqs. 15-16): dconv_j[q] = sum_{n: |alpha n - q| <= K} h[alpha n - q] delta_j[n]
 __global__ void k_assa_dconv(const float* __restrict__ resid, const float* __restrict__ taps, OpConst k,
-                             float* __restrict__ dconv) {
-    const int j = blockIdx.y;
+                             float* __restrict__ dconv, int64_t ld, int32_t pad, int32_t j0) {
+    const int j = j0 + blockIdx.y;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     const int Nup = k.alpha * k.Nt;
     if (q >= Nup) return;
@@ -202,7 +202,7 @@ __global__ void k_assa_dconv(const float* __restrict__ resid, const float* __res
     const int nhi = min(k.Nt - 1, (q + k.K) / k.alpha);
     float acc = 0.f;
     for (int n = nlo; n <= nhi; ++n) acc = fmaf(taps[k.alpha * n - q + k.K], dj[n], acc);
-    dconv[(int64_t)j * Nup + q] = acc;
+    dconv[(int64_t)j * ld + pad + q] = acc;
 }
 
 constexpr int MODE_COUNT = 3;
@@ -339,15 +339,21 @@ cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st) {
 }
 
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
-    const int Nup = c->k.alpha * c->Nt;
-    dim3 g((Nup + 255) / 256, c->Nd);
-    ++c->n_launch;
-    k_assa_dconv<<<g, 256, 0, st>>>(resid, c->d_taps, c->k, c->d_dconv);
-    cudaError_t e = cudaGetLastError();
+    if (c->mp_on) return launch_mp_adjoint(c, resid, mode, ep, st);  // gpair_mp.cu
+    cudaError_t e = launch_assa_dconv(c, resid, c->d_dconv, (int64_t)c->k.alpha * c->Nt, 0, 0, c->Nd, st);
     if (e != cudaSuccess) return e;
     if (mode == EPI_GRAD) return assa_adj_dispatch<EPI_GRAD>(c, ep, st);
     if (mode == EPI_NPC_ADAM) return assa_adj_dispatch<EPI_NPC_ADAM>(c, ep, st);
     return assa_adj_dispatch<EPI_CLAMP>(c, ep, st);
+}
+
+cudaError_t launch_assa_dconv(gpair_ctx* c, const float* resid, float* out, int64_t ld, int pad, int j0, int nj,
+                              cudaStream_t st) {
+    const int Nup = c->k.alpha * c->Nt;
+    dim3 g((Nup + 255) / 256, nj);
+    ++c->n_launch;
+    k_assa_dconv<<<g, 256, 0, st>>>(resid, c->d_taps, c->k, out, ld, pad, j0);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st) {

@@ -196,6 +196,9 @@ int assa_forward_warps();
 cudaError_t launch_assa_forward(gpair_ctx* c, cudaStream_t st);
 cudaError_t launch_assa_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st);
 cudaError_t launch_assa_count(gpair_ctx* c, cudaStream_t st);
+// zero-fill + correlation (Eqs. 15-16) of sensors [j0, j0 + nj) into out[j][pad + q], row stride ld
+cudaError_t launch_assa_dconv(gpair_ctx* c, const float* resid, float* out, int64_t ld, int pad, int j0, int nj,
+                              cudaStream_t st);
 
 // general operator (gpair_near.cu)
 cudaError_t build_general(gpair_ctx* c, cudaStream_t st, std::string& why, int& geom_err);

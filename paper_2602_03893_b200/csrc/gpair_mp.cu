@@ -64,11 +64,13 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, unsigne
                  ::"r"(mp_saddr(dst)), "l"(src), "r"(bytes), "r"(mp_saddr(bar)) : "memory");
 }
 
-// Thread per (region, sensor): the range of n_lo over the region's groups, from the fp64
-// group anchors: n_lo = floor(e - ku) + 1, e = (r / v - t0) f_s, r in [R - rad, R + rad]
-// (one sample of margin on each side).  MP_EMPTY when no window reaches the record.
+// Thread per (region, sensor): the range of staged rows over the region's groups, from the
+// fp64 group anchors, e = (r / v - t0) f_s, r in [R - rad, R + rad], one row of margin each side:
+//   exact operator: n_lo = floor(e - ku) + 1 (start sample of the window);
+//   ASSA (row f1):  k_ij = floor(alpha e + 1/2) (upsampled index, Eq. 9).
+// MP_EMPTY when no window / impulse reaches the record.
 __global__ void k_mp_windows(const float4* __restrict__ grp, int32_t ncells, const float* __restrict__ sens,
-                             int32_t cpr, int32_t nregions, OpConst k, int32_t* wlo, int* maxlen) {
+                             int32_t cpr, int32_t nregions, OpConst k, int32_t assa, int32_t* wlo, int* maxlen) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= (int64_t)nregions * k.Nd) return;
     const int j = (int)(t % k.Nd);
@@ -82,14 +84,19 @@ __global__ void k_mp_windows(const float4* __restrict__ grp, int32_t ncells, con
             const float4 G = grp[(int64_t)cc * GPC + gq];
             const double dx = (double)G.x - sx, dy = (double)G.y - sy, dz = (double)G.z - sz;
             const double R = sqrt(dx * dx + dy * dy + dz * dz), rad = G.w;
-            const double elo = fma(R - rad, k.inv_h, -k.t0fs) - ku;
-            const double ehi = fma(R + rad, k.inv_h, -k.t0fs) - ku;
-            lo = min(lo, (int)floor(elo));
-            hi = max(hi, (int)floor(ehi) + 2);
+            const double elo = fma(R - rad, k.inv_h, -k.t0fs);
+            const double ehi = fma(R + rad, k.inv_h, -k.t0fs);
+            if (assa) {
+                lo = min(lo, (int)floor(k.alpha * elo + 0.5) - 1);
+                hi = max(hi, (int)floor(k.alpha * ehi + 0.5) + 1);
+            } else {
+                lo = min(lo, (int)floor(elo - ku));
+                hi = max(hi, (int)floor(ehi - ku) + 2);
+            }
         }
     }
-    const int W = k.cnt_int;
-    if (lo > hi || hi < -(W - 1) || lo > k.Nt - 1) {
+    const int rmin = assa ? 0 : -(k.cnt_int - 1), rmax = assa ? k.alpha * k.Nt - 1 : k.Nt - 1;
+    if (lo > hi || hi < rmin || lo > rmax) {
         wlo[(int64_t)r * k.Nd + j] = MP_EMPTY;
         return;
     }
@@ -153,9 +160,22 @@ __device__ __noinline__ double mp_rare(float4 G, float4 d4, const float* __restr
     return (double)pw.w * s;
 }
 
+// Rare ASSA pair: assa_setup (exact-ToF anchors, fp64 re-decision of k_ij near a rounding
+// edge, bit-identical to the oracle); the impulse exists only inside the upsampled record.
+template <int SDEG>
+__device__ __noinline__ double mp_rare_assa(float4 G, float4 d4, const float* __restrict__ orig, int64_t gi,
+                                            int64_t Mpad, const float* __restrict__ sens, int j,
+                                            const float* __restrict__ dtab, int32_t NtP, int32_t pad, const OpConst k) {
+    const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
+    const Anchor a = make_anchor(G, sx, sy, sz, k);
+    const AssaPair p = assa_setup<SDEG>(a, d4, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+    if ((unsigned)p.k >= (unsigned)(k.alpha * k.Nt)) return 0.0;
+    return (double)(p.w * dtab[(int64_t)j * NtP + p.k + pad]);
+}
+
 constexpr int MP_NS = 5;  // staged batches in flight (ring of full mbarriers)
 
-template <int SDEG>
+template <int SDEG, bool ASSA>
 __global__ void __launch_bounds__(256, 3)
     k_adjoint_mp(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const char* __restrict__ Mt,
@@ -164,7 +184,8 @@ __global__ void __launch_bounds__(256, 3)
     static_assert(MP_SB == 8, "anchor layout: lane = (sensor lane % 8, group lane / 8)");
     extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int sbytes = MP_SB * Lr2 * MP_ROW;                       // bytes per staged batch
+    constexpr int ROW = ASSA ? 4 : MP_ROW;                          // bytes per staged row
+    const int sbytes = MP_SB * Lr2 * ROW;                           // bytes per staged batch
     char* s_M = (char*)smem8;                                       // [MP_NS][MP_SB][Lr2] rows
     float4* s_anc = (float4*)(s_M + MP_NS * sbytes);                // [nw][GPC][MP_ANC_GSTRIDE]
     uint64_t* bar = (uint64_t*)(s_anc + nw * GPC * MP_ANC_GSTRIDE); // full[MP_NS]
@@ -181,7 +202,9 @@ __global__ void __launch_bounds__(256, 3)
     const int jg0 = (blockIdx.y + k.grp0) * MP_SG;
     const int jg1 = min(jg0 + MP_SG, k.Nd);
     const int nb = (jg1 - jg0 + MP_SB - 1) / MP_SB;
-    const unsigned rowbytes = (unsigned)Lr2 * MP_ROW;
+    const unsigned rowbytes = (unsigned)Lr2 * ROW;
+    // first table row of a sensor's staged block (ASSA: 16-B aligned, Lr2 % 4 == 0)
+    auto row0 = [&](int lo) { return lo == MP_EMPTY ? 0 : (ASSA ? ((lo + pad) & ~3) : lo + W - 1 + pad); };
 
     // batch b's rows [lo_j, lo_j + Lr2) of every sensor by 1-D TMA into stage b % MP_NS
     // (an empty sensor copies zero rows of the table); issued by one thread
@@ -191,9 +214,8 @@ __global__ void __launch_bounds__(256, 3)
         mbar_expect_tx(full, (unsigned)nj * rowbytes);
         char* dst = s_M + (b % MP_NS) * sbytes;
         for (int jj = 0; jj < nj; ++jj) {
-            const int lo = __ldg(wrow + jb + jj);
-            const int ra0 = lo == MP_EMPTY ? 0 : lo + W - 1 + pad;
-            tma_bulk_g2s(dst + jj * rowbytes, Mt + ((int64_t)(jb + jj) * NtP + ra0) * MP_ROW, rowbytes, full);
+            const int ra0 = row0(__ldg(wrow + jb + jj));
+            tma_bulk_g2s(dst + jj * rowbytes, Mt + ((int64_t)(jb + jj) * NtP + ra0) * ROW, rowbytes, full);
         }
     };
     if (threadIdx.x == 0) {
@@ -210,6 +232,10 @@ __global__ void __launch_bounds__(256, 3)
     const f2_t kx = pk2(d4.x, d4.x), ky = pk2(d4.y, d4.y), kz = pk2(d4.z, d4.z), kw = pk2(d4.w, d4.w);
     const f2_t clo = pk2(k.c_lo, k.c_lo), mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
     const f2_t c1x = pk2(1.f + xi0, 1.f + xi0);
+    const f2_t alf = pk2((float)k.alpha, (float)k.alpha), half = pk2(0.5f, 0.5f), nhalf = pk2(-0.5f, -0.5f);
+    const f2_t two_h = pk2(k.two_over_h, k.two_over_h);
+    const float gam_a = 0.5f - GAMMA * (float)k.alpha;
+    float accf = 0.f;  // ASSA: per-batch fp32 sum (one gather per pair), folded into acc
     // this lane's anchor job: sensor jj = lane % 8 of the batch, group gq = lane / 8 of the cell
     const int ajj = lane & (MP_SB - 1), agq = lane >> 3;
     float* aslot = (float*)(s_anc + (warp * GPC + agq) * MP_ANC_GSTRIDE + (ajj >> 1) * 4) + (ajj & 1);
@@ -236,6 +262,9 @@ __global__ void __launch_bounds__(256, 3)
         const int lo_l = lo_n;
         if (cok && lo_l != MP_EMPTY) {
             const Anchor a = make_anchor(Gq, sxn, syn, szn, k);
+            // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
+            const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
+                                  : a.na - lo_l - (RND_MAGIC_BITS - 1);
             aslot[0] = a.Ux;
             aslot[2] = a.Uy;
             aslot[4] = a.Uz;
@@ -243,7 +272,7 @@ __global__ void __launch_bounds__(256, 3)
             aslot[8] = a.invR2;
             aslot[10] = a.inv2Rh;
             aslot[12] = a.h2R;
-            aslot[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : a.na - lo_l - (RND_MAGIC_BITS - 1));
+            aslot[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : nrel);
         }
         const unsigned live = __ballot_sync(0xffffffffu, lo_l != MP_EMPTY) & ((1u << MP_SB) - 1u);
         prefetch(b + 1);
@@ -263,6 +292,27 @@ __global__ void __launch_bounds__(256, 3)
                 f2_t S, Tw;
                 series2<SDEG>(eps, S, Tw);
                 const f2_t eu = fma2(mul2(q, pk2(A2.z, A2.w)), S, pk2(A1.z, A1.w));
+                if constexpr (ASSA) {
+                    // k_ij = alpha n_a + floor(alpha eu + 1/2), w = A / r (assa_pre's arithmetic, A = 1)
+                    const f2_t w2 = mul2(mul2(pk2(A3.x, A3.y), Tw), two_h);
+                    const f2_t xa = fma2(alf, eu, half);
+                    const f2_t t = add2(add2(xa, nhalf), mag);
+                    const f2_t fl = add2(t, nmag);
+                    const f2_t dd = sub2(sub2(xa, fl), half);
+                    float t0, t1, d0, d1, wa, wb;
+                    upk2(t, t0, t1);
+                    upk2(dd, d0, d1);
+                    upk2(w2, wa, wb);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        if (!((lv >> h) & 1u)) continue;  // warp-uniform
+                        const int row = (int)((unsigned)__float_as_int(h ? A3.w : A3.z) + (unsigned)__float_as_int(h ? t1 : t0));
+                        const bool rare = fabsf(h ? d1 : d0) > gam_a || (unsigned)row >= (unsigned)Lr2;
+                        rmask |= (unsigned)rare << (2 * p + h);
+                        const float dv = *(const float*)(stage + ((2 * p + h) * Lr2 + min((unsigned)row, (unsigned)Lr2 - 1u)) * 4);
+                        accf = fmaf(rare ? 0.f : (h ? wb : wa), dv, accf);  // Eq. 17
+                    }
+                } else {
                 const f2_t w2 = mul2(pk2(A3.x, A3.y), Tw);
                 const f2_t x = add2(eu, clo);  // alpha - 1/2, alpha = eu - ku
                 const f2_t t = add2(x, mag);
@@ -294,11 +344,20 @@ __global__ void __launch_bounds__(256, 3)
                     pv = fma(pv, X, m01.x);
                     acc = fma((double)w, pv, acc);
                 }
+                }
             }
-            while (rmask) {  // rare pairs of this batch (ambiguous edges, exact-ToF groups)
+            if (ASSA) {
+                acc += (double)accf;
+                accf = 0.f;
+            }
+            while (rmask) {  // rare pairs of this batch (ambiguous edges / indices, exact-ToF groups)
                 const int jj = __ffs(rmask) - 1;
                 rmask &= rmask - 1u;
-                acc += mp_rare<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, resid, k, K64);
+                if (ASSA)
+                    acc += mp_rare_assa<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, (const float*)Mt, NtP,
+                                              pad, k);
+                else
+                    acc += mp_rare<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, resid, k, K64);
             }
         }
         // the last warp done with stage s refills it with batch b + MP_NS (no producer convoy): lane 0
@@ -316,9 +375,8 @@ __global__ void __launch_bounds__(256, 3)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             if (lane == 0) mbar_expect_tx(bar + s, (unsigned)njn * rowbytes);
             if (lane < njn) {
-                const int lo = __ldg(wrow + jbn + lane);
-                const int ra0 = lo == MP_EMPTY ? 0 : lo + W - 1 + pad;
-                tma_bulk_g2s(s_M + s * sbytes + lane * rowbytes, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * MP_ROW,
+                const int ra0 = row0(__ldg(wrow + jbn + lane));
+                tma_bulk_g2s(s_M + s * sbytes + lane * rowbytes, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
                              rowbytes, bar + s);
             }
         }
@@ -326,8 +384,9 @@ __global__ void __launch_bounds__(256, 3)
     if (cok) gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + gi] = (gacc_t)acc;
 }
 
-size_t mp_smem(int Lr2, int nw) {
-    return (size_t)MP_NS * MP_SB * Lr2 * MP_ROW + (size_t)nw * GPC * MP_ANC_GSTRIDE * 16 + MP_NS * 8 + MP_NS * 4;
+size_t mp_smem(int Lr2, int nw, bool assa) {
+    return (size_t)MP_NS * MP_SB * Lr2 * (assa ? 4 : MP_ROW) + (size_t)nw * GPC * MP_ANC_GSTRIDE * 16 + MP_NS * 8 +
+           MP_NS * 4;
 }
 
 // Degree-7 interpolation of f(xi0 + xi - m), m < W, at the Chebyshev nodes of [-1/2, 1/2]
@@ -375,26 +434,31 @@ double mp_fit(int W, double K, std::vector<double>& coef) {
     return fmax > 0.0 ? err / fmax : 1.0;
 }
 
-template <int SDEG>
+template <int SDEG, bool ASSA>
 cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     const int G = (c->Nd + MP_SG - 1) / MP_SG;
     const int g0 = c->lng > 0 ? c->lg0 : 0;
     const int ng = c->lng > 0 ? std::min(c->lng, G - g0) : G;
     const int j0 = g0 * MP_SG, nj = std::min(c->Nd, (g0 + ng) * MP_SG) - j0;
     const int W = c->k.cnt_int;
-    ++c->n_launch;
-    k_mp_prep<<<dim3((unsigned)((c->Nt + W - 1 + 127) / 128), (unsigned)nj), 128, (size_t)W * 64, st>>>(
-        resid, c->d_mp_coef, W, c->Nt, c->mp_NtP, c->mp_pad, j0, (char*)c->d_mp);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    if (ASSA) {  // zero-fill + correlation (Eqs. 15-16) into the padded table
+        e = launch_assa_dconv(c, resid, (float*)c->d_mp, c->mp_NtP, c->mp_pad, j0, nj, st);
+    } else {
+        ++c->n_launch;
+        k_mp_prep<<<dim3((unsigned)((c->Nt + W - 1 + 127) / 128), (unsigned)nj), 128, (size_t)W * 64, st>>>(
+            resid, c->d_mp_coef, W, c->Nt, c->mp_NtP, c->mp_pad, j0, (char*)c->d_mp);
+        e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
-    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr);
-    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, ASSA);
+    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     OpConst kk = c->k;
     kk.grp0 = g0;
     const double K64 = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
     ++c->n_launch;
-    k_adjoint_mp<SDEG><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
+    k_adjoint_mp<SDEG, ASSA><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
         c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_m, (const char*)c->d_mp, resid, c->d_gpart, c->mp_cpr, c->ncells,
         c->mp_Lr2, c->mp_NtP, c->mp_pad, c->Mpad, kk, (float)(0.5 * W - 0.5), K64);
     e = cudaGetLastError();
@@ -408,7 +472,9 @@ cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParam
 int mp_groups(const gpair_ctx* c) { return (c->Nd + MP_SG - 1) / MP_SG; }
 
 cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
-    return c->ser == SER_FAST5 ? mp_launch<5>(c, resid, mode, ep, st) : mp_launch<2>(c, resid, mode, ep, st);
+    if (c->assa)
+        return c->series_small ? mp_launch<2, true>(c, resid, mode, ep, st) : mp_launch<5, true>(c, resid, mode, ep, st);
+    return c->ser == SER_FAST5 ? mp_launch<5, false>(c, resid, mode, ep, st) : mp_launch<2, false>(c, resid, mode, ep, st);
 }
 
 // Create-time set-up: eligibility (exact-integer window on the fast anchor paths), the
@@ -416,13 +482,19 @@ cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const 
 cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
     c->mp_on = 0;
     const int W = c->k.cnt_int;
-    if (W < 3 || W > 128 || (c->ser != 0 && c->ser != SER_FAST5) || c->assa || c->gen || !c->d_gpart ||
-        (c->dbg & DBG_ADJ_NO_MP))
-        return cudaSuccess;
-    const double K = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
+    const bool assa = c->assa != 0;
+    if (c->gen || (c->dbg & DBG_ADJ_NO_MP)) return cudaSuccess;
     std::vector<double> coef;
-    c->mp_fit_err = mp_fit(W, K, coef);
-    if (!(c->mp_fit_err <= MP_TOL)) return cudaSuccess;  // short Gaussians: the LCF / sensor-lane kernels
+    if (!assa) {
+        if (W < 3 || W > 128 || (c->ser != 0 && c->ser != SER_FAST5) || !c->d_gpart) return cudaSuccess;
+        const double K = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
+        c->mp_fit_err = mp_fit(W, K, coef);
+        if (!(c->mp_fit_err <= MP_TOL)) return cudaSuccess;  // short Gaussians: the LCF / sensor-lane kernels
+    } else if (!c->d_gpart) {  // ASSA contexts with a non-integer window: the group partials are ours
+        cudaError_t ea = cudaMalloc(&c->d_gpart, sizeof(gacc_t) * (size_t)((c->Nd + 127) / 128) * c->Mpad);
+        if (ea != cudaSuccess) return ea;
+        c->workspace_bytes += (int64_t)sizeof(gacc_t) * ((c->Nd + 127) / 128) * c->Mpad;
+    }
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
     int cpr = 8;
@@ -441,7 +513,7 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
         if (e == cudaSuccess) {
             const int64_t nt = (int64_t)nreg * c->Nd;
             k_mp_windows<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(c->d_grp, c->ncells, c->d_sens, cpr, nreg, c->k,
-                                                                       wlo, d_len);
+                                                                       assa ? 1 : 0, wlo, d_len);
             e = cudaGetLastError();
         }
         if (e == cudaSuccess) e = cudaMemcpyAsync(&h_len, d_len, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -452,8 +524,9 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
             why = "gpair_mp.cu: window table";
             return e;
         }
-        const int Lr2 = std::max(h_len, 1);
-        if (mp_smem(Lr2, cpr) > 200 * 1024) {
+        // ASSA: 4-B rows, blocks start 16-B aligned (up to 3 rows earlier) and span a multiple of 4 rows
+        const int Lr2 = assa ? (std::max(h_len, 1) + 3 + 3) / 4 * 4 : std::max(h_len, 1);
+        if (mp_smem(Lr2, cpr, assa) > 200 * 1024) {
             cudaFree(wlo);
             if (cpr > 1) {
                 cpr /= 2;
@@ -470,11 +543,28 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
         break;
     }
     cudaFree(d_len);
-    c->mp_pad = c->mp_Lr2 + 1;  // zero rows on both sides: every staged block stays inside the table
-    c->mp_NtP = c->Nt + W - 1 + 2 * c->mp_pad;
-    const size_t nM = (size_t)c->Nd * c->mp_NtP * (MP_ROW / 8);  // doubles
+    size_t nM;  // doubles
+    if (assa) {  // dconv table [Nd][alpha Nt + 2 pad] fp32, pad a multiple of 4
+        c->mp_pad = (c->mp_Lr2 + 4 + 3) / 4 * 4;
+        c->mp_NtP = (c->k.alpha * c->Nt + 2 * c->mp_pad + 3) / 4 * 4;  // rows of every sensor start 16-B aligned
+        nM = ((size_t)c->Nd * c->mp_NtP + 1) / 2;
+    } else {
+        c->mp_pad = c->mp_Lr2 + 1;  // zero rows on both sides: every staged block stays inside the table
+        c->mp_NtP = c->Nt + W - 1 + 2 * c->mp_pad;
+        nM = (size_t)c->Nd * c->mp_NtP * (MP_ROW / 8);
+    }
     e = cudaMalloc(&c->d_mp, nM * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_mp, 0, nM * sizeof(double), st);
+    if (assa) {
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) {
+            why = "gpair_mp.cu: dconv table";
+            return e;
+        }
+        c->workspace_bytes += (int64_t)nM * sizeof(double);
+        c->mp_on = 1;
+        return cudaSuccess;
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_mp_coef, coef.size() * sizeof(double));
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(c->d_mp_coef, coef.data(), coef.size() * sizeof(double), cudaMemcpyHostToDevice, st);

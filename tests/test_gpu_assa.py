@@ -26,7 +26,14 @@ def _built():
     build.build()
 
 
-def make_ctx(c, s, op, nmin=25):
+ADJ = {"mp": ({}, 4), "lane": ({"GPAIR_ADJ_NO_MP": "1"}, 0)}  # adjoint kernel: k_adjoint_mp / k_assa_adjoint
+
+
+def make_ctx(c, s, op, nmin=25, monkeypatch=None, adj="mp"):
+    if monkeypatch is not None:
+        monkeypatch.delenv("GPAIR_ADJ_NO_MP", raising=False)
+        for key, val in ADJ[adj][0].items():
+            monkeypatch.setenv(key, val)
     return gpair.Context(T(c), T(s), sigma=op["sigma"], v=op["v"], fs=op["fs"], n_samples=op["n_samples"],
                          t0=op["t0"], k=op["k"], assa=True, assa_nmin=nmin)
 
@@ -48,13 +55,15 @@ def impulse_count(c, s, op, alpha):
     return n
 
 
-def test_cfg1_assa_forward_adjoint_full():
+@pytest.mark.parametrize("adj", list(ADJ))
+def test_cfg1_assa_forward_adjoint_full(adj, monkeypatch):
     cfg = inputs.CONFIGS["cfg1"]
     c, s, op = cfg.centers(), cfg.sensors(), cfg.op_kwargs()
-    ctx = make_ctx(c, s, op)
+    ctx = make_ctx(c, s, op, monkeypatch=monkeypatch, adj=adj)
     p, kw = assa_kw(op)
     info = ctx.info()
     assert (info["assa"], info["assa_alpha"], info["assa_K"], info["assa_n_half"]) == (1, 2, 16, 8)
+    assert info["adj_kernel"] == ADJ[adj][1], info
     x = inputs.dense_amplitudes(cfg.M)
     y = ctx.forward(T(x)).cpu().numpy()
     assert_parity(y, oracle.assa_forward(c, x, s, n_samples=op["n_samples"], **kw), "cfg1 assa forward")
@@ -64,12 +73,14 @@ def test_cfg1_assa_forward_adjoint_full():
     assert ctx.count_pair_samples() == impulse_count(c, s, op, p["alpha"])
 
 
+@pytest.mark.parametrize("adj", list(ADJ))
 @pytest.mark.parametrize("seed", range(10))
-def test_assa_random_suite(seed):
+def test_assa_random_suite(seed, adj, monkeypatch):
     c, s, op = inputs.random_suite_case(seed)
     rng = np.random.default_rng(seed)
     nmin = [25, 25, 9, 41, 25][seed % 5]
-    ctx = make_ctx(c, s, op, nmin)
+    ctx = make_ctx(c, s, op, nmin, monkeypatch=monkeypatch, adj=adj)
+    assert ctx.info()["adj_kernel"] == ADJ[adj][1]
     p, kw = assa_kw(op, nmin)
     x = rng.random(c.shape[1]).astype(np.float32)
     y_ref = oracle.assa_forward(c, x, s, n_samples=op["n_samples"], **kw)
