@@ -32,6 +32,7 @@ UNIT = "pair-evals/s"
 # fp64 residual column) = SURVEY 8d's SFU rate of one exp per pair-sample (16 MUFU / clk / SM)
 PAIR_SAMPLES_PER_CLK_SM = 16
 ISSUE_PER_CLK_SM = 4  # warp instructions / clk / SM (4 SMSPs)
+MP_ROW_BYTES = 48  # k_adjoint_mp: one staged row of the moment table per pair (gpair_mp.cu)
 
 
 def parse():
@@ -309,9 +310,8 @@ def main():
         except Exception:
             side = {}
     names = {"forward": "k_assa_forward" if args.op == "assa" else "k_forward",
-             "adjoint": "k_assa_adjoint" if args.op == "assa" else
-             {0: "k_adjoint", 1: "k_adjoint_t", 2: "k_adjoint_lcf", 3: "k_adjoint_sl",
-              4: "k_adjoint_mp"}.get(info["adj_kernel"], "adjoint")}
+             "adjoint": {0: "k_assa_adjoint" if args.op == "assa" else "k_adjoint", 1: "k_adjoint_t",
+                         2: "k_adjoint_lcf", 3: "k_adjoint_sl", 4: "k_adjoint_mp"}.get(info["adj_kernel"], "adjoint")}
     if args.op == "exact":
         # units: in-window pair-samples, counted on the GPU for this context
         units, unit, bound = pair_samples_local, "Gpair-samples/s", "alu"
@@ -340,6 +340,18 @@ def main():
             kipp = side.get("instr_per_pair", {}).get(key)
             kpeak = n_sm * ISSUE_PER_CLK_SM * 32 * f_max / kipp if kipp else None
         per_kernel[names[key]] = {"ms": k_ms, "achieved": ach / 1e9, "frac": (ach / kpeak) if kpeak else None}
+        if key == "adjoint" and info["adj_kernel"] == 4 and args.op == "exact":
+            # the moment-polynomial adjoint reads one staged moment row per pair (no per-sample work,
+            # so its pair-sample rate exceeds the per-sample roofline above): its own bound is the
+            # shared-memory pipe at MP_ROW_BYTES per pair, 128 B / clk / SM; the launch also holds the
+            # moment prep and the group gather
+            row_b = MP_ROW_BYTES
+            pairs = Ml * cfg.n_sensors  # this rank's kernel shard
+            own_peak = n_sm * 128.0 / row_b * f_max
+            per_kernel[names[key]]["own_roofline"] = {
+                "bound": "smem", "unit": "Gpairs/s", "achieved": pairs / (k_ms * 1e-3) / 1e9,
+                "peak": own_peak / 1e9, "frac": pairs / (k_ms * 1e-3) / own_peak,
+                "peak_def": f"{n_sm} SMs x 128 B/clk / {row_b} B per pair x {f_max / 1e6:.0f} MHz"}
     achieved = units / (dom_ms * 1e-3)
     peak = peak_of(f_max) if peak_of else None
     roof = {"bound": bound, "kernel": names[dom], "achieved": achieved / 1e9,

@@ -43,6 +43,16 @@ constexpr int MP_SG = 256;         // sensors per CTA (blockIdx.y = sensor group
 constexpr int32_t MP_EMPTY = INT_MIN;
 constexpr double MP_TOL = 1e-8;    // max interpolation error / max |f| accepted at create (W >= 10 at k = 3)
 
+// GPAIR_MP_CHECK=1 (a variant build, scripts/gpu_mp_check.sh): device-side bounds checks of every
+// staged copy, table row and rare-path sample index; a violation traps (the launch fails loudly).
+#ifndef GPAIR_MP_CHECK
+#define GPAIR_MP_CHECK 0
+#endif
+#define MP_CHECK(cond)                        \
+    do {                                      \
+        if (GPAIR_MP_CHECK && !(cond)) __trap(); \
+    } while (0)
+
 __device__ __forceinline__ unsigned mp_saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mp_saddr(bar)), "r"(count) : "memory");
@@ -130,6 +140,7 @@ __global__ void k_mp_prep(const float* __restrict__ resid, const double* __restr
 #pragma unroll
         for (int q = 0; q < 8; ++q) a[q] = fma(c[q], dv, a[q]);
     }
+    MP_CHECK(row + pad >= 0 && row + pad < NtP);
     char* o = Mt + ((int64_t)j * NtP + row + pad) * MP_ROW;
     *(double2*)o = make_double2(a[0], a[1]);
     *(double2*)(o + 16) = make_double2(a[2], a[3]);
@@ -151,6 +162,7 @@ __device__ __noinline__ double mp_rare(float4 G, float4 d4, const float* __restr
     const float sx = sens[j], sy = sens[k.Nd + j], sz = sens[2 * k.Nd + j];
     const Anchor a = make_anchor(G, sx, sy, sz, k);
     const PairWin pw = pair_setup<SDEG>(a, d4, 1.f, orig, gi, Mpad, sx, sy, sz, k);
+    MP_CHECK(pw.cnt <= 0 || (pw.n_lo >= 0 && pw.n_lo + pw.cnt <= k.Nt));
     const float* d = resid + (int64_t)j * k.Nt + pw.n_lo;
     double s = 0.0;
     for (int m = 0; m < pw.cnt; ++m) {
@@ -173,7 +185,10 @@ __device__ __noinline__ double mp_rare_assa(float4 G, float4 d4, const float* __
     return (double)(p.w * dtab[(int64_t)j * NtP + p.k + pad]);
 }
 
-constexpr int MP_NS = 5;  // staged batches in flight (ring of full mbarriers)
+#ifndef GPAIR_MP_NS
+#define GPAIR_MP_NS 5
+#endif
+constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mbarriers)
 
 template <int SDEG, bool ASSA>
 __global__ void __launch_bounds__(256, 3)
@@ -215,6 +230,7 @@ __global__ void __launch_bounds__(256, 3)
         char* dst = s_M + (b % MP_NS) * sbytes;
         for (int jj = 0; jj < nj; ++jj) {
             const int ra0 = row0(__ldg(wrow + jb + jj));
+            MP_CHECK(jb + jj < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
             tma_bulk_g2s(dst + jj * rowbytes, Mt + ((int64_t)(jb + jj) * NtP + ra0) * ROW, rowbytes, full);
         }
     };
@@ -376,6 +392,7 @@ __global__ void __launch_bounds__(256, 3)
             if (lane == 0) mbar_expect_tx(bar + s, (unsigned)njn * rowbytes);
             if (lane < njn) {
                 const int ra0 = row0(__ldg(wrow + jbn + lane));
+                MP_CHECK(jbn + lane < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
                 tma_bulk_g2s(s_M + s * sbytes + lane * rowbytes, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
                              rowbytes, bar + s);
             }

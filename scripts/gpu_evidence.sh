@@ -15,7 +15,7 @@ echo "bench rc=$?" >> gpurun_out/bench_${TAG}.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv \
     python bench.py --config $CFG --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch_${TAG}.log 2>&1
 echo "launch list rc=$?"
-for K in k_forward k_adjoint_lcf "k_reduce\$"; do
+for K in k_forward k_adjoint_mp "k_reduce\$"; do
   KN=$(echo "$K" | tr -d '$\\')
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$K" -c 1 \
       -o gpurun_out/prof_${CFG}_${KN}_${TAG} -f python scripts/profile_once.py $CFG > gpurun_out/ncu_full_${KN}_${TAG}.log 2>&1
@@ -24,6 +24,12 @@ for K in k_forward k_adjoint_lcf "k_reduce\$"; do
   python scripts/sass_mix.py gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep 268435456 > gpurun_out/ncu_sassmix_${KN}_${TAG}.txt 2>&1
   [ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_${KN}_${TAG}.ncu-rep
 done
+# the ASSA adjoint on the moment-polynomial kernel
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_adjoint_mp -c 1 \
+    -o gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG} -f python scripts/profile_once.py $CFG assa > gpurun_out/ncu_full_assa_mp_${TAG}.log 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep > gpurun_out/ncu_summary_assa_k_adjoint_mp_${TAG}.txt 2>&1
+python scripts/sass_mix.py gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep 268435456 > gpurun_out/ncu_sassmix_assa_k_adjoint_mp_${TAG}.txt 2>&1
+[ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep
 # the other bench lines: the reference arm (fp64 oracle), the ASSA operator, cfg5 / cfg3
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1
 timeout 600 python bench.py --op assa --no-cpu-baseline > gpurun_out/bench_assa_${TAG}.log 2>&1

@@ -1,5 +1,5 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck / synccheck):
-TAB forward + LCF / sensor-lane / lane-per-kernel adjoints, the per-sample path, iterate
+TAB forward + moment-polynomial (TMA / mbarrier ring) / LCF / sensor-lane / lane-per-kernel adjoints, the per-sample path, iterate
 (NPC + clamp), ASSA, VCR and the near-field operator, on tiny instances."""
 import os
 import sys
@@ -34,9 +34,11 @@ def run(c, s, op, **kw):
 c = inputs.grid_centers(8, 8, 8, 1e-4)
 s = inputs.hemisphere(40, 60e-3)
 op = dict(sigma=1e-4, v=1500.0, fs=40e6, n_samples=2048, t0=0.0, k=3.0)
-KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE")
-for env in ({}, {"GPAIR_ADJ_NO_LCF": "1"}, {"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, {"GPAIR_NO_TAB": "1"},
-            {"GPAIR_PIPELINE": "1"}, {"GPAIR_PIPELINE": "1", "GPAIR_NO_TAB": "1"}):
+KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_MP", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE")
+NM = {"GPAIR_ADJ_NO_MP": "1"}
+for env in ({}, NM, dict(NM, GPAIR_ADJ_NO_LCF="1"), dict(NM, GPAIR_ADJ_NO_LCF="1", GPAIR_ADJ_NO_T="1"),
+            {"GPAIR_NO_TAB": "1"}, dict(NM, GPAIR_NO_TAB="1"), {"GPAIR_PIPELINE": "1"}, dict(NM, GPAIR_PIPELINE="1"),
+            {"GPAIR_PIPELINE": "1", "GPAIR_NO_TAB": "1"}):
     for key in KEYS:
         os.environ.pop(key, None)
     os.environ.update(env)
@@ -44,13 +46,20 @@ for env in ({}, {"GPAIR_ADJ_NO_LCF": "1"}, {"GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_
     print("path", env, "tab", info["tab"], "adj", info["adj_kernel"], flush=True)
 for key in KEYS:
     os.environ.pop(key, None)
-# the double-buffered cp.async forward and the LCF adjoint at other window lengths (W = 12, 24, 32)
-for W in (12, 24, 32):
-    sw = W * (1500.0 / 40e6) / 6.0
-    print("W", W, run(inputs.grid_centers(6, 6, 6, sw), s, dict(op, sigma=sw))["adj_kernel"], flush=True)
+# the double-buffered cp.async forward and the moment-polynomial / LCF adjoints at other window lengths
+for env in ({}, NM):
+    os.environ.update(env)
+    for W in (12, 24, 32):
+        sw = W * (1500.0 / 40e6) / 6.0
+        print("W", W, env, run(inputs.grid_centers(6, 6, 6, sw), s, dict(op, sigma=sw))["adj_kernel"], flush=True)
+    for key in KEYS:
+        os.environ.pop(key, None)
 cfg1 = inputs.CONFIGS["cfg1"]
 print("cfg1", run(cfg1.centers(), cfg1.sensors(), cfg1.op_kwargs())["adj_kernel"], flush=True)
-print("assa", run(c, s, op, assa=True)["assa"], flush=True)
+print("assa (moment-polynomial adjoint)", run(c, s, op, assa=True)["adj_kernel"], flush=True)
+os.environ["GPAIR_ADJ_NO_MP"] = "1"
+print("assa (lane-per-kernel adjoint)", run(c, s, op, assa=True)["adj_kernel"], flush=True)
+os.environ.pop("GPAIR_ADJ_NO_MP", None)
 sig = np.full(c.shape[1], 1e-4, np.float32)
 print("general", run(c, s, op, sigmas=T(sig))["general"], flush=True)
 # near field: sensors inside the grid
