@@ -190,8 +190,11 @@ __device__ __noinline__ double mp_rare_assa(float4 G, float4 d4, const float* __
 #endif
 constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mbarriers)
 
+#ifndef GPAIR_MP_MINB
+#define GPAIR_MP_MINB 3
+#endif
 template <int SDEG, bool ASSA>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     k_adjoint_mp(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const char* __restrict__ Mt,
                  const float* __restrict__ resid, gacc_t* __restrict__ gpart, int32_t cpr, int32_t ncells,
