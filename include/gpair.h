@@ -189,6 +189,8 @@ typedef struct {
     int32_t collective;         /* 1: kernel-sharded path (NCCL all-reduce of y, separate
                                    residual kernel): world > 1 or GPAIR_COLLECTIVE          */
     int32_t fwd_union;          /* 1: register-window forward (opt-in GPAIR_FWD_UNION=1) */
+    double adj_fit_err;         /* moment-polynomial adjoint: max error of the degree-7 interpolants of the
+                                   window weights / max |f| (create-time fit; 0 when not attempted)   */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial

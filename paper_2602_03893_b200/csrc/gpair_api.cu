@@ -615,6 +615,7 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->adj_kernel = c->assa ? (c->mp_on ? gpair::ADJ_MP : 0) : gpair::adjoint_kernel(c);
     o->collective = c->coll;
     o->fwd_union = c->f_union;
+    o->adj_fit_err = c->mp_fit_err;
     return GPAIR_OK;
 }
 

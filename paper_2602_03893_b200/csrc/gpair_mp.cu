@@ -494,7 +494,7 @@ int mp_groups(const gpair_ctx* c) { return (c->Nd + MP_SG - 1) / MP_SG; }
 cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     if (c->assa)
         return c->series_small ? mp_launch<2, true>(c, resid, mode, ep, st) : mp_launch<5, true>(c, resid, mode, ep, st);
-    return c->ser == SER_FAST5 ? mp_launch<5, false>(c, resid, mode, ep, st) : mp_launch<2, false>(c, resid, mode, ep, st);
+    return c->series_small ? mp_launch<2, false>(c, resid, mode, ep, st) : mp_launch<5, false>(c, resid, mode, ep, st);
 }
 
 // Create-time set-up: eligibility (exact-integer window on the fast anchor paths), the
@@ -506,11 +506,14 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
     if (c->gen || (c->dbg & DBG_ADJ_NO_MP)) return cudaSuccess;
     std::vector<double> coef;
     if (!assa) {
-        if (W < 3 || W > 128 || (c->ser != 0 && c->ser != SER_FAST5) || !c->d_gpart) return cudaSuccess;
+        // any exact-integer window (cnt_int > 0; not only the forward's template sizes) on the
+        // anchor series paths (degree 2 when every |eps| <= EPS_SMALL, else 5 with exact-ToF groups)
+        if (W < 3 || W > 128 || c->ser == SER_GEN) return cudaSuccess;
         const double K = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
         c->mp_fit_err = mp_fit(W, K, coef);
         if (!(c->mp_fit_err <= MP_TOL)) return cudaSuccess;  // short Gaussians: the LCF / sensor-lane kernels
-    } else if (!c->d_gpart) {  // ASSA contexts with a non-integer window: the group partials are ours
+    }
+    if (!c->d_gpart) {  // contexts without the sensor-lane adjoints' group partials: allocate ours
         cudaError_t ea = cudaMalloc(&c->d_gpart, sizeof(gacc_t) * (size_t)((c->Nd + 127) / 128) * c->Mpad);
         if (ea != cudaSuccess) return ea;
         c->workspace_bytes += (int64_t)sizeof(gacc_t) * ((c->Nd + 127) / 128) * c->Mpad;

@@ -98,6 +98,7 @@ class Info(ctypes.Structure):
         ("adj_kernel", ctypes.c_int32),
         ("collective", ctypes.c_int32),
         ("fwd_union", ctypes.c_int32),
+        ("adj_fit_err", ctypes.c_double),
     ]
 
     def as_dict(self):

@@ -189,6 +189,33 @@ def test_per_sample_sensor_lane_adjoint(W, monkeypatch):
     ctx.close()
 
 
+# the moment-polynomial adjoint's eligibility boundary: any exact-integer window whose
+# degree-7 interpolant of the window weights reaches 1e-8 of max |f|, i.e. W >= 10 at k = 3 (sigma >=
+# 1.67 samples), including window lengths that are not the forward's template sizes (10, 13); W = 8
+# falls back to the sensor-lane per-sample adjoint.  Record clipping at both ends (the record starts
+# inside the nearest windows and ends inside the farthest).  Jittered (non-grid) kernels below W = 40
+# (wide windows over a jittered cloud need more staged rows than the ring holds: fallback kernel).
+@pytest.mark.parametrize("W", [8, 10, 13, 20, 64])
+def test_moment_adjoint_window_lengths(W, monkeypatch):
+    fs, v = 40e6, 1500.0
+    sigma = W * (v / fs) / 6.0
+    c = inputs.grid_centers(9, 10, 8, sigma, jitter=0.3 if W < 40 else 0.0, seed=W)
+    s = inputs.hemisphere(40, 50e-3)
+    # the record starts inside the nearest windows and ends inside the farthest ones
+    half = 0.5 * float(np.max(c.max(axis=1) - c.min(axis=1)))
+    t0 = (50e-3 - 0.8 * half) / v
+    op = dict(sigma=sigma, v=v, fs=fs, n_samples=int(1.6 * half / v * fs) + W, t0=t0, k=3.0)
+    ctx = make_ctx(c, s, op, monkeypatch, {})
+    info = ctx.info()
+    assert info["adj_kernel"] == (3 if W < 10 else 4), info
+    assert (info["adj_fit_err"] <= 1e-8) == (W >= 10), info
+    rng = np.random.default_rng(100 + W)
+    d = rng.standard_normal((s.shape[1], op["n_samples"])).astype(np.float32)
+    akw = {k: v for k, v in op.items() if k != "n_samples"}
+    check(ctx.adjoint(T(d)).cpu().numpy(), oracle.adjoint(c, d, s, **akw), f"W {W} adjoint")
+    ctx.close()
+
+
 # any window length (fast packed paths where W is a template size, generic paths otherwise),
 # degree-2 or degree-5 series (array radius), jitter, t0 > 0, clipped records
 @pytest.mark.parametrize("seed", range(8))
