@@ -56,7 +56,8 @@ struct gpair_ctx_s {
     gpair::gacc_t* d_gpart = nullptr;     // [ceil(Nd/256)][Mpad] per-sensor-group partial gradients (k_adjoint_t)
     // moment-polynomial adjoint (gpair_mp.cu): regions of mp_cpr cells, start-sample ranges, moments
     int mp_on = 0;
-    double mp_fit_err = 0.0;      // max error of the degree-7 interpolants / max |f| (create)
+    double mp_fit_err = 0.0;      // max error of the interpolants of the window weights / max |f| (create)
+    int32_t mp_row = 48;          // bytes per moment row: 32 (degree 6) or 48 (degree 7)
     int32_t mp_cpr = 0, mp_regions = 0, mp_Lr2 = 0, mp_NtP = 0, mp_pad = 0;
     int32_t* d_wlo_m = nullptr;   // [mp_regions][Nd] lowest n_lo of the region's pairs (INT_MIN: none)
     double* d_mp = nullptr;       // [Nd][mp_NtP][8] fp64 moments M_k[j][n] at row n + W - 1 + mp_pad (chunk-swizzled)

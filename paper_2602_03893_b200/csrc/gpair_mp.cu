@@ -122,6 +122,8 @@ __global__ void k_mp_windows(const float4* __restrict__ grp, int32_t ncells, con
 constexpr int MP_ROW = 48;
 
 // M_k[j][n] = sum_m c_mk delta_j[n + m] for n in [-(W - 1), Nt - 1], fp64 sums.  Thread per row.
+// R32: 32-B rows of the degree-6 fit (M_0 fp64, M_1..M_6 fp32); else 48-B rows of the degree-7 fit.
+template <bool R32>
 __global__ void k_mp_prep(const float* __restrict__ resid, const double* __restrict__ coef, int32_t W, int32_t Nt,
                           int32_t NtP, int32_t pad, int32_t j0, char* __restrict__ Mt) {
     extern __shared__ double s_c[];  // [W][8]
@@ -141,10 +143,21 @@ __global__ void k_mp_prep(const float* __restrict__ resid, const double* __restr
         for (int q = 0; q < 8; ++q) a[q] = fma(c[q], dv, a[q]);
     }
     MP_CHECK(row + pad >= 0 && row + pad < NtP);
-    char* o = Mt + ((int64_t)j * NtP + row + pad) * MP_ROW;
-    *(double2*)o = make_double2(a[0], a[1]);
-    *(double2*)(o + 16) = make_double2(a[2], a[3]);
-    *(float4*)(o + 32) = make_float4((float)a[4], (float)a[5], (float)a[6], (float)a[7]);
+    if (R32) {
+        // the two 16-B chunks of absolute row ra swap places when bit 2 of ra is set: 8 consecutive
+        // rows then cover the 8 16-B bank slots (blocks are staged from rows that are multiples of 8)
+        const int ra = row + pad;
+        char* o = Mt + ((int64_t)j * NtP + ra) * 32;
+        const int sw = ((ra >> 2) & 1) * 16;
+        *(double*)(o + sw) = a[0];
+        *(float2*)(o + sw + 8) = make_float2((float)a[1], (float)a[2]);
+        *(float4*)(o + (16 ^ sw)) = make_float4((float)a[3], (float)a[4], (float)a[5], (float)a[6]);
+    } else {
+        char* o = Mt + ((int64_t)j * NtP + row + pad) * MP_ROW;
+        *(double2*)o = make_double2(a[0], a[1]);
+        *(double2*)(o + 16) = make_double2(a[2], a[3]);
+        *(float4*)(o + 32) = make_float4((float)a[4], (float)a[5], (float)a[6], (float)a[7]);
+    }
 }
 
 // Anchors of a (group, sensor pair) in shared memory, f32x2-interleaved over the two sensors of
@@ -193,7 +206,7 @@ constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mb
 #ifndef GPAIR_MP_MINB
 #define GPAIR_MP_MINB 3
 #endif
-template <int SDEG, bool ASSA>
+template <int SDEG, bool ASSA, bool R32>
 __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     k_adjoint_mp(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const char* __restrict__ Mt,
@@ -202,7 +215,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     static_assert(MP_SB == 8, "anchor layout: lane = (sensor lane % 8, group lane / 8)");
     extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int ROW = ASSA ? 4 : MP_ROW;                          // bytes per staged row
+    constexpr int ROW = ASSA ? 4 : (R32 ? 32 : MP_ROW);             // bytes per staged row
     const int sbytes = MP_SB * Lr2 * ROW;                           // bytes per staged batch
     char* s_M = (char*)smem8;                                       // [MP_NS][MP_SB][Lr2] rows
     float4* s_anc = (float4*)(s_M + MP_NS * sbytes);                // [nw][GPC][MP_ANC_GSTRIDE]
@@ -222,7 +235,9 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     const int nb = (jg1 - jg0 + MP_SB - 1) / MP_SB;
     const unsigned rowbytes = (unsigned)Lr2 * ROW;
     // first table row of a sensor's staged block (ASSA: 16-B aligned, Lr2 % 4 == 0)
-    auto row0 = [&](int lo) { return lo == MP_EMPTY ? 0 : (ASSA ? ((lo + pad) & ~3) : lo + W - 1 + pad); };
+    auto row0 = [&](int lo) {
+        return lo == MP_EMPTY ? 0 : (ASSA ? ((lo + pad) & ~3) : R32 ? ((lo + W - 1 + pad) & ~7) : lo + W - 1 + pad);
+    };
 
     // batch b's rows [lo_j, lo_j + Lr2) of every sensor by 1-D TMA into stage b % MP_NS
     // (an empty sensor copies zero rows of the table); issued by one thread
@@ -283,7 +298,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
             const Anchor a = make_anchor(Gq, sxn, syn, szn, k);
             // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
             const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
-                                  : a.na - lo_l - (RND_MAGIC_BITS - 1);
+                                  : a.na - (row0(lo_l) - (W - 1) - pad) - (RND_MAGIC_BITS - 1);
             aslot[0] = a.Ux;
             aslot[2] = a.Uy;
             aslot[4] = a.Uz;
@@ -351,17 +366,27 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                     rmask |= (unsigned)rare << (2 * p + h);
                     const float xi = h ? xb : xa;
                     const float w = rare ? 0.f : (h ? wb : wa);
-                    const char* rp = stage + ((2 * p + h) * Lr2 + min((unsigned)row, (unsigned)Lr2 - 1u)) * MP_ROW;
-                    const double2 m01 = *(const double2*)rp;
-                    const double2 m23 = *(const double2*)(rp + 16);
-                    const float4 m47 = *(const float4*)(rp + 32);
-                    const float tl = fmaf(fmaf(fmaf(m47.w, xi, m47.z), xi, m47.y), xi, m47.x);
-                    const double X = (double)xi;
-                    double pv = fma((double)tl, X, m23.y);
-                    pv = fma(pv, X, m23.x);
-                    pv = fma(pv, X, m01.y);
-                    pv = fma(pv, X, m01.x);
-                    acc = fma((double)w, pv, acc);
+                    const char* rp = stage + ((2 * p + h) * Lr2 + min((unsigned)row, (unsigned)Lr2 - 1u)) * ROW;
+                    if (R32) {  // M_0 fp64, M_1..M_6 fp32: the fp32 tail's terms are < 1/3 of the value
+                        const int sw = ((int)min((unsigned)row, (unsigned)Lr2 - 1u) >> 2 & 1) * 16;
+                        const float4 q0 = *(const float4*)(rp + sw);         // (M_0 lo, M_0 hi, M_1, M_2)
+                        const float4 q1 = *(const float4*)(rp + (16 ^ sw));  // M_3..M_6
+                        float tl = fmaf(fmaf(fmaf(q1.w, xi, q1.z), xi, q1.y), xi, q1.x);
+                        tl = fmaf(fmaf(tl, xi, q0.w), xi, q0.z);
+                        const double m0 = __hiloint2double(__float_as_int(q0.y), __float_as_int(q0.x));
+                        acc = fma((double)w, fma((double)tl, (double)xi, m0), acc);
+                    } else {
+                        const double2 m01 = *(const double2*)rp;
+                        const double2 m23 = *(const double2*)(rp + 16);
+                        const float4 m47 = *(const float4*)(rp + 32);
+                        const float tl = fmaf(fmaf(fmaf(m47.w, xi, m47.z), xi, m47.y), xi, m47.x);
+                        const double X = (double)xi;
+                        double pv = fma((double)tl, X, m23.y);
+                        pv = fma(pv, X, m23.x);
+                        pv = fma(pv, X, m01.y);
+                        pv = fma(pv, X, m01.x);
+                        acc = fma((double)w, pv, acc);
+                    }
                 }
                 }
             }
@@ -404,24 +429,25 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     if (cok) gpart[(int64_t)(blockIdx.y + k.grp0) * Mpad + gi] = (gacc_t)acc;
 }
 
-size_t mp_smem(int Lr2, int nw, bool assa) {
-    return (size_t)MP_NS * MP_SB * Lr2 * (assa ? 4 : MP_ROW) + (size_t)nw * GPC * MP_ANC_GSTRIDE * 16 + MP_NS * 8 +
+size_t mp_smem(int Lr2, int nw, int row_bytes) {
+    return (size_t)MP_NS * MP_SB * Lr2 * row_bytes + (size_t)nw * GPC * MP_ANC_GSTRIDE * 16 + MP_NS * 8 +
            MP_NS * 4;
 }
 
-// Degree-7 interpolation of f(xi0 + xi - m), m < W, at the Chebyshev nodes of [-1/2, 1/2]
-// (fp64 Vandermonde solve with partial pivoting), coefficients [m][k].  Returns the max error
+// Degree-deg (<= 7) interpolation of f(xi0 + xi - m), m < W, at the deg + 1 Chebyshev nodes of
+// [-1/2, 1/2] (fp64 Vandermonde solve with partial pivoting), coefficients [m][8] (zero-padded).  Returns the max error
 // over a 4001-point grid relative to max |f|.
-double mp_fit(int W, double K, std::vector<double>& coef) {
-    constexpr int P = 8;
+double mp_fit(int W, double K, std::vector<double>& coef, int deg) {
+    constexpr int PM = 8;
+    const int P = deg + 1;  // interpolation nodes / coefficients (<= 8); coef is [W][8], zero-padded
     const double xi0 = 0.5 * W - 0.5;
-    double nodes[P];
+    double nodes[PM];
     for (int i = 0; i < P; ++i) nodes[i] = 0.5 * std::cos((2 * i + 1) * 3.141592653589793 / (2 * P));
     auto f = [&](double u) { return u * std::exp2(K * u * u); };
-    coef.assign((size_t)W * P, 0.0);
+    coef.assign((size_t)W * PM, 0.0);
     double err = 0.0, fmax = 0.0;
     for (int m = 0; m < W; ++m) {
-        double A[P][P + 1];
+        double A[PM][PM + 1];
         for (int i = 0; i < P; ++i) {
             double pw = 1.0;
             for (int kk = 0; kk < P; ++kk) {
@@ -441,11 +467,11 @@ double mp_fit(int W, double K, std::vector<double>& coef) {
                 for (int cc = col; cc <= P; ++cc) A[r][cc] -= fct * A[col][cc];
             }
         }
-        for (int kk = 0; kk < P; ++kk) coef[(size_t)m * P + kk] = A[kk][P] / A[kk][kk];
+        for (int kk = 0; kk < P; ++kk) coef[(size_t)m * PM + kk] = A[kk][P] / A[kk][kk];
         for (int g = 0; g <= 4000; ++g) {
             const double xi = -0.5 + g / 4000.0;
-            double p = coef[(size_t)m * P + P - 1];
-            for (int kk = P - 2; kk >= 0; --kk) p = p * xi + coef[(size_t)m * P + kk];
+            double p = coef[(size_t)m * PM + P - 1];
+            for (int kk = P - 2; kk >= 0; --kk) p = p * xi + coef[(size_t)m * PM + kk];
             const double fv = f(xi0 + xi - m);
             err = std::max(err, std::fabs(p - fv));
             fmax = std::max(fmax, std::fabs(fv));
@@ -454,7 +480,7 @@ double mp_fit(int W, double K, std::vector<double>& coef) {
     return fmax > 0.0 ? err / fmax : 1.0;
 }
 
-template <int SDEG, bool ASSA>
+template <int SDEG, bool ASSA, bool R32>
 cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     const int G = (c->Nd + MP_SG - 1) / MP_SG;
     const int g0 = c->lng > 0 ? c->lg0 : 0;
@@ -466,19 +492,19 @@ cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParam
         e = launch_assa_dconv(c, resid, (float*)c->d_mp, c->mp_NtP, c->mp_pad, j0, nj, st);
     } else {
         ++c->n_launch;
-        k_mp_prep<<<dim3((unsigned)((c->Nt + W - 1 + 127) / 128), (unsigned)nj), 128, (size_t)W * 64, st>>>(
+        k_mp_prep<R32><<<dim3((unsigned)((c->Nt + W - 1 + 127) / 128), (unsigned)nj), 128, (size_t)W * 64, st>>>(
             resid, c->d_mp_coef, W, c->Nt, c->mp_NtP, c->mp_pad, j0, (char*)c->d_mp);
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, ASSA);
-    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, c->mp_row);
+    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     OpConst kk = c->k;
     kk.grp0 = g0;
     const double K64 = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
     ++c->n_launch;
-    k_adjoint_mp<SDEG, ASSA><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
+    k_adjoint_mp<SDEG, ASSA, R32><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
         c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_m, (const char*)c->d_mp, resid, c->d_gpart, c->mp_cpr, c->ncells,
         c->mp_Lr2, c->mp_NtP, c->mp_pad, c->Mpad, kk, (float)(0.5 * W - 0.5), K64);
     e = cudaGetLastError();
@@ -493,8 +519,13 @@ int mp_groups(const gpair_ctx* c) { return (c->Nd + MP_SG - 1) / MP_SG; }
 
 cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     if (c->assa)
-        return c->series_small ? mp_launch<2, true>(c, resid, mode, ep, st) : mp_launch<5, true>(c, resid, mode, ep, st);
-    return c->series_small ? mp_launch<2, false>(c, resid, mode, ep, st) : mp_launch<5, false>(c, resid, mode, ep, st);
+        return c->series_small ? mp_launch<2, true, false>(c, resid, mode, ep, st)
+                               : mp_launch<5, true, false>(c, resid, mode, ep, st);
+    if (c->mp_row == 32)
+        return c->series_small ? mp_launch<2, false, true>(c, resid, mode, ep, st)
+                               : mp_launch<5, false, true>(c, resid, mode, ep, st);
+    return c->series_small ? mp_launch<2, false, false>(c, resid, mode, ep, st)
+                           : mp_launch<5, false, false>(c, resid, mode, ep, st);
 }
 
 // Create-time set-up: eligibility (exact-integer window on the fast anchor paths), the
@@ -510,7 +541,15 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
         // anchor series paths (degree 2 when every |eps| <= EPS_SMALL, else 5 with exact-ToF groups)
         if (W < 3 || W > 128 || c->ser == SER_GEN) return cudaSuccess;
         const double K = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
-        c->mp_fit_err = mp_fit(W, K, coef);
+        // 32-B rows (degree 6: M_0 fp64 + M_1..M_6 fp32) where that fit reaches MP_TOL, else 48-B rows
+        // (degree 7: M_0..M_3 fp64 + M_4..M_7 fp32); GPAIR_MP_ROW48=1 forces the latter (A/B, tests)
+        const char* r48 = std::getenv("GPAIR_MP_ROW48");
+        c->mp_fit_err = mp_fit(W, K, coef, 6);
+        c->mp_row = 32;
+        if (!(c->mp_fit_err <= MP_TOL) || (r48 && r48[0] == '1')) {
+            c->mp_fit_err = mp_fit(W, K, coef, 7);
+            c->mp_row = MP_ROW;
+        }
         if (!(c->mp_fit_err <= MP_TOL)) return cudaSuccess;  // short Gaussians: the LCF / sensor-lane kernels
     }
     if (!c->d_gpart) {  // contexts without the sensor-lane adjoints' group partials: allocate ours
@@ -548,8 +587,9 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
             return e;
         }
         // ASSA: 4-B rows, blocks start 16-B aligned (up to 3 rows earlier) and span a multiple of 4 rows
-        const int Lr2 = assa ? (std::max(h_len, 1) + 3 + 3) / 4 * 4 : std::max(h_len, 1);
-        if (mp_smem(Lr2, cpr, assa) > 200 * 1024) {
+        // 32-B rows: blocks start on an 8-row boundary (up to 7 rows earlier; the chunk swizzle)
+        const int Lr2 = assa ? (std::max(h_len, 1) + 3 + 3) / 4 * 4 : std::max(h_len, 1) + (c->mp_row == 32 ? 7 : 0);
+        if (mp_smem(Lr2, cpr, assa ? 4 : c->mp_row) > 200 * 1024) {
             cudaFree(wlo);
             if (cpr > 1) {
                 cpr /= 2;
@@ -572,9 +612,9 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
         c->mp_NtP = (c->k.alpha * c->Nt + 2 * c->mp_pad + 3) / 4 * 4;  // rows of every sensor start 16-B aligned
         nM = ((size_t)c->Nd * c->mp_NtP + 1) / 2;
     } else {
-        c->mp_pad = c->mp_Lr2 + 1;  // zero rows on both sides: every staged block stays inside the table
+        c->mp_pad = c->mp_Lr2 + 8;  // zero rows on both sides: every staged block stays inside the table
         c->mp_NtP = c->Nt + W - 1 + 2 * c->mp_pad;
-        nM = (size_t)c->Nd * c->mp_NtP * (MP_ROW / 8);
+        nM = (size_t)c->Nd * c->mp_NtP * (c->mp_row / 8);
     }
     e = cudaMalloc(&c->d_mp, nM * sizeof(double));
     if (e == cudaSuccess) e = cudaMemsetAsync(c->d_mp, 0, nM * sizeof(double), st);

@@ -26,6 +26,7 @@ pytestmark = pytest.mark.gpu
 # switches -> (info.tab, info.adj_kernel)
 PATHS = {
     "tab+mp": ({}, (1, 4)),
+    "tab+mp48": ({"GPAIR_MP_ROW48": "1"}, (1, 4)),  # the 48-B (degree-7) moment rows
     "tab+lcf": ({"GPAIR_ADJ_NO_MP": "1"}, (1, 2)),
     "tab+lane_t": ({"GPAIR_ADJ_NO_MP": "1", "GPAIR_ADJ_NO_LCF": "1"}, (1, 1)),
     "tab+lane_kernel": ({"GPAIR_ADJ_NO_MP": "1", "GPAIR_ADJ_NO_LCF": "1", "GPAIR_ADJ_NO_T": "1"}, (1, 0)),
@@ -39,7 +40,7 @@ PATHS = {
     # register-window forward (opt-in)
     "tab_union+mp": ({"GPAIR_FWD_UNION": "1"}, (1, 4)),
 }
-ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_ADJ_NO_MP", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE", "GPAIR_FWD_UNION")
+ENV_KEYS = ("GPAIR_NO_TAB", "GPAIR_MP_ROW48", "GPAIR_ADJ_NO_MP", "GPAIR_ADJ_NO_LCF", "GPAIR_ADJ_NO_T", "GPAIR_PIPELINE", "GPAIR_FWD_UNION")
 
 
 @pytest.fixture(scope="module", autouse=True)
