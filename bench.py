@@ -32,7 +32,6 @@ UNIT = "pair-evals/s"
 # fp64 residual column) = SURVEY 8d's SFU rate of one exp per pair-sample (16 MUFU / clk / SM)
 PAIR_SAMPLES_PER_CLK_SM = 16
 ISSUE_PER_CLK_SM = 4  # warp instructions / clk / SM (4 SMSPs)
-MP_ROW_BYTES = 48  # k_adjoint_mp: one staged row of the moment table per pair (gpair_mp.cu)
 
 
 def parse():
@@ -343,9 +342,10 @@ def main():
         if key == "adjoint" and info["adj_kernel"] == 4 and args.op == "exact":
             # the moment-polynomial adjoint reads one staged moment row per pair (no per-sample work,
             # so its pair-sample rate exceeds the per-sample roofline above): its own bound is the
-            # shared-memory pipe at MP_ROW_BYTES per pair, 128 B / clk / SM; the launch also holds the
-            # moment prep and the group gather
-            row_b = MP_ROW_BYTES
+            # shared-memory pipe at one staged moment row per pair (gpair_info.adj_row_bytes: 32 or
+            # 48 B), 128 B / clk / SM; the launch also holds the moment prep and the group gather
+            #
+            row_b = info["adj_row_bytes"]
             pairs = Ml * cfg.n_sensors  # this rank's kernel shard
             own_peak = n_sm * 128.0 / row_b * f_max
             per_kernel[names[key]]["own_roofline"] = {

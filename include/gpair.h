@@ -191,6 +191,7 @@ typedef struct {
     int32_t fwd_union;          /* 1: register-window forward (opt-in GPAIR_FWD_UNION=1) */
     double adj_fit_err;         /* moment-polynomial adjoint: max error of the degree-7 interpolants of the
                                    window weights / max |f| (create-time fit; 0 when not attempted)   */
+    int32_t adj_row_bytes;      /* moment-polynomial adjoint: bytes per staged moment row (32 or 48; ASSA 4) */
 } gpair_info;
 
 /* Create a context: validates `d`, sorts the kernels into 32-kernel spatial

@@ -616,6 +616,7 @@ gpair_status gpair_get_info(const gpair_ctx* c, gpair_info* o) {
     o->collective = c->coll;
     o->fwd_union = c->f_union;
     o->adj_fit_err = c->mp_fit_err;
+    o->adj_row_bytes = c->mp_on ? (c->assa ? 4 : c->mp_row) : 0;
     return GPAIR_OK;
 }
 

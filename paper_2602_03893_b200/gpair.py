@@ -99,6 +99,7 @@ class Info(ctypes.Structure):
         ("collective", ctypes.c_int32),
         ("fwd_union", ctypes.c_int32),
         ("adj_fit_err", ctypes.c_double),
+        ("adj_row_bytes", ctypes.c_int32),
     ]
 
     def as_dict(self):
