@@ -497,7 +497,7 @@ cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParam
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, c->mp_row);
+    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, ASSA ? 4 : c->mp_row);
     e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     OpConst kk = c->k;
