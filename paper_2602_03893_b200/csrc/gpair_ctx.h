@@ -58,6 +58,7 @@ struct gpair_ctx_s {
     int mp_on = 0;
     double mp_fit_err = 0.0;      // max error of the interpolants of the window weights / max |f| (create)
     int32_t mp_row = 48;          // bytes per moment row: 32 (degree 6) or 48 (degree 7)
+    int32_t mp_slot = 0;          // compile-time slot stride in rows (40/48/64/96) of k_adjoint_mp, 0: runtime
     int32_t mp_cpr = 0, mp_regions = 0, mp_Lr2 = 0, mp_NtP = 0, mp_pad = 0;
     int32_t* d_wlo_m = nullptr;   // [mp_regions][Nd] lowest n_lo of the region's pairs (INT_MIN: none)
     double* d_mp = nullptr;       // [Nd][mp_NtP][8] fp64 moments M_k[j][n] at row n + W - 1 + mp_pad (chunk-swizzled)

@@ -206,7 +206,9 @@ constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mb
 #ifndef GPAIR_MP_MINB
 #define GPAIR_MP_MINB 3
 #endif
-template <int SDEG, bool ASSA, bool R32>
+// LR > 0: compile-time slot stride (rows per sensor in a staged batch, >= Lr2), so every staged row
+// address is one add of an immediate; LR = 0: the runtime Lr2
+template <int SDEG, bool ASSA, bool R32, int LR>
 __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     k_adjoint_mp(const float4* __restrict__ kd, const float4* __restrict__ grp, const float* __restrict__ orig,
                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const char* __restrict__ Mt,
@@ -216,8 +218,9 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int ROW = ASSA ? 4 : (R32 ? 32 : MP_ROW);             // bytes per staged row
-    const int sbytes = MP_SB * Lr2 * ROW;                           // bytes per staged batch
-    char* s_M = (char*)smem8;                                       // [MP_NS][MP_SB][Lr2] rows
+    const int LRS = LR > 0 ? LR : Lr2;                              // rows per sensor slot
+    const int sbytes = MP_SB * LRS * ROW;                           // bytes per staged batch
+    char* s_M = (char*)smem8;                                       // [MP_NS][MP_SB][LRS] rows
     float4* s_anc = (float4*)(s_M + MP_NS * sbytes);                // [nw][GPC][MP_ANC_GSTRIDE]
     uint64_t* bar = (uint64_t*)(s_anc + nw * GPC * MP_ANC_GSTRIDE); // full[MP_NS]
     int* s_done = (int*)(bar + MP_NS);                              // [MP_NS] warps done with a stage
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
         for (int jj = 0; jj < nj; ++jj) {
             const int ra0 = row0(__ldg(wrow + jb + jj));
             MP_CHECK(jb + jj < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
-            tma_bulk_g2s(dst + jj * rowbytes, Mt + ((int64_t)(jb + jj) * NtP + ra0) * ROW, rowbytes, full);
+            tma_bulk_g2s(dst + jj * LRS * ROW, Mt + ((int64_t)(jb + jj) * NtP + ra0) * ROW, rowbytes, full);
         }
     };
     if (threadIdx.x == 0) {
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                         const int row = (int)((unsigned)__float_as_int(h ? A3.w : A3.z) + (unsigned)__float_as_int(h ? t1 : t0));
                         const bool rare = fabsf(h ? d1 : d0) > gam_a || (unsigned)row >= (unsigned)Lr2;
                         rmask |= (unsigned)rare << (2 * p + h);
-                        const float dv = *(const float*)(stage + ((2 * p + h) * Lr2 + min((unsigned)row, (unsigned)Lr2 - 1u)) * 4);
+                        const float dv = *(const float*)(stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * 4);
                         accf = fmaf(rare ? 0.f : (h ? wb : wa), dv, accf);  // Eq. 17
                     }
                 } else {
@@ -366,7 +369,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                     rmask |= (unsigned)rare << (2 * p + h);
                     const float xi = h ? xb : xa;
                     const float w = rare ? 0.f : (h ? wb : wa);
-                    const char* rp = stage + ((2 * p + h) * Lr2 + min((unsigned)row, (unsigned)Lr2 - 1u)) * ROW;
+                    const char* rp = stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * ROW;
                     if (R32) {  // M_0 fp64, M_1..M_6 fp32: the fp32 tail's terms are < 1/3 of the value
                         const int sw = ((int)min((unsigned)row, (unsigned)Lr2 - 1u) >> 2 & 1) * 16;
                         const float4 q0 = *(const float4*)(rp + sw);         // (M_0 lo, M_0 hi, M_1, M_2)
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
             if (lane < njn) {
                 const int ra0 = row0(__ldg(wrow + jbn + lane));
                 MP_CHECK(jbn + lane < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
-                tma_bulk_g2s(s_M + s * sbytes + lane * rowbytes, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
+                tma_bulk_g2s(s_M + s * sbytes + lane * LRS * ROW, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
                              rowbytes, bar + s);
             }
         }
@@ -480,7 +483,7 @@ double mp_fit(int W, double K, std::vector<double>& coef, int deg) {
     return fmax > 0.0 ? err / fmax : 1.0;
 }
 
-template <int SDEG, bool ASSA, bool R32>
+template <int SDEG, bool ASSA, bool R32, int LR>
 cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     const int G = (c->Nd + MP_SG - 1) / MP_SG;
     const int g0 = c->lng > 0 ? c->lg0 : 0;
@@ -497,14 +500,14 @@ cudaError_t mp_launch(gpair_ctx* c, const float* resid, int mode, const EpiParam
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;
-    const size_t smem = mp_smem(c->mp_Lr2, c->mp_cpr, ASSA ? 4 : c->mp_row);
-    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA, R32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = mp_smem(LR > 0 ? LR : c->mp_Lr2, c->mp_cpr, ASSA ? 4 : c->mp_row);
+    e = cudaFuncSetAttribute(k_adjoint_mp<SDEG, ASSA, R32, LR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     OpConst kk = c->k;
     kk.grp0 = g0;
     const double K64 = -1.4426950408889634 * c->k.h * c->k.h / (2.0 * c->k.sigma * c->k.sigma);
     ++c->n_launch;
-    k_adjoint_mp<SDEG, ASSA, R32><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
+    k_adjoint_mp<SDEG, ASSA, R32, LR><<<dim3((unsigned)c->mp_regions, (unsigned)ng), 32 * c->mp_cpr, smem, st>>>(
         c->d_kd, c->d_grp, c->d_orig, c->d_sens, c->d_wlo_m, (const char*)c->d_mp, resid, c->d_gpart, c->mp_cpr, c->ncells,
         c->mp_Lr2, c->mp_NtP, c->mp_pad, c->Mpad, kk, (float)(0.5 * W - 0.5), K64);
     e = cudaGetLastError();
@@ -519,13 +522,20 @@ int mp_groups(const gpair_ctx* c) { return (c->Nd + MP_SG - 1) / MP_SG; }
 
 cudaError_t launch_mp_adjoint(gpair_ctx* c, const float* resid, int mode, const EpiParams& ep, cudaStream_t st) {
     if (c->assa)
-        return c->series_small ? mp_launch<2, true, false>(c, resid, mode, ep, st)
-                               : mp_launch<5, true, false>(c, resid, mode, ep, st);
-    if (c->mp_row == 32)
-        return c->series_small ? mp_launch<2, false, true>(c, resid, mode, ep, st)
-                               : mp_launch<5, false, true>(c, resid, mode, ep, st);
-    return c->series_small ? mp_launch<2, false, false>(c, resid, mode, ep, st)
-                           : mp_launch<5, false, false>(c, resid, mode, ep, st);
+        return c->series_small ? mp_launch<2, true, false, 0>(c, resid, mode, ep, st)
+                               : mp_launch<5, true, false, 0>(c, resid, mode, ep, st);
+    if (c->mp_row == 32) {
+        const bool d2 = c->series_small != 0;
+        switch (c->mp_slot) {  // compile-time slot stride (mp_setup: the smallest >= Lr2)
+            case 40: return d2 ? mp_launch<2, false, true, 40>(c, resid, mode, ep, st) : mp_launch<5, false, true, 40>(c, resid, mode, ep, st);
+            case 48: return d2 ? mp_launch<2, false, true, 48>(c, resid, mode, ep, st) : mp_launch<5, false, true, 48>(c, resid, mode, ep, st);
+            case 64: return d2 ? mp_launch<2, false, true, 64>(c, resid, mode, ep, st) : mp_launch<5, false, true, 64>(c, resid, mode, ep, st);
+            case 96: return d2 ? mp_launch<2, false, true, 96>(c, resid, mode, ep, st) : mp_launch<5, false, true, 96>(c, resid, mode, ep, st);
+            default: return d2 ? mp_launch<2, false, true, 0>(c, resid, mode, ep, st) : mp_launch<5, false, true, 0>(c, resid, mode, ep, st);
+        }
+    }
+    return c->series_small ? mp_launch<2, false, false, 0>(c, resid, mode, ep, st)
+                           : mp_launch<5, false, false, 0>(c, resid, mode, ep, st);
 }
 
 // Create-time set-up: eligibility (exact-integer window on the fast anchor paths), the
@@ -601,6 +611,17 @@ cudaError_t mp_setup(gpair_ctx* c, cudaStream_t st, std::string& why) {
         c->mp_cpr = cpr;
         c->mp_regions = nreg;
         c->mp_Lr2 = Lr2;
+        // compile-time slot stride of the 32-B-row kernel (0: runtime), when its ring still fits 3 CTAs
+        c->mp_slot = 0;
+        if (!assa && c->mp_row == 32) {
+            for (int lr : {40, 48, 64, 96})
+                if (Lr2 <= lr && mp_smem(lr, cpr, 32) <= 72 * 1024) {
+                    c->mp_slot = lr;
+                    break;
+                }
+            if (const char* ev = std::getenv("GPAIR_MP_SLOT_RUNTIME"))
+                if (ev[0] == '1') c->mp_slot = 0;  // A/B runs
+        }
         c->d_wlo_m = wlo;
         c->workspace_bytes += (int64_t)sizeof(int32_t) * nreg * c->Nd;
         break;
