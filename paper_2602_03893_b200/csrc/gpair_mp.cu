@@ -7,25 +7,27 @@
 // W samples n_lo + m, m = 0..W-1, at u = u_lo - m with u_lo = xi0 + xi, xi0 = W/2 - 1/2 and
 // xi in [-1/2, 1/2).  So a pair enters only through (n_lo, xi, w):
 //   g_ij = w sum_m f(xi0 + xi - m) delta_j[n_lo + m].
-// Each f(xi0 + xi - m) is smooth in xi on [-1/2, 1/2]; its degree-7 interpolant at the 8
-// Chebyshev nodes, sum_k c_mk xi^k, matches it to < MP_TOL of max |f| (checked at create:
-// 1.4e-10 at the bench constants, far below the fp32 time of flight's ~1e-7 per pair).  Hence
+// Each f(xi0 + xi - m) is smooth in xi on [-1/2, 1/2]; its interpolant at Chebyshev nodes,
+// sum_k c_mk xi^k, matches it to < MP_TOL of max |f| (checked at create: degree 6 gives 3.8e-9 and
+// degree 7 1.4e-10 at the bench constants, far below the fp32 time of flight's ~1e-7 per pair).
+// Hence
 //   g_ij = w sum_k xi^k M_k[j][n_lo],    M_k[j][n] = sum_m c_mk delta_j[n + m],
-// with delta = 0 outside the record (reading R8: clipped windows, no masking).  k_mp_prep forms
-// the 8 moments of every (sensor, start sample) in fp64 once per residual; k_adjoint_mp then
-// pays per pair one fp32 time of flight (two-level anchors, gpair_internal.cuh), one 64-B row of
-// M from shared memory and 8 DFMA (Horner in xi + the accumulate), all in fp64 after the fp32
-// time of flight -- against the LCF kernel's 16-sample fp64 Horner chains and per-pair fp64
-// exponentials.  Ambiguous window edges (GAMMA band) and exact-ToF groups take the oracle-exact
-// window (pair_setup) and a per-sample fp64 sum over the residual (rare).
+// with delta = 0 outside the record (reading R8: clipped windows, no masking).  k_mp_prep forms the
+// moments of every (sensor, start sample) in fp64 once per residual, stored as 32-B rows (degree 6:
+// M_0 fp64, M_1..M_6 fp32) or 48-B rows (degree 7: M_0..M_3 fp64, M_4..M_7 fp32); k_adjoint_mp then
+// pays per pair one fp32 time of flight (two-level anchors, gpair_internal.cuh), one row of M from
+// shared memory, an fp32 Horner tail and 2 (or 5) DFMA -- against the LCF kernel's 16-sample fp64
+// Horner chains and per-pair fp64 exponentials.  Ambiguous window edges (GAMMA band) and exact-ToF
+// groups take the oracle-exact window (pair_setup) and a per-sample fp64 sum over the residual.
+// The ASSA operator's adjoint (row f1) runs on the same kernel with 4-B rows of its dconv table.
 //
-// Layout: lane = kernel (a warp = one 32-kernel cell, a CTA = a region of mp_cpr cells), the
-// CTA loops over its 256-sensor group in batches of MP_SB sensors: per batch the fp64 anchors
-// (group, sensor) go to warp-private shared memory and the M rows [lo_j, lo_j + Lr) of each
-// sensor (lo_j: the region's lowest possible n_lo, k_mp_windows) are staged by cp.async into a
-// shared [sensor][row][8] fp64 block (16-B chunks XOR-swizzled by row so that the ~16 rows one
-// warp reads per sensor hit distinct banks).  Each lane accumulates its kernel's sum over the
-// group's sensors in fp64 and writes gpart[group][i]; k_adj_gather sums the groups in a fixed
+// Layout: lane = kernel (a warp = one 32-kernel cell, a CTA = a region of mp_cpr cells); the CTA
+// loops over its 256-sensor group in batches of MP_SB sensors.  Per batch the fp64 anchors (group,
+// sensor) go to warp-private shared memory, f32x2-interleaved over sensor pairs, and each sensor's
+// rows [lo_j, lo_j + L_r) of the table (lo_j: the region's lowest possible n_lo, k_mp_windows) are
+// staged by one 1-D TMA copy (cp.async.bulk, completion on an mbarrier) into a ring of MP_NS
+// stages; the last warp done with a stage refills it.  Each lane accumulates its kernel's sum over
+// the group's sensors in fp64 and writes gpart[group][i]; k_adj_gather sums the groups in a fixed
 // order and applies the update (deterministic, no atomics).
 #include <algorithm>
 #include <climits>
