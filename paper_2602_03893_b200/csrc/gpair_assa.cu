@@ -59,8 +59,10 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
     const float* __restrict__ taps, float* __restrict__ partial, int32_t cpr, int32_t ncells, int32_t Lf,
     int32_t zrows, int64_t Mpad, OpConst k) {
     extern __shared__ float4 smem4[];
-    float4* s_kd = smem4;                                // [A_STAGE*32]
-    float4* s_grp = s_kd + A_STAGE * CELL;               // [A_STAGE*GPC]
+    // kernel pairs interleaved: s_kxy[p] = (x0, x1, y0, y1), s_kzw[p] = (z0, z1, w0, w1) (f32x2 set-up)
+    float* s_kxy = (float*)smem4;                        // [A_STAGE*32*2]
+    float* s_kzw = s_kxy + A_STAGE * CELL * 2;           // [A_STAGE*32*2]
+    float4* s_grp = smem4 + A_STAGE * CELL;              // [A_STAGE*GPC]
     float* s_amp = (float*)(s_grp + A_STAGE * GPC);      // [A_STAGE*32]
     float* s_taps = s_amp + A_STAGE * CELL;              // [2K+1] (padded to 4)
     const int ntaps = 2 * k.K + 1;
@@ -91,7 +93,12 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
         const int nc = min(A_STAGE, c1 - cb);
         __syncthreads();
         for (int t = threadIdx.x; t < nc * CELL; t += blockDim.x) {
-            s_kd[t] = kd[(int64_t)cb * CELL + t];
+            const float4 v = kd[(int64_t)cb * CELL + t];
+            const int pb = (t >> 1) * 4 + (t & 1);
+            s_kxy[pb] = v.x;
+            s_kxy[pb + 2] = v.y;
+            s_kzw[pb] = v.z;
+            s_kzw[pb + 2] = v.w;
             s_amp[t] = amp[(int64_t)cb * CELL + t];
         }
         if (threadIdx.x < nc * GPC) s_grp[threadIdx.x] = grp[(int64_t)cb * GPC + threadIdx.x];
@@ -99,28 +106,58 @@ __global__ void __launch_bounds__(32 * A_WARPS) k_assa_forward(
         for (int gq = 0; gq < nc * GPC && lo_j >= 0; ++gq) {
             const Anchor a = make_anchor(s_grp[gq], sx, sy, sz, k);
             const bool fast = SER <= 2 && !__any_sync(__activemask(), a.na == NA_EXACT);
-            const float4* kdg = s_kd + gq * GROUP;
             const float* ampg = s_amp + gq * GROUP;
             const int64_t gi0 = (int64_t)cb * CELL + gq * GROUP;
             if (fast) {
-                // 4 independent setups, one rare branch, then the RMWs (ILP)
+                // two kernels per f32x2 step (assa_pre's arithmetic, bit-identical index decisions),
+                // the group's 4 steps unrolled: 8 independent set-ups, then the RMWs (ILP)
+                const f2_t Ux = pk2(a.Ux, a.Ux), Uy = pk2(a.Uy, a.Uy), Uz = pk2(a.Uz, a.Uz);
+                const f2_t iR2 = pk2(a.invR2, a.invR2), i2Rh = pk2(a.inv2Rh, a.inv2Rh);
+                const f2_t Eu = pk2(a.Eu, a.Eu), h2R = pk2(a.h2R, a.h2R);
+                const f2_t alf = pk2((float)k.alpha, (float)k.alpha), half = pk2(0.5f, 0.5f);
+                const f2_t nhalf = pk2(-0.5f, -0.5f), two_h = pk2(k.two_over_h, k.two_over_h);
+                const f2_t mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
+                const float gam = 0.5f - GAMMA * (float)k.alpha;
+                const int kna = k.alpha * a.na - RND_MAGIC_BITS - klo;  // row = bits(t) + kna
+                int row[GROUP];
+                float wv[GROUP];
+                unsigned amb = 0;
 #pragma unroll
-                for (int t0 = 0; t0 < GROUP; t0 += 4) {
-                    AssaPre q[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) q[u] = assa_pre(a, kdg[t0 + u], ampg[t0 + u], k);
-                    if (q[0].amb | q[1].amb | q[2].amb | q[3].amb) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (q[u].amb) q[u].k = assa_fix(orig, gi0 + t0 + u, Mpad, sx, sy, sz, k);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if ((unsigned)q[u].k < (unsigned)kmax) zs[(q[u].k - klo) * 32] += q[u].w;  // Eq. 9
+                for (int t = 0; t < GROUP; t += 2) {
+                    const int li = gq * GROUP + t;
+                    const float4 pxy = *(const float4*)(s_kxy + 2 * li), pzw = *(const float4*)(s_kzw + 2 * li);
+                    const f2_t A2 = *(const f2_t*)(s_amp + li);
+                    const f2_t q = fma2(Ux, pk2(pxy.x, pxy.y), fma2(Uy, pk2(pxy.z, pxy.w), fma2(Uz, pk2(pzw.x, pzw.y), pk2(pzw.z, pzw.w))));
+                    f2_t S, Tw;
+                    series2<2>(mul2(q, iR2), S, Tw);
+                    const f2_t eu = fma2(mul2(q, i2Rh), S, Eu);
+                    const f2_t w2 = mul2(mul2(A2, mul2(h2R, Tw)), two_h);
+                    const f2_t xa = fma2(alf, eu, half);
+                    const f2_t tt = add2(add2(xa, nhalf), mag);
+                    const f2_t fl = add2(tt, nmag);
+                    const f2_t dd = sub2(sub2(xa, fl), half);
+                    float t0, t1, d0, d1;
+                    upk2(tt, t0, t1);
+                    upk2(dd, d0, d1);
+                    upk2(w2, wv[t], wv[t + 1]);
+                    row[t] = __float_as_int(t0) + kna;
+                    row[t + 1] = __float_as_int(t1) + kna;
+                    amb |= (fabsf(d0) > gam ? 1u : 0u) << t;
+                    amb |= (fabsf(d1) > gam ? 1u : 0u) << (t + 1);
                 }
+                if (amb) {
+#pragma unroll
+                    for (int t = 0; t < GROUP; ++t)
+                        if ((amb >> t) & 1u) row[t] = assa_fix(orig, gi0 + t, Mpad, sx, sy, sz, k) - klo;
+                }
+#pragma unroll
+                for (int t = 0; t < GROUP; ++t)  // Eq. 9: the impulse exists inside the upsampled record
+                    if ((unsigned)(row[t] + klo) < (unsigned)kmax) zs[row[t] * 32] += wv[t];
             } else {
                 for (int t = 0; t < GROUP; ++t) {
-                    const AssaPair p = assa_setup<SER>(a, kdg[t], ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k);
+                    const int li = gq * GROUP + t, pb = (li >> 1) * 4 + (li & 1);
+                    const float4 kdt = make_float4(s_kxy[pb], s_kxy[pb + 2], s_kzw[pb], s_kzw[pb + 2]);
+                    const AssaPair p = assa_setup<SER>(a, kdt, ampg[t], orig, gi0 + t, Mpad, sx, sy, sz, k);
                     if ((unsigned)p.k < (unsigned)kmax) zs[(p.k - klo) * 32] += p.w;  // impulse exists (Eq. 9)
                 }
             }
