@@ -30,7 +30,7 @@ namespace {
 
 constexpr int A_STAGE = 8;     // cells staged per step
 #ifndef GPAIR_ASSA_WARPS
-#define GPAIR_ASSA_WARPS 4
+#define GPAIR_ASSA_WARPS 3
 #endif
 constexpr int A_WARPS = GPAIR_ASSA_WARPS;  // sensor warps per forward CTA
 constexpr int MAX_TAPS = 1024; // 2K+1 limit of the shared-memory taps table
