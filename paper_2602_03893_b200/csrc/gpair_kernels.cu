@@ -101,6 +101,12 @@ __device__ __forceinline__ void exp2_pm64(double x, double& ep, double& em) {
 #define GPAIR_FWD_UNROLL 1
 #endif
 constexpr int kFwdUnroll = GPAIR_FWD_UNROLL;  // unroll of the 8-kernel group loop
+#ifndef GPAIR_FWD_STEP_UNROLL
+#define GPAIR_FWD_STEP_UNROLL 1
+#endif
+// unroll of the fast path's 2-kernel steps in a group: 1 (2: 43.2 ms, 2 with 2 CTAs / SM: 46.7 ms at cfg4;
+// profiles/r2/variants_fwd_unroll.txt)
+constexpr int kFwdStepUnroll = GPAIR_FWD_STEP_UNROLL;
 
 // Accumulate one pair's WMAX in-window samples into its smem column (lane
 // stride 32): packed f32x2, no predicates (the common case).
@@ -300,7 +306,7 @@ __global__ void __launch_bounds__(256, GPAIR_FWD_MINB) k_forward(const float4* _
                     const f2_t mag = pk2(RND_MAGIC, RND_MAGIC), nmag = pk2(-RND_MAGIC, -RND_MAGIC);
                     const int nrel = a.na - (RND_MAGIC_BITS - 1) - lo_j;  // n_lo - lo_j = bits(t) + nrel
                     const unsigned span = (unsigned)(k.Nt - k.cnt_int);
-#pragma unroll 1
+#pragma unroll kFwdStepUnroll
                     for (int t = 0; t < GROUP; t += 2) {
                         const int li = gq * GROUP + t;
                         const float4 pxy = *(const float4*)(s_kxy + 2 * li), pzw = *(const float4*)(s_kzw + 2 * li);
