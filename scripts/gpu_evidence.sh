@@ -30,6 +30,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ad
 python scripts/ncu_summary.py gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep > gpurun_out/ncu_summary_assa_k_adjoint_mp_${TAG}.txt 2>&1
 python scripts/sass_mix.py gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep 268435456 > gpurun_out/ncu_sassmix_assa_k_adjoint_mp_${TAG}.txt 2>&1
 [ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_assa_k_adjoint_mp_${TAG}.ncu-rep
+# the ASSA forward
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_assa_forward -c 1 \
+    -o gpurun_out/prof_${CFG}_k_assa_forward_${TAG} -f python scripts/profile_once.py $CFG assa > gpurun_out/ncu_full_assa_fwd_${TAG}.log 2>&1
+python scripts/ncu_summary.py gpurun_out/prof_${CFG}_k_assa_forward_${TAG}.ncu-rep > gpurun_out/ncu_summary_k_assa_forward_${TAG}.txt 2>&1
+python scripts/sass_mix.py gpurun_out/prof_${CFG}_k_assa_forward_${TAG}.ncu-rep 268435456 > gpurun_out/ncu_sassmix_k_assa_forward_${TAG}.txt 2>&1
+[ -z "$KEEP_REP" ] && rm -f gpurun_out/prof_${CFG}_k_assa_forward_${TAG}.ncu-rep
 # the other bench lines: the reference arm (fp64 oracle), the ASSA operator, cfg5 / cfg3
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.log 2>&1
 timeout 600 python bench.py --op assa --no-cpu-baseline > gpurun_out/bench_assa_${TAG}.log 2>&1
