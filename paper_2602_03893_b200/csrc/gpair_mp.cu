@@ -320,10 +320,8 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
         if (cok) {
             const char* stage = s_M + s * sbytes;
             unsigned rmask = 0;
-#pragma unroll
-            for (int p = 0; p < MP_SB / 2; ++p) {
-                const unsigned lv = (live >> (2 * p)) & 3u;
-                if (!lv) continue;  // warp-uniform
+            // one step: the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1); lv = their live bits
+            auto step = [&](const int p, const unsigned lv) {
                 const float4 A0 = my_anc[4 * p], A1 = my_anc[4 * p + 1], A2 = my_anc[4 * p + 2], A3 = my_anc[4 * p + 3];
                 // fp32 time of flight of the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1) in f32x2
                 const f2_t q = fma2(pk2(A0.x, A0.y), kx, fma2(pk2(A0.z, A0.w), ky, fma2(pk2(A1.x, A1.y), kz, kw)));
@@ -393,6 +391,16 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                         acc = fma((double)w, pv, acc);
                     }
                 }
+                }
+            };
+            if (live == (1u << MP_SB) - 1u) {  // every sensor of the batch has a window here (common)
+#pragma unroll
+                for (int p = 0; p < MP_SB / 2; ++p) step(p, 3u);
+            } else {
+#pragma unroll
+                for (int p = 0; p < MP_SB / 2; ++p) {
+                    const unsigned lv = (live >> (2 * p)) & 3u;
+                    if (lv) step(p, lv);  // warp-uniform
                 }
             }
             if (ASSA) {
