@@ -1,0 +1,19 @@
+#!/bin/bash
+# 16-sensor batches in k_adjoint_mp (GPAIR_MP_SB=16: two anchor jobs per lane, half the per-batch
+# bookkeeping per pair): bounds-checked GPU tests on that build, then A/B timing against the default
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+(
+export GPAIR_LIB=libgpair_sb16c.so GPAIR_NVCC_FLAGS="-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=2 -DGPAIR_MP_CHECK=1"
+python paper_2602_03893_b200/build.py --force > /dev/null 2>&1 || { echo "build failed"; exit 1; }
+timeout 1200 python -m pytest tests/test_gpu_paths.py tests/test_gpu_parity.py tests/test_gpu_assa.py -q -x --timeout 900 > gpurun_out/pytest_sb16.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_sb16.log
+tail -2 gpurun_out/pytest_sb16.log
+)
+bash scripts/variants.sh "" "-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=2" "-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=3" "-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=3 -DGPAIR_MP_MINB=2" "" "-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=2" > gpurun_out/variants_sb16.txt 2>&1
+cat gpurun_out/variants_sb16.txt
+for V in "" "-DGPAIR_MP_SB=16 -DGPAIR_MP_NS=2"; do
+  export GPAIR_NVCC_FLAGS="$V"
+  python paper_2602_03893_b200/build.py --force > /dev/null 2>&1
+  R=$(timeout 600 python bench.py --op assa --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1)
+  echo "ASSA [$V] $(echo $R | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],2), {k: round(v,2) for k,v in d["roofline"]["kernel_ms"].items()})')" | tee -a gpurun_out/variants_sb16.txt
+done
