@@ -16,7 +16,8 @@
 // moments of every (sensor, start sample) in fp64 once per residual, stored as 32-B rows (degree 6:
 // M_0 fp64, M_1..M_6 fp32) or 48-B rows (degree 7: M_0..M_3 fp64, M_4..M_7 fp32); k_adjoint_mp then
 // pays per pair one fp32 time of flight (two-level anchors, gpair_internal.cuh), one row of M from
-// shared memory, an fp32 Horner tail and 2 (or 5) DFMA -- against the LCF kernel's 16-sample fp64
+// shared memory, an fp32 Horner tail and 1 (or 5) DFMA
+// (32-B rows: the tail w xi T is summed in fp32 over a batch) -- against the LCF kernel's 16-sample fp64
 // Horner chains and per-pair fp64 exponentials.  Ambiguous window edges (GAMMA band) and exact-ToF
 // groups take the oracle-exact window (pair_setup) and a per-sample fp64 sum over the residual.
 // The ASSA operator's adjoint (row f1) runs on the same kernel with 4-B rows of its dconv table.
@@ -40,7 +41,11 @@ namespace gpair {
 
 namespace {
 
-constexpr int MP_SB = 8;           // sensors per staged batch (one anchor per lane: 8 sensors x 4 groups)
+#ifndef GPAIR_MP_SB
+#define GPAIR_MP_SB 16
+#endif
+constexpr int MP_SB = GPAIR_MP_SB;  // sensors per staged batch (8 or 16)
+constexpr int MP_AJ = MP_SB / 8;    // anchor jobs per lane and batch (lane = 8 sensors x 4 groups)
 constexpr int MP_SG = 256;         // sensors per CTA (blockIdx.y = sensor group = gpart row)
 constexpr int32_t MP_EMPTY = INT_MIN;
 constexpr double MP_TOL = 1e-8;    // max interpolation error / max |f| accepted at create (W >= 10 at k = 3)
@@ -166,7 +171,7 @@ __global__ void k_mp_prep(const float* __restrict__ resid, const double* __restr
 // a step: the fp32 part of the fp64 anchor (make_anchor) with n_a folded into the start row of
 // the sensor's staged block, nrel = n_a - lo_j - (RND_MAGIC_BITS - 1) (NA_EXACT: exact path).
 // [group][pair of sensors]: {Ux, Uy} {Uz, Eu} {invR2, inv2Rh} {h2R, nrel}, each (s0, s1).
-constexpr int MP_ANC_GSTRIDE = (8 / 2) * 4 + 1;  // float4 slots per group (+1: 4 groups on distinct banks)
+constexpr int MP_ANC_GSTRIDE = (MP_SB / 2) * 4 + 1;  // float4 slots per group (+1: 4 groups on distinct banks)
 
 // Rare pair: the oracle-exact window (pair_setup: exact edges, exact-ToF anchors, record
 // clipping) and a per-sample fp64 sum over the residual row.
@@ -201,13 +206,19 @@ __device__ __noinline__ double mp_rare_assa(float4 G, float4 d4, const float* __
 }
 
 #ifndef GPAIR_MP_NS
-#define GPAIR_MP_NS 5
+#define GPAIR_MP_NS 2
 #endif
 constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mbarriers)
 
 #ifndef GPAIR_MP_MINB
 #define GPAIR_MP_MINB 3
 #endif
+#ifndef GPAIR_MP_TAILF32
+#define GPAIR_MP_TAILF32 1
+#endif
+// 32-B rows: the fp32 tail w xi T of a pair is summed in fp32 over the batch (MP_SB pairs) and folded into
+// the fp64 sum once per batch, so a pair costs one F2F + one DFMA (w M_0) instead of three + two
+constexpr bool MP_TAILF32 = GPAIR_MP_TAILF32 != 0;
 // LR > 0: compile-time slot stride (rows per sensor in a staged batch, >= Lr2), so every staged row
 // address is one add of an immediate; LR = 0: the runtime Lr2
 template <int SDEG, bool ASSA, bool R32, int LR>
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                  const float* __restrict__ sens, const int32_t* __restrict__ wlo, const char* __restrict__ Mt,
                  const float* __restrict__ resid, gacc_t* __restrict__ gpart, int32_t cpr, int32_t ncells,
                  int32_t Lr2, int32_t NtP, int32_t pad, int64_t Mpad, OpConst k, float xi0, double K64) {
-    static_assert(MP_SB == 8, "anchor layout: lane = (sensor lane % 8, group lane / 8)");
+    static_assert(MP_SB == 8 || MP_SB == 16, "anchor layout: lane = (sensor lane % 8 + 8 a, group lane / 8)");
     extern __shared__ double smem8[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int ROW = ASSA ? 4 : (R32 ? 32 : MP_ROW);             // bytes per staged row
@@ -274,20 +285,24 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     const f2_t alf = pk2((float)k.alpha, (float)k.alpha), half = pk2(0.5f, 0.5f), nhalf = pk2(-0.5f, -0.5f);
     const f2_t two_h = pk2(k.two_over_h, k.two_over_h);
     const float gam_a = 0.5f - GAMMA * (float)k.alpha;
-    float accf = 0.f;  // ASSA: per-batch fp32 sum (one gather per pair), folded into acc
+    float accf = 0.f;  // per-batch fp32 sum (ASSA: the pair values; 32-B rows: the tails), folded into acc
     // this lane's anchor job: sensor jj = lane % 8 of the batch, group gq = lane / 8 of the cell
-    const int ajj = lane & (MP_SB - 1), agq = lane >> 3;
+    // (MP_SB = 16: a second job for sensor ajj + 8, 16 float4 slots further)
+    const int ajj = lane & 7, agq = lane >> 3;
     float* aslot = (float*)(s_anc + (warp * GPC + agq) * MP_ANC_GSTRIDE + (ajj >> 1) * 4) + (ajj & 1);
-    int lo_n = MP_EMPTY;  // prefetched window start of the next batch's anchor job
-    float sxn = 0.f, syn = 0.f, szn = 0.f;
+    int lo_n[MP_AJ];  // prefetched window starts of the next batch's anchor jobs
+    float sxn[MP_AJ] = {}, syn[MP_AJ] = {}, szn[MP_AJ] = {};
     auto prefetch = [&](int b) {
-        const int jb = jg0 + b * MP_SB, j = jb + ajj;
-        lo_n = MP_EMPTY;
-        if (b < nb && j < jg1) {
-            lo_n = __ldg(wrow + j);
-            sxn = __ldg(sens + j);
-            syn = __ldg(sens + k.Nd + j);
-            szn = __ldg(sens + 2 * k.Nd + j);
+#pragma unroll
+        for (int a = 0; a < MP_AJ; ++a) {
+            const int j = jg0 + b * MP_SB + ajj + 8 * a;
+            lo_n[a] = MP_EMPTY;
+            if (b < nb && j < jg1) {
+                lo_n[a] = __ldg(wrow + j);
+                sxn[a] = __ldg(sens + j);
+                syn[a] = __ldg(sens + k.Nd + j);
+                szn[a] = __ldg(sens + 2 * k.Nd + j);
+            }
         }
     };
     prefetch(0);
@@ -298,22 +313,27 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
         const int s = b % MP_NS;
         const unsigned ph = (unsigned)(b / MP_NS) & 1u;
         __syncwarp();  // the previous batch's anchors are consumed
-        const int lo_l = lo_n;
-        if (cok && lo_l != MP_EMPTY) {
-            const Anchor a = make_anchor(Gq, sxn, syn, szn, k);
-            // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
-            const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
-                                  : a.na - (row0(lo_l) - (W - 1) - pad) - (RND_MAGIC_BITS - 1);
-            aslot[0] = a.Ux;
-            aslot[2] = a.Uy;
-            aslot[4] = a.Uz;
-            aslot[6] = a.Eu;
-            aslot[8] = a.invR2;
-            aslot[10] = a.inv2Rh;
-            aslot[12] = a.h2R;
-            aslot[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : nrel);
+        unsigned live = 0;
+#pragma unroll
+        for (int aj = 0; aj < MP_AJ; ++aj) {
+            const int lo_l = lo_n[aj];
+            if (cok && lo_l != MP_EMPTY) {
+                const Anchor a = make_anchor(Gq, sxn[aj], syn[aj], szn[aj], k);
+                // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
+                const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
+                                      : a.na - (row0(lo_l) - (W - 1) - pad) - (RND_MAGIC_BITS - 1);
+                float* as = aslot + 64 * aj;
+                as[0] = a.Ux;
+                as[2] = a.Uy;
+                as[4] = a.Uz;
+                as[6] = a.Eu;
+                as[8] = a.invR2;
+                as[10] = a.inv2Rh;
+                as[12] = a.h2R;
+                as[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : nrel);
+            }
+            live |= (__ballot_sync(0xffffffffu, lo_l != MP_EMPTY) & 0xFFu) << (8 * aj);
         }
-        const unsigned live = __ballot_sync(0xffffffffu, lo_l != MP_EMPTY) & ((1u << MP_SB) - 1u);
         prefetch(b + 1);
         __syncwarp();
         mbar_wait(bar + s, ph);
@@ -377,7 +397,12 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                         float tl = fmaf(fmaf(fmaf(q1.w, xi, q1.z), xi, q1.y), xi, q1.x);
                         tl = fmaf(fmaf(tl, xi, q0.w), xi, q0.z);
                         const double m0 = __hiloint2double(__float_as_int(q0.y), __float_as_int(q0.x));
-                        acc = fma((double)w, fma((double)tl, (double)xi, m0), acc);
+                        if (MP_TAILF32) {
+                            acc = fma((double)w, m0, acc);
+                            accf = fmaf(w * xi, tl, accf);
+                        } else {
+                            acc = fma((double)w, fma((double)tl, (double)xi, m0), acc);
+                        }
                     } else {
                         const double2 m01 = *(const double2*)rp;
                         const double2 m23 = *(const double2*)(rp + 16);
@@ -403,7 +428,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
                     if (lv) step(p, lv);  // warp-uniform
                 }
             }
-            if (ASSA) {
+            if (ASSA || (R32 && MP_TAILF32)) {
                 acc += (double)accf;
                 accf = 0.f;
             }
@@ -418,7 +443,7 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
             }
         }
         // the last warp done with stage s refills it with batch b + MP_NS (no producer convoy): lane 0
-        // arms the barrier, lanes 0..7 issue one sensor's rows each
+        // arms the barrier, lanes 0..MP_SB-1 issue one sensor's rows each
         __syncwarp();
         int last = 0;
         if (lane == 0) {
