@@ -219,6 +219,9 @@ constexpr int MP_NS = GPAIR_MP_NS;  // staged batches in flight (ring of full mb
 // 32-B rows: the fp32 tail w xi T of a pair is summed in fp32 over the batch (MP_SB pairs) and folded into
 // the fp64 sum once per batch, so a pair costs one F2F + one DFMA (w M_0) instead of three + two
 constexpr bool MP_TAILF32 = GPAIR_MP_TAILF32 != 0;
+#ifndef GPAIR_MP_STAGE_UNROLL
+#define GPAIR_MP_STAGE_UNROLL 1
+#endif
 // LR > 0: compile-time slot stride (rows per sensor in a staged batch, >= Lr2), so every staged row
 // address is one add of an immediate; LR = 0: the runtime Lr2
 template <int SDEG, bool ASSA, bool R32, int LR>
@@ -308,159 +311,167 @@ __global__ void __launch_bounds__(256, GPAIR_MP_MINB)
     prefetch(0);
     const float4 Gq = __ldg(grow + agq);
     double acc = 0.0;
-    for (int b = 0; b < nb; ++b) {
-        const int jb = jg0 + b * MP_SB;
-        const int s = b % MP_NS;
-        const unsigned ph = (unsigned)(b / MP_NS) & 1u;
-        __syncwarp();  // the previous batch's anchors are consumed
-        unsigned live = 0;
+    // the ring is walked MP_NS batches at a time; ASSA unrolls it so the stage index s is a
+    // compile-time constant (staged-row addresses = register + immediate; one-box A/B 15.24 -> 14.98 ms);
+    // the exact operator's larger body spills when unrolled (19.8 -> 23.3 ms, variants_unroll.txt)
+    constexpr int STAGE_UNROLL = (ASSA && GPAIR_MP_STAGE_UNROLL) ? MP_NS : 1;
+    for (int b0 = 0; b0 < nb; b0 += MP_NS) {
+#pragma unroll STAGE_UNROLL
+        for (int s = 0; s < MP_NS; ++s) {
+            const int b = b0 + s;
+            if (b >= nb) break;
+            const int jb = jg0 + b * MP_SB;
+            const unsigned ph = (unsigned)(b0 / MP_NS) & 1u;
+            __syncwarp();  // the previous batch's anchors are consumed
+            unsigned live = 0;
 #pragma unroll
-        for (int aj = 0; aj < MP_AJ; ++aj) {
-            const int lo_l = lo_n[aj];
-            if (cok && lo_l != MP_EMPTY) {
-                const Anchor a = make_anchor(Gq, sxn[aj], syn[aj], szn[aj], k);
-                // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
-                const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
-                                      : a.na - (row0(lo_l) - (W - 1) - pad) - (RND_MAGIC_BITS - 1);
-                float* as = aslot + 64 * aj;
-                as[0] = a.Ux;
-                as[2] = a.Uy;
-                as[4] = a.Uz;
-                as[6] = a.Eu;
-                as[8] = a.invR2;
-                as[10] = a.inv2Rh;
-                as[12] = a.h2R;
-                as[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : nrel);
+            for (int aj = 0; aj < MP_AJ; ++aj) {
+                const int lo_l = lo_n[aj];
+                if (cok && lo_l != MP_EMPTY) {
+                    const Anchor a = make_anchor(Gq, sxn[aj], syn[aj], szn[aj], k);
+                    // staged row = nrel + bits(t): n_lo - lo_j (exact) or k_ij - q0 (ASSA, q0 = first staged index)
+                    const int nrel = ASSA ? k.alpha * a.na - RND_MAGIC_BITS - (row0(lo_l) - pad)
+                                          : a.na - (row0(lo_l) - (W - 1) - pad) - (RND_MAGIC_BITS - 1);
+                    float* as = aslot + 64 * aj;
+                    as[0] = a.Ux;
+                    as[2] = a.Uy;
+                    as[4] = a.Uz;
+                    as[6] = a.Eu;
+                    as[8] = a.invR2;
+                    as[10] = a.inv2Rh;
+                    as[12] = a.h2R;
+                    as[14] = __int_as_float(a.na == NA_EXACT ? NA_EXACT : nrel);
+                }
+                live |= (__ballot_sync(0xffffffffu, lo_l != MP_EMPTY) & 0xFFu) << (8 * aj);
             }
-            live |= (__ballot_sync(0xffffffffu, lo_l != MP_EMPTY) & 0xFFu) << (8 * aj);
-        }
-        prefetch(b + 1);
-        __syncwarp();
-        mbar_wait(bar + s, ph);
-        if (cok) {
-            const char* stage = s_M + s * sbytes;
-            unsigned rmask = 0;
-            // one step: the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1); lv = their live bits
-            auto step = [&](const int p, const unsigned lv) {
-                const float4 A0 = my_anc[4 * p], A1 = my_anc[4 * p + 1], A2 = my_anc[4 * p + 2], A3 = my_anc[4 * p + 3];
-                // fp32 time of flight of the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1) in f32x2
-                const f2_t q = fma2(pk2(A0.x, A0.y), kx, fma2(pk2(A0.z, A0.w), ky, fma2(pk2(A1.x, A1.y), kz, kw)));
-                const f2_t eps = mul2(q, pk2(A2.x, A2.y));
-                f2_t S, Tw;
-                series2<SDEG>(eps, S, Tw);
-                const f2_t eu = fma2(mul2(q, pk2(A2.z, A2.w)), S, pk2(A1.z, A1.w));
-                if constexpr (ASSA) {
-                    // k_ij = alpha n_a + floor(alpha eu + 1/2), w = A / r (assa_pre's arithmetic, A = 1)
-                    const f2_t w2 = mul2(mul2(pk2(A3.x, A3.y), Tw), two_h);
-                    const f2_t xa = fma2(alf, eu, half);
-                    const f2_t t = add2(add2(xa, nhalf), mag);
-                    const f2_t fl = add2(t, nmag);
-                    const f2_t dd = sub2(sub2(xa, fl), half);
-                    float t0, t1, d0, d1, wa, wb;
+            prefetch(b + 1);
+            __syncwarp();
+            mbar_wait(bar + s, ph);
+            if (cok) {
+                const char* stage = s_M + s * sbytes;
+                unsigned rmask = 0;
+                // one step: the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1); lv = their live bits
+                auto step = [&](const int p, const unsigned lv) {
+                    const float4 A0 = my_anc[4 * p], A1 = my_anc[4 * p + 1], A2 = my_anc[4 * p + 2], A3 = my_anc[4 * p + 3];
+                    // fp32 time of flight of the pairs (kernel, sensor 2p) and (kernel, sensor 2p + 1) in f32x2
+                    const f2_t q = fma2(pk2(A0.x, A0.y), kx, fma2(pk2(A0.z, A0.w), ky, fma2(pk2(A1.x, A1.y), kz, kw)));
+                    const f2_t eps = mul2(q, pk2(A2.x, A2.y));
+                    f2_t S, Tw;
+                    series2<SDEG>(eps, S, Tw);
+                    const f2_t eu = fma2(mul2(q, pk2(A2.z, A2.w)), S, pk2(A1.z, A1.w));
+                    if constexpr (ASSA) {
+                        // k_ij = alpha n_a + floor(alpha eu + 1/2), w = A / r (assa_pre's arithmetic, A = 1)
+                        const f2_t w2 = mul2(mul2(pk2(A3.x, A3.y), Tw), two_h);
+                        const f2_t xa = fma2(alf, eu, half);
+                        const f2_t t = add2(add2(xa, nhalf), mag);
+                        const f2_t fl = add2(t, nmag);
+                        const f2_t dd = sub2(sub2(xa, fl), half);
+                        float t0, t1, d0, d1, wa, wb;
+                        upk2(t, t0, t1);
+                        upk2(dd, d0, d1);
+                        upk2(w2, wa, wb);
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            if (!((lv >> h) & 1u)) continue;  // warp-uniform
+                            const int row = (int)((unsigned)__float_as_int(h ? A3.w : A3.z) + (unsigned)__float_as_int(h ? t1 : t0));
+                            const bool rare = fabsf(h ? d1 : d0) > gam_a || (unsigned)row >= (unsigned)Lr2;
+                            rmask |= (unsigned)rare << (2 * p + h);
+                            const float dv = *(const float*)(stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * 4);
+                            accf = fmaf(rare ? 0.f : (h ? wb : wa), dv, accf);  // Eq. 17
+                        }
+                    } else {
+                    const f2_t w2 = mul2(pk2(A3.x, A3.y), Tw);
+                    const f2_t x = add2(eu, clo);  // alpha - 1/2, alpha = eu - ku
+                    const f2_t t = add2(x, mag);
+                    const f2_t fl = add2(t, nmag);  // floor(alpha) unless ambiguous
+                    const f2_t dd = sub2(x, fl);    // frac(alpha) - 1/2
+                    const f2_t xi2 = sub2(eu, add2(fl, c1x));  // u_lo - xi0 (exact)
+                    float t0, t1, d0, d1, xa, xb, wa, wb;
                     upk2(t, t0, t1);
                     upk2(dd, d0, d1);
+                    upk2(xi2, xa, xb);
                     upk2(w2, wa, wb);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         if (!((lv >> h) & 1u)) continue;  // warp-uniform
                         const int row = (int)((unsigned)__float_as_int(h ? A3.w : A3.z) + (unsigned)__float_as_int(h ? t1 : t0));
-                        const bool rare = fabsf(h ? d1 : d0) > gam_a || (unsigned)row >= (unsigned)Lr2;
+                        const bool rare = fabsf(h ? d1 : d0) > 0.5f - GAMMA || (unsigned)row >= (unsigned)Lr2;
                         rmask |= (unsigned)rare << (2 * p + h);
-                        const float dv = *(const float*)(stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * 4);
-                        accf = fmaf(rare ? 0.f : (h ? wb : wa), dv, accf);  // Eq. 17
-                    }
-                } else {
-                const f2_t w2 = mul2(pk2(A3.x, A3.y), Tw);
-                const f2_t x = add2(eu, clo);  // alpha - 1/2, alpha = eu - ku
-                const f2_t t = add2(x, mag);
-                const f2_t fl = add2(t, nmag);  // floor(alpha) unless ambiguous
-                const f2_t dd = sub2(x, fl);    // frac(alpha) - 1/2
-                const f2_t xi2 = sub2(eu, add2(fl, c1x));  // u_lo - xi0 (exact)
-                float t0, t1, d0, d1, xa, xb, wa, wb;
-                upk2(t, t0, t1);
-                upk2(dd, d0, d1);
-                upk2(xi2, xa, xb);
-                upk2(w2, wa, wb);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (!((lv >> h) & 1u)) continue;  // warp-uniform
-                    const int row = (int)((unsigned)__float_as_int(h ? A3.w : A3.z) + (unsigned)__float_as_int(h ? t1 : t0));
-                    const bool rare = fabsf(h ? d1 : d0) > 0.5f - GAMMA || (unsigned)row >= (unsigned)Lr2;
-                    rmask |= (unsigned)rare << (2 * p + h);
-                    const float xi = h ? xb : xa;
-                    const float w = rare ? 0.f : (h ? wb : wa);
-                    const char* rp = stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * ROW;
-                    if (R32) {  // M_0 fp64, M_1..M_6 fp32: the fp32 tail's terms are < 1/3 of the value
-                        const int sw = ((int)min((unsigned)row, (unsigned)Lr2 - 1u) >> 2 & 1) * 16;
-                        const float4 q0 = *(const float4*)(rp + sw);         // (M_0 lo, M_0 hi, M_1, M_2)
-                        const float4 q1 = *(const float4*)(rp + (16 ^ sw));  // M_3..M_6
-                        float tl = fmaf(fmaf(fmaf(q1.w, xi, q1.z), xi, q1.y), xi, q1.x);
-                        tl = fmaf(fmaf(tl, xi, q0.w), xi, q0.z);
-                        const double m0 = __hiloint2double(__float_as_int(q0.y), __float_as_int(q0.x));
-                        if (MP_TAILF32) {
-                            acc = fma((double)w, m0, acc);
-                            accf = fmaf(w * xi, tl, accf);
+                        const float xi = h ? xb : xa;
+                        const float w = rare ? 0.f : (h ? wb : wa);
+                        const char* rp = stage + ((2 * p + h) * LRS + min((unsigned)row, (unsigned)Lr2 - 1u)) * ROW;
+                        if (R32) {  // M_0 fp64, M_1..M_6 fp32: the fp32 tail's terms are < 1/3 of the value
+                            const int sw = ((int)min((unsigned)row, (unsigned)Lr2 - 1u) >> 2 & 1) * 16;
+                            const float4 q0 = *(const float4*)(rp + sw);         // (M_0 lo, M_0 hi, M_1, M_2)
+                            const float4 q1 = *(const float4*)(rp + (16 ^ sw));  // M_3..M_6
+                            float tl = fmaf(fmaf(fmaf(q1.w, xi, q1.z), xi, q1.y), xi, q1.x);
+                            tl = fmaf(fmaf(tl, xi, q0.w), xi, q0.z);
+                            const double m0 = __hiloint2double(__float_as_int(q0.y), __float_as_int(q0.x));
+                            if (MP_TAILF32) {
+                                acc = fma((double)w, m0, acc);
+                                accf = fmaf(w * xi, tl, accf);
+                            } else {
+                                acc = fma((double)w, fma((double)tl, (double)xi, m0), acc);
+                            }
                         } else {
-                            acc = fma((double)w, fma((double)tl, (double)xi, m0), acc);
+                            const double2 m01 = *(const double2*)rp;
+                            const double2 m23 = *(const double2*)(rp + 16);
+                            const float4 m47 = *(const float4*)(rp + 32);
+                            const float tl = fmaf(fmaf(fmaf(m47.w, xi, m47.z), xi, m47.y), xi, m47.x);
+                            const double X = (double)xi;
+                            double pv = fma((double)tl, X, m23.y);
+                            pv = fma(pv, X, m23.x);
+                            pv = fma(pv, X, m01.y);
+                            pv = fma(pv, X, m01.x);
+                            acc = fma((double)w, pv, acc);
                         }
-                    } else {
-                        const double2 m01 = *(const double2*)rp;
-                        const double2 m23 = *(const double2*)(rp + 16);
-                        const float4 m47 = *(const float4*)(rp + 32);
-                        const float tl = fmaf(fmaf(fmaf(m47.w, xi, m47.z), xi, m47.y), xi, m47.x);
-                        const double X = (double)xi;
-                        double pv = fma((double)tl, X, m23.y);
-                        pv = fma(pv, X, m23.x);
-                        pv = fma(pv, X, m01.y);
-                        pv = fma(pv, X, m01.x);
-                        acc = fma((double)w, pv, acc);
+                    }
+                    }
+                };
+                if (live == (1u << MP_SB) - 1u) {  // every sensor of the batch has a window here (common)
+#pragma unroll
+                    for (int p = 0; p < MP_SB / 2; ++p) step(p, 3u);
+                } else {
+#pragma unroll
+                    for (int p = 0; p < MP_SB / 2; ++p) {
+                        const unsigned lv = (live >> (2 * p)) & 3u;
+                        if (lv) step(p, lv);  // warp-uniform
                     }
                 }
+                if (ASSA || (R32 && MP_TAILF32)) {
+                    acc += (double)accf;
+                    accf = 0.f;
                 }
-            };
-            if (live == (1u << MP_SB) - 1u) {  // every sensor of the batch has a window here (common)
-#pragma unroll
-                for (int p = 0; p < MP_SB / 2; ++p) step(p, 3u);
-            } else {
-#pragma unroll
-                for (int p = 0; p < MP_SB / 2; ++p) {
-                    const unsigned lv = (live >> (2 * p)) & 3u;
-                    if (lv) step(p, lv);  // warp-uniform
+                while (rmask) {  // rare pairs of this batch (ambiguous edges / indices, exact-ToF groups)
+                    const int jj = __ffs(rmask) - 1;
+                    rmask &= rmask - 1u;
+                    if (ASSA)
+                        acc += mp_rare_assa<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, (const float*)Mt, NtP,
+                                                  pad, k);
+                    else
+                        acc += mp_rare<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, resid, k, K64);
                 }
             }
-            if (ASSA || (R32 && MP_TAILF32)) {
-                acc += (double)accf;
-                accf = 0.f;
+            // the last warp done with stage s refills it with batch b + MP_NS (no producer convoy): lane 0
+            // arms the barrier, lanes 0..MP_SB-1 issue one sensor's rows each
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = atomicAdd(s_done + s, 1) == nw - 1;
+                if (last) s_done[s] = 0;
             }
-            while (rmask) {  // rare pairs of this batch (ambiguous edges / indices, exact-ToF groups)
-                const int jj = __ffs(rmask) - 1;
-                rmask &= rmask - 1u;
-                if (ASSA)
-                    acc += mp_rare_assa<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, (const float*)Mt, NtP,
-                                              pad, k);
-                else
-                    acc += mp_rare<SDEG>(grow[lane >> 3], d4, orig, gi, Mpad, sens, jb + jj, resid, k, K64);
-            }
-        }
-        // the last warp done with stage s refills it with batch b + MP_NS (no producer convoy): lane 0
-        // arms the barrier, lanes 0..MP_SB-1 issue one sensor's rows each
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) {
-            __threadfence_block();
-            last = atomicAdd(s_done + s, 1) == nw - 1;
-            if (last) s_done[s] = 0;
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last && b + MP_NS < nb) {
-            const int jbn = jb + MP_NS * MP_SB, njn = min(MP_SB, jg1 - jbn);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (lane == 0) mbar_expect_tx(bar + s, (unsigned)njn * rowbytes);
-            if (lane < njn) {
-                const int ra0 = row0(__ldg(wrow + jbn + lane));
-                MP_CHECK(jbn + lane < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
-                tma_bulk_g2s(s_M + s * sbytes + lane * LRS * ROW, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
-                             rowbytes, bar + s);
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last && b + MP_NS < nb) {
+                const int jbn = jb + MP_NS * MP_SB, njn = min(MP_SB, jg1 - jbn);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (lane == 0) mbar_expect_tx(bar + s, (unsigned)njn * rowbytes);
+                if (lane < njn) {
+                    const int ra0 = row0(__ldg(wrow + jbn + lane));
+                    MP_CHECK(jbn + lane < k.Nd && ra0 >= 0 && ra0 + Lr2 <= NtP && (ra0 * ROW) % 16 == 0);
+                    tma_bulk_g2s(s_M + s * sbytes + lane * LRS * ROW, Mt + ((int64_t)(jbn + lane) * NtP + ra0) * ROW,
+                                 rowbytes, bar + s);
+                }
             }
         }
     }
